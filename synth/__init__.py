@@ -1,0 +1,152 @@
+"""Seeded synthetic INPUT generators shared by the oracle tests, the GPU parity
+tests and bench.py.
+
+This module holds none of the method's arithmetic: it only draws graphs,
+event schedules, datasets and initial models from numpy's seeded generators.
+The oracle (oracle/) and the CUDA path (paper_1710_06952_b200/) both consume
+what it returns; neither side's computation lives here.  Recipes are stated in
+DESIGN.md section "Input recipes" and follow the paper's workload shapes
+(ring of workers P:485-487, batch 32/128 P:853, ~1 MB / ~100 MB models
+P:781-783, Strategy-1 data P:386-388).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+EV_NO_GRAD = 1  # event flag: pure averaging (W_k only), no gradient
+
+
+def ring(n: int):
+    """Ring topology: edges (j, j+1 mod n); parity roles (0 active,
+    1 passive), bipartite iff n is even."""
+    if n < 1:
+        raise ValueError("n must be >= 1")
+    if n == 1:
+        return np.zeros((0, 2), np.int32), np.zeros(1, np.int8)
+    if n == 2:
+        return np.array([[0, 1]], np.int32), np.array([0, 1], np.int8)
+    e = np.array([[j, (j + 1) % n] for j in range(n)], np.int32)
+    role = (np.arange(n) % 2).astype(np.int8)
+    return e, role
+
+
+def skip_ring(n: int, odd_only: bool = True):
+    """Skip ring: sender j talks to j + 2^i + 1 (mod n) for
+    i = 0..floor(log2(n-1)) (reading c13).  odd_only keeps the offsets that
+    preserve the parity bipartition."""
+    if n < 3:
+        return ring(n)
+    offs = [2 ** i + 1 for i in range(int(np.floor(np.log2(n - 1))) + 1)]
+    offs = sorted({o % n for o in offs if o % n != 0})
+    if odd_only:
+        offs = [o for o in offs if o % 2 == 1]
+    E = set()
+    for j in range(n):
+        for o in offs:
+            a, b = j, (j + o) % n
+            if a != b:
+                E.add((min(a, b), max(a, b)))
+    e = np.array(sorted(E), np.int32).reshape(-1, 2)
+    role = (np.arange(n) % 2).astype(np.int8)
+    return e, role
+
+
+def neighbours(n: int, edges: np.ndarray):
+    nb = [[] for _ in range(n)]
+    for a, b in np.asarray(edges).reshape(-1, 2):
+        nb[int(a)].append(int(b))
+        nb[int(b)].append(int(a))
+    return [sorted(x) for x in nb]
+
+
+def schedule_iid(n, edges, K, T=0, seed=0, M=0, S=0, no_grad=False, tau=None,
+                 local_prob=0.0):
+    """Event schedule under law c4: i_k ~ U{0..n-1}, j_k ~ U(N(i_k)),
+    tau_k ~ U{0..min(k,T)} (or the fixed `tau`, clipped to k).  With
+    local_prob > 0 an event is a partner-less local update (j = -1) with that
+    probability.  Returns (events[K,4] int32 = (i, j, tau, flags),
+    batch_idx[K,M] int32 or None)."""
+    rng = np.random.default_rng(seed)
+    nb = neighbours(n, edges)
+    ev = np.zeros((K, 4), np.int32)
+    for k in range(K):
+        i = int(rng.integers(n))
+        if nb[i] and not (local_prob > 0 and rng.random() < local_prob):
+            j = nb[i][int(rng.integers(len(nb[i])))]
+        else:
+            j = -1
+        if tau is None:
+            t = int(rng.integers(min(k, T) + 1))
+        else:
+            t = min(int(tau), k)
+        ev[k] = (i, j, t, EV_NO_GRAD if no_grad else 0)
+    bidx = None
+    if M > 0 and S > 0:
+        bidx = rng.integers(0, S, size=(K, M), dtype=np.int64).astype(np.int32)
+    return ev, bidx
+
+
+def x0_uniform(n: int, d: int, seed: int = 7) -> np.ndarray:
+    """Per-worker initial models, values 2u-1 with u = m * 2^-24 exact in fp32
+    (pure-gossip tests only, reading c7)."""
+    rng = np.random.default_rng(seed)
+    m = rng.integers(0, 1 << 24, size=(n, d), dtype=np.int64)
+    return (m.astype(np.float64) * 2.0 ** -23 - 1.0).astype(np.float32)
+
+
+def lsq_data(S: int = 8192, d: int = 1024, seed: int = 1, noise: float = 0.01):
+    """Config 1: A ~ N(0, 1/d) fp32, x_true ~ N(0,1), b = A x_true + noise*N(0,1)."""
+    rng = np.random.default_rng(seed)
+    A = (rng.standard_normal((S, d)) / np.sqrt(d)).astype(np.float32)
+    xt = rng.standard_normal(d)
+    b = (A.astype(np.float64) @ xt + noise * rng.standard_normal(S)).astype(np.float32)
+    return A, b
+
+
+def logreg_data(S: int = 8192, d: int = 1024, seed: int = 2):
+    """Labels y = sign(a.w_true + 0.1 N(0,1)) in {-1,+1}, a ~ N(0, 1/d)."""
+    rng = np.random.default_rng(seed)
+    A = (rng.standard_normal((S, d)) / np.sqrt(d)).astype(np.float32)
+    w = rng.standard_normal(d)
+    z = A.astype(np.float64) @ w + 0.1 * rng.standard_normal(S)
+    y = np.where(z >= 0, 1.0, -1.0).astype(np.float32)
+    return A, y
+
+
+def mlp_data(S: int = 50000, n_in: int = 3072, n_out: int = 10, s: float = 0.02, seed: int = 3):
+    """Config 3: CIFAR-shaped synthetic data x = mu_y + N(0, I), mu_c ~ N(0, s^2 I)."""
+    rng = np.random.default_rng(seed)
+    mu = rng.standard_normal((n_out, n_in)) * s
+    y = rng.integers(0, n_out, size=S).astype(np.int32)
+    X = (mu[y] + rng.standard_normal((S, n_in))).astype(np.float32)
+    return X, y
+
+
+def mlp_init(n_in: int = 3072, n_hid: int = 512, n_out: int = 10, seed: int = 4) -> np.ndarray:
+    """He-uniform init, flat layout [W1 (hid x in) | b1 | W2 (out x hid) | b2]
+    (reading c18), identical for all workers."""
+    rng = np.random.default_rng(seed)
+    l1 = np.sqrt(6.0 / n_in)
+    l2 = np.sqrt(6.0 / n_hid)
+    W1 = rng.uniform(-l1, l1, (n_hid, n_in))
+    W2 = rng.uniform(-l2, l2, (n_out, n_hid))
+    return np.concatenate([W1.ravel(), np.zeros(n_hid), W2.ravel(), np.zeros(n_out)]).astype(np.float32)
+
+
+def quad_keys(seed: int = 11):
+    """Two u32 keys for the synthetic quadratic (data landscape, noise)."""
+    rng = np.random.default_rng(seed)
+    k = rng.integers(0, 1 << 32, size=2, dtype=np.uint64)
+    return int(k[0]), int(k[1])
+
+
+def stragglers(n: int, seed: int = 99, slow_worker: int | None = 0, slow: float = 10.0,
+               hetero: bool = False) -> np.ndarray:
+    """Per-worker slowdown factors s_w >= 1 (config 4: one worker 10x, P:1078-1081;
+    config 5: s_w = 10^u log-uniform in [1,10] plus worker 0 at 10x)."""
+    f = np.ones(n, np.float32)
+    if hetero:
+        f = (10.0 ** np.random.default_rng(seed).random(n)).astype(np.float32)
+    if slow_worker is not None and n > 0:
+        f[slow_worker] = slow
+    return f
