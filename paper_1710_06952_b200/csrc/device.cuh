@@ -1,0 +1,220 @@
+// device.cuh -- device-side building blocks of the AD-PSGD hot path (sm_100a).
+//
+// Shared by the standalone kernels (kernels.cu) and the persistent engine
+// (engine.cu).  Nothing here is shared with the CPU oracle (oracle/).
+//
+// Rounding (reading R6): every fp32 op of the update rule and of the
+// synthetic quadratic is an explicit round-to-nearest intrinsic (__fadd_rn,
+// __fmul_rn, __fsub_rn), which nvcc never contracts into FFMA; the library is
+// built without --use_fast_math, so no FTZ/DAZ.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace adp {
+
+constexpr int kMaxLocal = 128;        // workers per GPU engine (config 5 at 1 GPU: 128)
+constexpr uint32_t kStateIdle = 0, kStateClaimed = 1, kStateRunning = 2, kStateFinished = 3;
+
+// ------------------------------------------------------------ control words --
+// One per worker in its HOME GPU's control arena (peer-visible via CUDA IPC).
+struct alignas(128) WorkerCtl {
+  unsigned int lock;               // 0 free, 1 held (try-lock, system scope)
+  unsigned int epoch;              // committed events touching this worker (replay order)
+  unsigned long long updates;      // committed gradient updates made by this worker (p_i)
+  unsigned long long gossips;      // pair averages initiated by / applied to this worker
+  unsigned int pad[26];
+};
+static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
+
+// One per rank; rank 0's `ticket` is the system-wide virtual counter k.
+struct alignas(128) GlobalCtl {
+  unsigned long long ticket;       // next k to hand out
+  unsigned int error;              // latched device error (adpsgd_status code)
+  unsigned int error_info;
+  unsigned long long st_events, st_pair, st_cross;   // this rank's engine counters
+  unsigned long long st_busy_ns;
+  double st_bytes, st_nvl_bytes;
+  unsigned int abort_flag;
+  unsigned int pad[13];
+};
+
+struct LogEntry {                  // == adpsgd_log_entry
+  long long k;
+  int i, j, tau;
+  unsigned int flags;
+  unsigned long long t0, t1;
+};
+
+// Per-worker descriptor, one table per process: pointers valid in THIS process
+// (local device memory or IPC-mapped peer memory reached over NVLink).
+struct WorkerDesc {
+  float* x;                        // model row, d_pad floats
+  WorkerCtl* ctl;
+  int rank;                        // home rank
+  int role;                        // 0 active, 1 passive
+  int nb_off, nb_cnt;              // CSR neighbour range
+  float straggle;                  // slowdown factor s_w >= 1
+  int local;                       // index among this rank's workers, -1 if remote
+};
+
+// --------------------------------------------------------------- hashing ----
+// lowbias32 integer finaliser: defines the synthetic quadratic.
+__device__ __forceinline__ uint32_t lowbias32(uint32_t x) {
+  x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+  return x;
+}
+
+// Philox4x32-10 (Salmon et al. SC'11), used for batch sampling and neighbour choice.
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t lo0 = 0xD2511F53u * c.x, hi0 = __umulhi(0xD2511F53u, c.x);
+    const uint32_t lo1 = 0xCD9E8D57u * c.z, hi1 = __umulhi(0xCD9E8D57u, c.z);
+    c = make_uint4(hi1 ^ c.y ^ k.x, lo1, hi0 ^ c.w ^ k.y, lo0);
+    k.x += 0x9E3779B9u; k.y += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// ------------------------------------------------------- synthetic quadratic --
+// f(x) = 1/2 sum_c h_c (x_c - x*_c)^2; batch-SUM stochastic gradient
+//   g_c = fl(fl(M h_c) fl(xhat_c - x*_c)) + fl(s (2r-1))
+// with h_c, x*_c from lowbias32(c ^ data_key) and r from lowbias32(c ^ K_k),
+// K_k = lowbias32(lowbias32(lo(k) ^ noise_key) ^ hi(k)).
+struct QuadParams {
+  uint32_t data_key, noise_key;
+  float Mf, s;
+};
+
+__host__ __device__ __forceinline__ uint32_t quad_event_key_h(uint32_t noise_key, unsigned long long k) {
+  auto lb = [](uint32_t x) {
+    x ^= x >> 16; x *= 0x7feb352du; x ^= x >> 15; x *= 0x846ca68bu; x ^= x >> 16;
+    return x;
+  };
+  return lb(lb((uint32_t)k ^ noise_key) ^ (uint32_t)(k >> 32));
+}
+
+__device__ __forceinline__ float quad_grad(float xhat, uint32_t c, uint32_t data_key, uint32_t kk,
+                                           float Mf, float s) {
+  const uint32_t w = lowbias32(c ^ data_key);
+  const float uh = __fmul_rn(__uint2float_rn(w >> 16), 1.0f / 65536.0f);      // exact
+  const float h = __fadd_rn(0.01f, __fmul_rn(0.99f, uh));
+  const float xs = __fsub_rn(__fmul_rn(__uint2float_rn(w & 0xffffu), 1.0f / 32768.0f), 1.0f);
+  const uint32_t u = lowbias32(c ^ kk);
+  const float r = __fmul_rn(__uint2float_rn(u >> 8), 1.0f / 16777216.0f);     // exact
+  const float v = __fsub_rn(__fmul_rn(2.0f, r), 1.0f);                         // exact
+  const float noise = __fmul_rn(s, v);
+  const float det = __fmul_rn(__fmul_rn(Mf, h), __fsub_rn(xhat, xs));
+  return __fadd_rn(det, noise);
+}
+
+// --------------------------------------------------------- memory helpers ----
+// Model data is read through L2 (.cg): within one persistent launch a row is
+// rewritten by other SMs / other GPUs between events, so L1 must not serve it.
+__device__ __forceinline__ float4 ld_cg4(const float4* p) { return __ldcg(p); }
+__device__ __forceinline__ void st_cg4(float4* p, float4 v) { __stcg(p, v); }
+
+__device__ __forceinline__ unsigned int ld_acquire_gpu(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys64(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_gpu(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.gpu.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" :: "l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// -------------------------------------------------- the fused update tile ----
+// One float4 of the AD-PSGD event (Alg. 1 steps 4-6):
+//   m = fl(fl(x_i + x_j) * 0.5)   (pair only)
+//   x_j <- m
+//   x_i <- fl(m - fl(gamma * g))  (g from the quadratic at xhat, or external)
+enum GradMode { kGradNone = 0, kGradExternal = 1, kGradQuadInline = 2, kGradQuadSnapshot = 3 };
+
+template <bool kPair, int kGrad>
+__device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext, const float4 xh,
+                                        uint32_t c0, long long d, float gamma,
+                                        const QuadParams& q, uint32_t kk) {
+  float av[4] = {a.x, a.y, a.z, a.w};
+  const float bv[4] = {b.x, b.y, b.z, b.w};
+  const float gv[4] = {gext.x, gext.y, gext.z, gext.w};
+  const float hv[4] = {xh.x, xh.y, xh.z, xh.w};
+  float out[4], mv[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float xhat = (kGrad == kGradQuadInline) ? av[e] : hv[e];   // tau = 0: pre-average x_i
+    float m = av[e];
+    if (kPair) m = __fmul_rn(__fadd_rn(av[e], bv[e]), 0.5f);
+    mv[e] = m;
+    float res = m;
+    if (kGrad != kGradNone) {
+      float g;
+      if (kGrad == kGradExternal) g = gv[e];
+      else g = quad_grad(xhat, c0 + e, q.data_key, kk, q.Mf, q.s);
+      if ((long long)(c0 + e) >= d) g = 0.0f;                          // padding stays 0
+      res = __fsub_rn(m, __fmul_rn(gamma, g));
+    }
+    out[e] = res;
+  }
+  a = make_float4(out[0], out[1], out[2], out[3]);
+  if (kPair) b = make_float4(mv[0], mv[1], mv[2], mv[3]);
+}
+
+// Process float4 range [lo, hi) of one event with `nthreads` threads of a CTA.
+// Loads of the (possibly remote) partner row are issued first, U-deep, so that
+// NVLink latency overlaps the local HBM loads (SURVEY 8(a) sketch).
+template <bool kPair, int kGrad, int U>
+__device__ __forceinline__ void event_range(float4* __restrict__ xi4, float4* __restrict__ xj4,
+                                            const float4* __restrict__ g4,
+                                            const float4* __restrict__ xh4, long long lo,
+                                            long long hi, int tid, int nthreads, long long d,
+                                            float gamma, const QuadParams& q, uint32_t kk) {
+  for (long long base = lo + tid; base < hi; base += (long long)nthreads * U) {
+    float4 a[U], b[U], gg[U], hh[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) b[u] = gg[u] = hh[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long idx = base + (long long)u * nthreads;
+      if (kPair && idx < hi) b[u] = ld_cg4(xj4 + idx);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long idx = base + (long long)u * nthreads;
+      if (idx < hi) {
+        a[u] = ld_cg4(xi4 + idx);
+        if (kGrad == kGradExternal) gg[u] = ld_cg4(g4 + idx);
+        if (kGrad == kGradQuadSnapshot) hh[u] = ld_cg4(xh4 + idx);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const long long idx = base + (long long)u * nthreads;
+      if (idx < hi) {
+        update4<kPair, kGrad>(a[u], b[u], gg[u], hh[u], (uint32_t)(idx * 4), d, gamma, q, kk);
+        if (kPair) st_cg4(xj4 + idx, b[u]);
+        st_cg4(xi4 + idx, a[u]);
+      }
+    }
+  }
+}
+
+}  // namespace adp

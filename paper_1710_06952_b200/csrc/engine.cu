@@ -1,0 +1,286 @@
+// engine.cu -- the persistent AD-PSGD engine: one cooperative kernel per GPU
+// runs every local worker's loop of the wait-free runtime (App. A)
+// on the device, with no host round trip per event.
+//
+// Per local worker w, in free-running mode (mode 0):
+//   1. compute phase: emulated gradient time s_w * t_c (timer; no SM spinning)
+//   2. w active : pick j ~ U(N(w)), try-lock(j) at system scope
+//      w passive: try-lock(w)     (its local gradient flush)
+//      Only passives carry locks and every event takes exactly one, so no
+//      wait cycle can form -- the device form of the bipartite argument
+//      (P:458-479).  A failed try-lock leaves the worker pending; no CTA
+//      ever blocks on it.
+//   3. take ticket k (CAS on rank 0's counter, bounded by the run's target):
+//      the virtual counter of P:429-432, taken while holding the lock so the
+//      ticket order is the serialisation order (log replay).
+//   4. fused pass over d, split evenly across ALL CTAs of the grid:
+//      m = fl(fl(x_w + x_j)*0.5); x_j <- m (P2P store if remote);
+//      x_w <- fl(m - fl(gamma g)), g = quadratic gradient at the pre-average
+//      x_w (tau = 0) -- Alg. 1 steps 4-6, reading R1.
+//   5. the CTA finishing the last slice commits: log {k,i,j,0}, counters,
+//      release fence (sys), unlock, schedule the next compute phase.
+// Replay mode (mode 1): the event list of each local worker is consumed in
+// order; event k starts when epoch[i] == e_i(k) and epoch[j] == e_j(k) (device
+// epoch flags, system scope), and commits by bumping both epochs.
+#include "internal.h"
+
+namespace adp {
+
+namespace {
+
+constexpr int kEngineThreads = 512;
+constexpr int kEngineUnroll = 2;
+constexpr int kExit = -2;
+
+struct SmemSlot {                  // tid 0 copies the running event here for the CTA
+  float* xi;
+  float* xj;
+  long long k;
+  int grad;
+  int pair;
+};
+
+__device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
+
+__device__ void latch_error(const EngineParams& p, unsigned int code) {
+  atomicCAS(&p.gctl->error, 0u, code);
+  atomicExch(&p.gctl->abort_flag, 1u);
+}
+
+// ticket k = next value of rank 0's counter, if below target (free-running)
+__device__ __noinline__ bool take_ticket(const EngineParams& p, unsigned long long* k) {
+  unsigned long long t = ld_relaxed_sys64(&p.gctl0->ticket);
+  while (true) {
+    if (t >= p.target) return false;
+    const unsigned long long old = atomicCAS_system(&p.gctl0->ticket, t, t + 1);
+    if (old == t) { *k = t; return true; }
+    t = old;
+  }
+}
+
+__device__ void publish_running(Slot* sl, unsigned int seq) {
+  __threadfence();                                   // fields before the tag
+  st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
+}
+
+// Called by tid 0 of some CTA that found no slice to do.  Returns true if it
+// started or finished a worker (progress).
+__device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned int tag, unsigned long long now) {
+  Slot* sl = p.slots + s;
+  const unsigned int seq = tag >> 2;
+  if (p.mode == 0) {
+    // stop early if the system-wide budget is exhausted (straggler in compute)
+    if (ld_relaxed_sys64(&p.gctl0->ticket) >= p.target) {
+      if (atomicCAS(&sl->tag, tag, tag_of(seq, kStateClaimed)) != tag) return false;
+      st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
+      return true;
+    }
+    if (now < *(volatile unsigned long long*)&sl->ready_ns) return false;
+  }
+  if (atomicCAS(&sl->tag, tag, tag_of(seq, kStateClaimed)) != tag) return false;   // claim
+
+  const int w = p.local_ids[s];
+  const WorkerDesc dw = p.workers[w];
+  if (p.mode == 1) {
+    // ---------------------------------------------------------- replay ----
+    const long long cur = *(volatile long long*)&sl->ev_cur;
+    if (cur >= *(volatile long long*)&sl->ev_end) {
+      st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
+      return true;
+    }
+    const ReplayEv e = p.rev[cur];
+    const unsigned int ei = ld_acquire_sys(&dw.ctl->epoch);
+    unsigned int ej = 0;
+    WorkerCtl* cj = nullptr;
+    if (e.j >= 0) { cj = p.workers[e.j].ctl; ej = ld_acquire_sys(&cj->epoch); }
+    if (ei != e.e_i || (e.j >= 0 && ej != e.e_j)) {        // predecessors not committed yet
+      st_release_gpu(&sl->tag, tag);
+      return false;
+    }
+    __threadfence_system();                                 // acquire their data
+    sl->i = w; sl->j = e.j; sl->tau = 0; sl->flags = e.flags; sl->k = e.k;
+    sl->xi = dw.x; sl->xj = e.j >= 0 ? p.workers[e.j].x : nullptr;
+    sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
+    sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
+    sl->ev_cur = cur + 1;
+    sl->t0 = now;
+    sl->done = 0;
+    publish_running(sl, seq);
+    return true;
+  }
+  // ------------------------------------------------------- free-running ----
+  int j = -1;
+  unsigned int* lock;
+  if (dw.role == 0 && dw.nb_cnt > 0) {
+    j = sl->pending_j;
+    if (j < -1) {
+      const uint4 r = philox4x32_10(make_uint4((uint32_t)w, sl->nb_ctr, 0x4E424F52u, 0u), p.seed);
+      j = p.nbrs[dw.nb_off + (int)(((unsigned long long)r.x * (unsigned)dw.nb_cnt) >> 32)];
+      sl->pending_j = j;
+    }
+    lock = &p.workers[j].ctl->lock;
+  } else {                                                  // passive (or isolated): local update
+    if (p.model == 0) {                                     // pure gossip: passives only serve
+      st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
+      return true;
+    }
+    lock = &dw.ctl->lock;
+  }
+  if (atomicCAS_system(lock, 0u, 1u) != 0u) {              // busy: stay pending, never block
+    st_release_gpu(&sl->tag, tag);
+    return false;
+  }
+  __threadfence_system();                                   // acquire the previous holder's data
+  unsigned long long k;
+  if (!take_ticket(p, &k)) {
+    __threadfence_system();
+    atomicExch_system(lock, 0u);
+    st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
+    return true;
+  }
+  sl->i = w; sl->j = j; sl->tau = 0; sl->flags = p.model == 0 ? 1u : 0u; sl->k = (long long)k;
+  sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
+  sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
+  sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
+  sl->pending_j = -2;
+  sl->nb_ctr += 1;
+  sl->t0 = now;
+  sl->done = 0;
+  publish_running(sl, seq);
+  return true;
+}
+
+// Called by tid 0 of the CTA that finished the last slice of slot s.
+__device__ __noinline__ void commit(const EngineParams& p, int s) {
+  Slot* sl = p.slots + s;
+  __threadfence_system();                 // every slice's stores (fenced by their CTAs) first
+  const unsigned long long now = globaltimer();
+  const int i = sl->i, j = sl->j;
+  const unsigned int flags = sl->flags;
+  const long long k = sl->k;
+  const bool grad = !(flags & 1u) && p.model != 0;
+  if (grad) atomicAdd(&sl->ctl_i->updates, 1ull);
+  if (j >= 0) atomicAdd(&sl->ctl_i->gossips, 1ull);
+  // event log (rank 0's ring; a P2P store when this rank is not 0)
+  LogEntry* le = p.log + (k % p.log_cap);
+  le->k = k; le->i = i; le->j = j; le->tau = sl->tau; le->flags = flags;
+  le->t0 = sl->t0; le->t1 = now;
+  // stats: algorithmic bytes: pair 16d, local 8d; NVLink 8d per cross pair
+  const double d4 = 4.0 * (double)p.d;
+  atomicAdd(&p.gctl->st_events, 1ull);
+  if (j >= 0) atomicAdd(&p.gctl->st_pair, 1ull);
+  if (sl->cross) { atomicAdd(&p.gctl->st_cross, 1ull); atomicAdd(&p.gctl->st_nvl_bytes, 2.0 * d4); }
+  atomicAdd(&p.gctl->st_bytes, (j >= 0 ? 4.0 : (grad ? 2.0 : 0.0)) * d4);
+  atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
+  __threadfence_system();                 // log + data before the release below
+  if (p.mode == 1) {
+    atomicAdd_system(&sl->ctl_i->epoch, 1u);
+    if (j >= 0) atomicAdd_system(&sl->ctl_j->epoch, 1u);
+    atomicAdd_system(&p.gctl0->ticket, 1ull);
+  } else {
+    atomicExch_system(sl->lock, 0u);
+    const float sw = p.workers[i].straggle;
+    sl->ready_ns = now + (unsigned long long)((double)sw * (double)p.compute_ns);
+  }
+  const unsigned int seq = sl->tag >> 2;
+  st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
+}
+
+template <bool kPair, int kGrad>
+__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e) {
+  const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = lo + per < p.n4 ? lo + per : p.n4;
+  const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
+  event_range<kPair, kGrad, kEngineUnroll>(reinterpret_cast<float4*>(e.xi),
+                                           reinterpret_cast<float4*>(e.xj), nullptr, nullptr, lo,
+                                           hi, threadIdx.x, blockDim.x, p.d, p.gamma, p.q, kk);
+}
+
+__global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_constant__ EngineParams p) {
+  __shared__ unsigned int done_seq[kMaxLocal];
+  __shared__ int s_pick;
+  __shared__ unsigned int s_seq;
+  __shared__ SmemSlot s_ev;
+  for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) done_seq[s] = 0u;
+  __syncthreads();
+  const int L = p.n_local;
+  const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
+  unsigned long long last_progress = globaltimer();
+  while (true) {
+    if (threadIdx.x == 0) {
+      int pick = -1;
+      if (ld_acquire_gpu(&p.gctl->abort_flag)) pick = kExit;
+      for (int t = 0; t < L && pick == -1; ++t) {
+        const int s = (t + rot) % L;
+        const unsigned int tag = ld_acquire_gpu(&p.slots[s].tag);
+        if ((tag & 3u) == kStateRunning && (tag >> 2) != done_seq[s]) {
+          pick = s;
+          s_seq = tag >> 2;
+          Slot* sl = p.slots + s;
+          s_ev.xi = *(float* volatile*)&sl->xi;
+          s_ev.xj = *(float* volatile*)&sl->xj;
+          s_ev.k = *(volatile long long*)&sl->k;
+          const unsigned int fl = *(volatile unsigned int*)&sl->flags;
+          s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+          s_ev.pair = s_ev.xj != nullptr;
+        }
+      }
+      if (pick == -1) {
+        const unsigned long long now = globaltimer();
+        int n_fin = 0;
+        bool progress = false;
+        for (int t = 0; t < L; ++t) {
+          const int s = (t + rot) % L;
+          const unsigned int tag = ld_acquire_gpu(&p.slots[s].tag);
+          const unsigned int st = tag & 3u;
+          if (st == kStateFinished) ++n_fin;
+          else if (st == kStateIdle) progress |= try_start(p, s, tag, now);
+        }
+        if (n_fin == L) pick = kExit;
+        if (progress) last_progress = now;
+        else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
+      } else {
+        last_progress = globaltimer();
+      }
+      s_pick = pick;
+    }
+    __syncthreads();
+    const int pick = s_pick;
+    if (pick == kExit) break;
+    if (pick >= 0) {
+      const SmemSlot e = s_ev;
+      if (e.pair) {
+        if (e.grad) slice<true, kGradQuadInline>(p, e);
+        else slice<true, kGradNone>(p, e);
+      } else if (e.grad) {
+        slice<false, kGradQuadInline>(p, e);
+      }
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        done_seq[pick] = s_seq;
+        __threadfence_system();           // this CTA's slice (incl. P2P stores) is visible
+        if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) commit(p, pick);
+      }
+    } else if (threadIdx.x == 0) {
+      __nanosleep(256);
+    }
+    __syncthreads();
+  }
+}
+
+}  // namespace
+
+int engine_max_ctas_per_sm(int threads) {
+  int n = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine, threads, 0);
+  return n;
+}
+
+cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s) {
+  EngineParams pp = p;
+  void* args[] = {&pp};
+  return cudaLaunchCooperativeKernel((const void*)k_engine, dim3(grid), dim3(threads), args, 0, s);
+}
+
+}  // namespace adp

@@ -1,0 +1,106 @@
+// internal.h -- host-side declarations shared by the runtime (runtime.cu) and
+// the kernel translation units (kernels.cu, engine.cu).  Not part of the ABI.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include "device.cuh"
+
+namespace adp {
+
+// --------------------------------------------------------------- engine ----
+struct Slot {                      // per local worker, in local device memory
+  unsigned int tag;                // (seq << 2) | state
+  unsigned int done;               // CTAs finished with the current event
+  int i, j;
+  int tau;
+  unsigned int flags;
+  long long k;
+  float* xi;
+  float* xj;
+  WorkerCtl* ctl_i;
+  WorkerCtl* ctl_j;                // partner's control (local or peer), null if none
+  unsigned int* lock;              // lock word held by the running event (free-running)
+  unsigned long long ready_ns;     // compute phase ends (free-running)
+  unsigned long long t0;
+  unsigned int nb_ctr;             // neighbour-choice counter (free-running)
+  int pending_j;                   // chosen partner awaiting its lock; -2 none
+  long long ev_cur, ev_end;        // replay cursor into ReplayEv list
+  int cross;                       // partner lives on another rank
+  int pad[5];
+};
+
+struct ReplayEv {                  // one schedule event owned by this rank (i local)
+  long long k;
+  int j;
+  unsigned int flags;
+  unsigned int e_i, e_j;           // required epochs of i and j before the event
+};
+
+struct EngineParams {
+  const WorkerDesc* workers;
+  const int* nbrs;
+  int n;
+  int n_local;
+  Slot* slots;
+  const int* local_ids;            // n_local global ids
+  GlobalCtl* gctl0;                // rank 0's GlobalCtl (ticket, log owner)
+  GlobalCtl* gctl;                 // this rank's GlobalCtl (error, stats)
+  LogEntry* log;                   // rank 0's log ring (peer-mapped on other ranks)
+  long long log_cap;
+  unsigned long long target;       // free-running: stop when ticket reaches it
+  int mode;                        // 0 free-running, 1 replay
+  int model;                       // adpsgd_model_kind (NONE / QUADRATIC)
+  int my_rank;
+  const ReplayEv* rev;
+  QuadParams q;
+  float gamma;
+  long long d;                     // real dimension
+  long long n4;                    // d_pad / 4
+  long long compute_ns;
+  uint2 seed;
+  unsigned long long watchdog_ns;
+};
+
+cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);
+int engine_max_ctas_per_sm(int threads);
+
+// ---------------------------------------------------- standalone kernels ----
+// Pair/local update with external, inline-quadratic, snapshot-quadratic or no gradient.
+cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat, long long d,
+                         long long n4, float gamma, const QuadParams& q, unsigned long long k,
+                         int grad_mode, cudaStream_t s);
+cudaError_t launch_quad_grad(const float* xhat, float* g, long long d, long long n4,
+                             const QuadParams& q, unsigned long long k, cudaStream_t s);
+// lsq (kind 3) / logreg (kind 4): g = sum_m grad F(xhat; (A[idx_m], b[idx_m]))
+cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, const int* idx,
+                               int M, uint2 batch_key, unsigned long long k, const float* xhat,
+                               float* g, long long d, cudaStream_t s);
+cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s);
+cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,
+                                 double* sum, cudaStream_t s);
+cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out,
+                                      cudaStream_t s);
+cudaError_t launch_consensus_mk(const float* X, int n_rows, long long d_pad, long long d,
+                                const double* sum, int n, double* acc, cudaStream_t s);
+cudaError_t launch_ar_grad_sum(const float* x, float* gsum, long long d, long long n4,
+                               const QuadParams& q, unsigned long long k_base, int n_local,
+                               const int* local_ids, cudaStream_t s);
+// bookkeeping of a host-path event: ticket = max(ticket, k+1), updates/gossips++, log entry
+cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
+                               long long k, int i, int j, unsigned int flags, int grad,
+                               cudaStream_t s);
+cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
+cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, long long d,
+                             long long n4, cudaStream_t s);
+cudaError_t launch_delay(unsigned long long ns, cudaStream_t s);
+cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d, const float* x0,
+                             cudaStream_t s);
+
+// MLP (kind 5): tcgen05-backed gradient (mlp.cu)
+struct MlpShape { int n_in, n_hid, n_out; };
+cudaError_t launch_mlp_grad(const MlpShape& sh, const float* X, const int* y, int S,
+                            const int* idx, int M, uint2 batch_key, unsigned long long k,
+                            const float* w, float* g, float* scratch, cudaStream_t s);
+size_t mlp_scratch_floats(const MlpShape& sh, int M);
+
+}  // namespace adp

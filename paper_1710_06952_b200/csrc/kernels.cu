@@ -1,0 +1,342 @@
+// kernels.cu -- standalone (stream-ordered) kernels of the AD-PSGD hot path.
+//
+// Used by the host executor (adpsgd_replay HOST, adpsgd_step, adpsgd_gossip),
+// the consensus output and the AllReduce-SGD baseline.
+// The persistent free-running/replay engine lives in engine.cu and reuses the
+// same per-float4 update (device.cuh: event_range / update4).
+#include "internal.h"
+
+namespace adp {
+
+namespace {
+
+constexpr int kThreads = 512;
+constexpr int kUnroll = 4;
+
+int sm_count() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
+}
+
+// grid sized to whole waves of the 148 SMs (2 CTAs/SM of 512 threads)
+int stream_grid(long long n4) {
+  long long want = (n4 + (long long)kThreads * kUnroll - 1) / ((long long)kThreads * kUnroll);
+  long long cap = 2LL * sm_count();
+  if (want < 1) want = 1;
+  return (int)(want < cap ? want : cap);
+}
+
+// ----------------------------------------------------------- event pass ----
+// Each CTA takes a contiguous slice of the float4 range (DRAM-page friendly).
+template <bool kPair, int kGrad>
+__global__ void __launch_bounds__(kThreads, 2) k_event(float* xi, float* xj, const float* g,
+                                                    const float* xhat, long long d, long long n4,
+                                                    float gamma, QuadParams q, uint32_t kk) {
+  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long long lo = (long long)blockIdx.x * per;
+  const long long hi = lo + per < n4 ? lo + per : n4;
+  event_range<kPair, kGrad, kUnroll>(reinterpret_cast<float4*>(xi), reinterpret_cast<float4*>(xj),
+                                     reinterpret_cast<const float4*>(g),
+                                     reinterpret_cast<const float4*>(xhat), lo, hi,
+                                     threadIdx.x, blockDim.x, d, gamma, q, kk);
+}
+
+__global__ void __launch_bounds__(kThreads) k_quad_grad(const float* __restrict__ xhat,
+                                                        float* __restrict__ g, long long d,
+                                                        long long n4, QuadParams q, uint32_t kk) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 x = ld_cg4(reinterpret_cast<const float4*>(xhat) + i);
+    const float xv[4] = {x.x, x.y, x.z, x.w};
+    float gv[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t c = (uint32_t)(i * 4 + e);
+      gv[e] = (long long)c < d ? quad_grad(xv[e], c, q.data_key, kk, q.Mf, q.s) : 0.0f;
+    }
+    st_cg4(reinterpret_cast<float4*>(g) + i, make_float4(gv[0], gv[1], gv[2], gv[3]));
+  }
+}
+
+// ----------------------------------------------- lsq / logreg gradient -----
+// One CTA per event (d ~ 1024, M ~ 32).  Phase 1: each warp
+// forms r_m = a_m . xhat (fp32, lane-strided partial sums + shuffle tree) and
+// the per-sample coefficient (lsq: r - b; logreg: -y sigma(-y r)).  Phase 2:
+// g_c = sum_m coef_m a_{m,c}, each thread owning columns.
+constexpr int kLinThreads = 256;
+constexpr int kMaxM = 1024;
+
+__device__ __forceinline__ int32_t batch_index(uint2 key, unsigned long long k, uint32_t m, int S) {
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)k, m, 0x42415443u, 0u), key);
+  return (int32_t)(((unsigned long long)o.x * (unsigned long long)(uint32_t)S) >> 32);
+}
+
+__global__ void __launch_bounds__(kLinThreads) k_linear_grad(int kind, const float* __restrict__ A,
+                                                             const float* __restrict__ b, int S,
+                                                             const int* __restrict__ idx_in, int M,
+                                                             uint2 key, unsigned long long k,
+                                                             const float* __restrict__ xhat,
+                                                             float* __restrict__ g, long long d) {
+  __shared__ float coef[kMaxM];
+  __shared__ int sidx[kMaxM];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int m = threadIdx.x; m < M; m += blockDim.x)
+    sidx[m] = idx_in ? idx_in[m] : batch_index(key, k, (uint32_t)m, S);
+  __syncthreads();
+  for (int m = warp; m < M; m += nw) {
+    const float* a = A + (long long)sidx[m] * d;
+    float acc = 0.0f;
+    for (long long c = lane; c < d; c += 32) acc = fmaf(a[c], __ldcg(xhat + c), acc);
+#pragma unroll
+    for (int o = 16; o; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const float bm = b[sidx[m]];
+      if (kind == 3) {
+        coef[m] = acc - bm;
+      } else {
+        const float z = -bm * acc;                       // -y a.x
+        coef[m] = -bm / (1.0f + expf(-z));               // -y sigma(-y a.x)
+      }
+    }
+  }
+  __syncthreads();
+  for (long long c = threadIdx.x; c < d; c += blockDim.x) {
+    float acc = 0.0f;
+    for (int m = 0; m < M; ++m) acc = fmaf(coef[m], A[(long long)sidx[m] * d + c], acc);
+    g[c] = acc;
+  }
+}
+
+__global__ void k_copy(float4* __restrict__ dst, const float4* __restrict__ src, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x)
+    st_cg4(dst + i, ld_cg4(src + i));
+}
+
+// ------------------------------------------------------ consensus output ---
+// sum[c] = sum over rows of X[r][c] in fp64 (reading: fp64 accumulation)
+__global__ void k_consensus_sum(const float* __restrict__ X, int n_rows, long long d_pad,
+                                long long d, double* __restrict__ sum) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n_rows; ++r) s += (double)__ldcg(X + (long long)r * d_pad + c);
+    sum[c] = s;
+  }
+}
+
+__global__ void k_consensus_finalize(const double* __restrict__ sum, int n, long long d,
+                                     float* __restrict__ out) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x)
+    out[c] = __double2float_rn(__ddiv_rn(sum[c], (double)n));
+}
+
+// M_k partial: sum over local rows and coordinates of (mean - x)^2, fp64
+__global__ void k_consensus_mk(const float* __restrict__ X, int n_rows, long long d_pad, long long d,
+                               const double* __restrict__ sum, int n, double* acc) {
+  double part = 0.0;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x) {
+    const double mean = sum[c] / (double)n;
+    for (int r = 0; r < n_rows; ++r) {
+      const double e = mean - (double)__ldcg(X + (long long)r * d_pad + c);
+      part += e * e;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(acc, v);
+  }
+}
+
+// ---------------------------------------------------- AllReduce-SGD baseline
+// gsum[c] = sum over this rank's workers w of g_c(x; event k_base + w_global)
+__global__ void __launch_bounds__(kThreads) k_ar_grad_sum(const float* __restrict__ x,
+                                                          float* __restrict__ gsum, long long d,
+                                                          long long n4, QuadParams q,
+                                                          unsigned long long k_base, int n_local,
+                                                          const int* __restrict__ local_ids) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 xv4 = ld_cg4(reinterpret_cast<const float4*>(x) + i);
+    const float xv[4] = {xv4.x, xv4.y, xv4.z, xv4.w};
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    for (int w = 0; w < n_local; ++w) {
+      const uint32_t kk = quad_event_key_h(q.noise_key, k_base + (unsigned long long)local_ids[w]);
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t c = (uint32_t)(i * 4 + e);
+        if ((long long)c < d) acc[e] = __fadd_rn(acc[e], quad_grad(xv[e], c, q.data_key, kk, q.Mf, q.s));
+      }
+    }
+    st_cg4(reinterpret_cast<float4*>(gsum) + i, make_float4(acc[0], acc[1], acc[2], acc[3]));
+  }
+}
+
+// x <- fl(x - fl(gamma * fl(gsum / n)))   (reading R12: mean of the gradients)
+__global__ void __launch_bounds__(kThreads) k_ar_update(float* __restrict__ x,
+                                                        const float* __restrict__ gsum, float gamma,
+                                                        int n, long long d, long long n4) {
+  const float nf = (float)n;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    float4 xv = ld_cg4(reinterpret_cast<const float4*>(x) + i);
+    const float4 gv = ld_cg4(reinterpret_cast<const float4*>(gsum) + i);
+    float xa[4] = {xv.x, xv.y, xv.z, xv.w};
+    const float ga[4] = {gv.x, gv.y, gv.z, gv.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if ((long long)(i * 4 + e) < d) xa[e] = __fsub_rn(xa[e], __fmul_rn(gamma, __fdiv_rn(ga[e], nf)));
+    st_cg4(reinterpret_cast<float4*>(x) + i, make_float4(xa[0], xa[1], xa[2], xa[3]));
+  }
+}
+
+// straggler / emulated-compute delay: one thread spins on %globaltimer
+__global__ void k_delay(unsigned long long ns) {
+  const unsigned long long t0 = globaltimer();
+  while (globaltimer() - t0 < ns) __nanosleep(1000);
+}
+
+__global__ void k_init_rows(float* X, int n_rows, long long d_pad, long long d, const float* x0) {
+  const long long tot = (long long)n_rows * d_pad;
+  for (long long t = blockIdx.x * (long long)blockDim.x + threadIdx.x; t < tot;
+       t += (long long)gridDim.x * blockDim.x) {
+    const long long c = t % d_pad;
+    X[t] = (c < d && x0) ? x0[c] : 0.0f;
+  }
+}
+
+__global__ void k_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
+                              long long k, int i, int j, unsigned int flags, int grad) {
+  atomicMax(&gctl0->ticket, (unsigned long long)(k + 1));
+  if (grad) atomicAdd(&ctl_i->updates, 1ull);
+  if (j >= 0) atomicAdd(&ctl_i->gossips, 1ull);
+  if (log) {
+    const unsigned long long t = globaltimer();
+    LogEntry* e = log + (k % log_cap);
+    e->k = k; e->i = i; e->j = j; e->tau = 0; e->flags = flags; e->t0 = t; e->t1 = t;
+  }
+}
+
+__global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
+
+template <bool P, int G>
+cudaError_t ev(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
+               float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s) {
+  k_event<P, G><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat, long long d,
+                         long long n4, float gamma, const QuadParams& q, unsigned long long k,
+                         int grad_mode, cudaStream_t s) {
+  const uint32_t kk = quad_event_key_h(q.noise_key, k);
+  const bool pair = xj != nullptr;
+  switch (grad_mode) {
+    case kGradNone:
+      return pair ? ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
+                  : cudaSuccess;
+    case kGradExternal:
+      return pair ? ev<true, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
+                  : ev<false, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+    case kGradQuadInline:
+      return pair ? ev<true, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
+                  : ev<false, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+    case kGradQuadSnapshot:
+      return pair ? ev<true, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
+                  : ev<false, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+cudaError_t launch_quad_grad(const float* xhat, float* g, long long d, long long n4,
+                             const QuadParams& q, unsigned long long k, cudaStream_t s) {
+  k_quad_grad<<<stream_grid(n4), kThreads, 0, s>>>(xhat, g, d, n4, q, quad_event_key_h(q.noise_key, k));
+  return cudaGetLastError();
+}
+
+cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, const int* idx,
+                               int M, uint2 batch_key, unsigned long long k, const float* xhat,
+                               float* g, long long d, cudaStream_t s) {
+  if (M > kMaxM) return cudaErrorInvalidValue;
+  k_linear_grad<<<1, kLinThreads, 0, s>>>(kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s) {
+  k_copy<<<stream_grid(n4), kThreads, 0, s>>>(reinterpret_cast<float4*>(dst),
+                                              reinterpret_cast<const float4*>(src), n4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,
+                                 double* sum, cudaStream_t s) {
+  k_consensus_sum<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, sum);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out,
+                                      cudaStream_t s) {
+  k_consensus_finalize<<<4 * sm_count(), 256, 0, s>>>(sum, n, d, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_consensus_mk(const float* X, int n_rows, long long d_pad, long long d,
+                                const double* sum, int n, double* acc, cudaStream_t s) {
+  k_consensus_mk<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, sum, n, acc);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ar_grad_sum(const float* x, float* gsum, long long d, long long n4,
+                               const QuadParams& q, unsigned long long k_base, int n_local,
+                               const int* local_ids, cudaStream_t s) {
+  k_ar_grad_sum<<<stream_grid(n4), kThreads, 0, s>>>(x, gsum, d, n4, q, k_base, n_local, local_ids);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, long long d,
+                             long long n4, cudaStream_t s) {
+  k_ar_update<<<stream_grid(n4), kThreads, 0, s>>>(x, gsum, gamma, n, d, n4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
+                               long long k, int i, int j, unsigned int flags, int grad,
+                               cudaStream_t s) {
+  k_step_commit<<<1, 1, 0, s>>>(gctl0, ctl_i, log, log_cap, k, i, j, flags, grad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
+  k_set_u64<<<1, 1, 0, s>>>(p, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_delay(unsigned long long ns, cudaStream_t s) {
+  k_delay<<<1, 1, 0, s>>>(ns);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d, const float* x0,
+                             cudaStream_t s) {
+  k_init_rows<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, x0);
+  return cudaGetLastError();
+}
+
+}  // namespace adp

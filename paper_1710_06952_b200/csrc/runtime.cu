@@ -1,0 +1,1045 @@
+// runtime.cu -- host runtime behind the C ABI (include/adpsgd.h).
+//
+// Owns placement, device memory, CUDA IPC peer mapping over NVLink, the NCCL
+// communicator, the host executor (stream-ordered replay / step / gossip) and
+// the launch of the persistent engine.  No exception crosses the ABI.
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include <nccl.h>
+
+#include "../../include/adpsgd.h"
+#include "internal.h"
+
+using namespace adp;
+
+static_assert(sizeof(adpsgd_log_entry) == sizeof(LogEntry), "log entry layout");
+
+namespace {
+
+thread_local std::string g_err;
+
+adpsgd_status fail(adpsgd_status s, const std::string& m) {
+  g_err = m;
+  return s;
+}
+
+#define CU(x)                                                                          \
+  do {                                                                                 \
+    cudaError_t e_ = (x);                                                              \
+    if (e_ != cudaSuccess)                                                             \
+      return fail(ADPSGD_E_CUDA, std::string(#x) + ": " + cudaGetErrorString(e_));     \
+  } while (0)
+#define NC(x)                                                                          \
+  do {                                                                                 \
+    ncclResult_t r_ = (x);                                                             \
+    if (r_ != ncclSuccess)                                                             \
+      return fail(ADPSGD_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));     \
+  } while (0)
+#define ST(x)                                                                          \
+  do {                                                                                 \
+    adpsgd_status s_ = (x);                                                            \
+    if (s_ != ADPSGD_OK) return s_;                                                    \
+  } while (0)
+
+constexpr uint32_t kBlobMagic = 0xADB5D200u;
+
+struct PeerBlob {
+  uint32_t magic, version;
+  int32_t rank, n_local;
+  int64_t d_pad;
+  int64_t gctl_offset, log_offset, log_cap;
+  cudaIpcMemHandle_t models, ctl;
+};
+
+uint64_t splitmix64(uint64_t& s) {
+  uint64_t z = (s += 0x9E3779B97F4A7C15ull);
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+
+}  // namespace
+
+struct adpsgd_ctx {
+  // ---- configuration (owned copies) ----
+  int rank = 0, world = 1, device = 0;
+  int n = 0;
+  long long d = 0, d_pad = 0, n4 = 0;
+  adpsgd_model_kind model = ADPSGD_MODEL_NONE;
+  float gamma = 0.f;
+  int M = 1, T = 0;
+  uint64_t seed = 0;
+  QuadParams q{};
+  long long compute_ns = 0;
+  int engine_cps = 0, engine_threads = 512;
+  long long log_cap = 1 << 20;
+  std::vector<int32_t> edges;
+  std::vector<int8_t> role;
+  std::vector<std::vector<int>> nb;
+  std::vector<int> nb_flat, nb_off;
+  std::vector<int> worker_rank, worker_local;
+  std::vector<float> straggle;
+  std::vector<int> local_ids;
+  int n_local = 0;
+  int S = 0, feat = 0;
+  MlpShape mlp{0, 0, 0};
+  // ---- device state ----
+  cudaStream_t stream = nullptr;
+  float* models = nullptr;
+  char* ctl_arena = nullptr;
+  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0;
+  WorkerCtl* ctl = nullptr;
+  GlobalCtl* gctl = nullptr;
+  LogEntry* log = nullptr;           // rank 0 only (local)
+  GlobalCtl* gctl0 = nullptr;        // rank 0's (local or peer)
+  LogEntry* log0 = nullptr;
+  std::vector<float*> peer_models;
+  std::vector<char*> peer_ctl;
+  std::vector<bool> peer_imported;
+  WorkerDesc* d_workers = nullptr;
+  int* d_nbrs = nullptr;
+  int* d_local_ids = nullptr;
+  Slot* d_slots = nullptr;
+  ReplayEv* d_rev = nullptr;
+  size_t rev_cap = 0;
+  float* dx0 = nullptr;
+  float *dA = nullptr, *db = nullptr;
+  int* dy = nullptr;
+  float* gslots = nullptr;
+  int gslot_n = 0;
+  float* gstep = nullptr;            // per-local-worker gradient buffers (adpsgd_step)
+  float* mlp_scratch = nullptr;
+  size_t mlp_scratch_n = 0;
+  int* d_batch = nullptr;
+  size_t batch_cap = 0;
+  double* sum64 = nullptr;
+  double* mk_acc = nullptr;
+  float *xr = nullptr, *gsum = nullptr;
+  unsigned long long ar_k = 0;
+  ncclComm_t comm = nullptr;
+  bool connected = false;
+  // ---- host executor state ----
+  std::mutex mu;
+  std::vector<cudaEvent_t> last_evt;
+  std::vector<uint64_t> step_ctr;
+  unsigned long long host_k = 0;
+  bool host_k_valid = true;
+  long long launches = 0;
+  unsigned int run_counter = 0;
+  std::vector<Slot> h_slots;
+  std::vector<ReplayEv> h_rev;
+
+  cudaStream_t use(adpsgd_stream s) const { return s ? (cudaStream_t)s : stream; }
+  float* row(int w) const { return models + (long long)worker_local[w] * d_pad; }
+  bool is_local(int w) const { return worker_rank[w] == rank; }
+  uint2 seed2() const { return make_uint2((uint32_t)seed, (uint32_t)(seed >> 32)); }
+};
+
+namespace {
+
+// ------------------------------------------------------------ graph checks --
+adpsgd_status check_graph(adpsgd_ctx* c, const adpsgd_graph* g) {
+  const int n = g->n;
+  if (n < 1 || g->n_edges < 0 || (g->n_edges > 0 && !g->edges))
+    return fail(ADPSGD_E_INVALID, "graph: n < 1 or null edges");
+  c->nb.assign(n, {});
+  for (int e = 0; e < g->n_edges; ++e) {
+    const int a = g->edges[2 * e], b = g->edges[2 * e + 1];
+    if (a < 0 || a >= n || b < 0 || b >= n || a == b)
+      return fail(ADPSGD_E_INVALID, "graph: edge out of range or self-loop (S:80)");
+    if (std::find(c->nb[a].begin(), c->nb[a].end(), b) != c->nb[a].end())
+      return fail(ADPSGD_E_INVALID, "graph: duplicate edge");
+    c->nb[a].push_back(b);
+    c->nb[b].push_back(a);
+  }
+  for (auto& v : c->nb) std::sort(v.begin(), v.end());
+  // connectivity + 2-colouring (BFS from 0, coloured active)
+  std::vector<int> col(n, -1), q;
+  col[0] = 0;
+  q.push_back(0);
+  bool bip = true;
+  for (size_t h = 0; h < q.size(); ++h) {
+    const int u = q[h];
+    for (int w : c->nb[u]) {
+      if (col[w] < 0) { col[w] = 1 - col[u]; q.push_back(w); }
+      else if (col[w] == col[u]) bip = false;
+    }
+  }
+  if ((int)q.size() != n) return fail(ADPSGD_E_DISCONNECTED, "graph is not connected (rho = 1)");
+  c->role.assign(n, 0);
+  if (g->role) {
+    for (int v = 0; v < n; ++v) {
+      if (g->role[v] != 0 && g->role[v] != 1) return fail(ADPSGD_E_INVALID, "role must be 0/1");
+      c->role[v] = g->role[v];
+    }
+    for (int e = 0; e < g->n_edges; ++e)
+      if (c->role[g->edges[2 * e]] == c->role[g->edges[2 * e + 1]])
+        return fail(ADPSGD_E_NOT_BIPARTITE, "edge joins two workers of the same role (P:469-476)");
+  } else {
+    if (!bip) return fail(ADPSGD_E_NOT_BIPARTITE, "graph has an odd cycle: no active/passive split");
+    for (int v = 0; v < n; ++v) c->role[v] = (int8_t)col[v];
+  }
+  c->edges.assign(g->edges, g->edges + 2 * g->n_edges);
+  c->nb_flat.clear();
+  c->nb_off.assign(n + 1, 0);
+  for (int v = 0; v < n; ++v) {
+    c->nb_off[v] = (int)c->nb_flat.size();
+    c->nb_flat.insert(c->nb_flat.end(), c->nb[v].begin(), c->nb[v].end());
+  }
+  c->nb_off[n] = (int)c->nb_flat.size();
+  return ADPSGD_OK;
+}
+
+bool is_neighbour(const adpsgd_ctx* c, int i, int j) {
+  return std::binary_search(c->nb[i].begin(), c->nb[i].end(), j);
+}
+
+adpsgd_status upload_workers(adpsgd_ctx* c) {
+  std::vector<WorkerDesc> wd(c->n);
+  for (int w = 0; w < c->n; ++w) {
+    const int r = c->worker_rank[w];
+    WorkerDesc& x = wd[w];
+    if (r == c->rank) {
+      x.x = c->row(w);
+      x.ctl = c->ctl + c->worker_local[w];
+    } else {
+      x.x = c->peer_models[r] ? c->peer_models[r] + (long long)c->worker_local[w] * c->d_pad : nullptr;
+      x.ctl = c->peer_ctl[r] ? reinterpret_cast<WorkerCtl*>(c->peer_ctl[r]) + c->worker_local[w] : nullptr;
+    }
+    x.rank = r;
+    x.role = c->role[w];
+    x.nb_off = c->nb_off[w];
+    x.nb_cnt = c->nb_off[w + 1] - c->nb_off[w];
+    x.straggle = c->straggle[w];
+    x.local = r == c->rank ? c->worker_local[w] : -1;
+  }
+  CU(cudaMemcpy(c->d_workers, wd.data(), sizeof(WorkerDesc) * c->n, cudaMemcpyHostToDevice));
+  return ADPSGD_OK;
+}
+
+adpsgd_status read_ticket(adpsgd_ctx* c, unsigned long long* k) {
+  CU(cudaStreamSynchronize(c->stream));
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(k, &c->gctl0->ticket, sizeof(*k), cudaMemcpyDeviceToHost));
+  return ADPSGD_OK;
+}
+
+adpsgd_status host_ticket(adpsgd_ctx* c, unsigned long long* k) {
+  if (!c->host_k_valid) {
+    ST(read_ticket(c, &c->host_k));
+    c->host_k_valid = true;
+  }
+  *k = c->host_k;
+  return ADPSGD_OK;
+}
+
+adpsgd_status ensure_gslots(adpsgd_ctx* c, int count) {
+  if (c->gslot_n >= count) return ADPSGD_OK;
+  if (c->gslots) cudaFree(c->gslots);
+  c->gslots = nullptr;
+  CU(cudaMalloc(&c->gslots, sizeof(float) * c->d_pad * count));
+  CU(cudaMemset(c->gslots, 0, sizeof(float) * c->d_pad * count));
+  c->gslot_n = count;
+  return ADPSGD_OK;
+}
+
+adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c) {
+  const size_t need = mlp_scratch_floats(c->mlp, c->M);
+  if (c->mlp_scratch_n >= need) return ADPSGD_OK;
+  if (c->mlp_scratch) cudaFree(c->mlp_scratch);
+  c->mlp_scratch = nullptr;
+  CU(cudaMalloc(&c->mlp_scratch, sizeof(float) * need));
+  c->mlp_scratch_n = need;
+  return ADPSGD_OK;
+}
+
+// gradient of the built-in model at xhat into g (minibatch of event k)
+adpsgd_status model_grad(adpsgd_ctx* c, const float* xhat, float* g, unsigned long long k,
+                         const int* idx_dev, cudaStream_t s) {
+  switch (c->model) {
+    case ADPSGD_MODEL_QUADRATIC:
+      CU(launch_quad_grad(xhat, g, c->d, c->n4, c->q, k, s));
+      break;
+    case ADPSGD_MODEL_LSQ:
+    case ADPSGD_MODEL_LOGREG:
+      CU(launch_linear_grad((int)c->model, c->dA, c->db, c->S, idx_dev, c->M, c->seed2(), k, xhat, g,
+                            c->d, s));
+      break;
+    case ADPSGD_MODEL_MLP:
+      ST(ensure_mlp_scratch(c));
+      CU(launch_mlp_grad(c->mlp, c->dA, c->dy, c->S, idx_dev, c->M, c->seed2(), k, xhat, g,
+                         c->mlp_scratch, s));
+      break;
+    default:
+      return fail(ADPSGD_E_UNSUPPORTED, "model has no built-in gradient");
+  }
+  c->launches += (c->model == ADPSGD_MODEL_MLP) ? 6 : 1;
+  return ADPSGD_OK;
+}
+
+adpsgd_status validate_events(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, bool need_local) {
+  for (int64_t e = 0; e < K; ++e) {
+    const int i = ev[e].i, j = ev[e].j, tau = ev[e].tau;
+    char buf[160];
+    if (i < 0 || i >= c->n || j < -1 || j >= c->n || i == j) {
+      snprintf(buf, sizeof buf, "event %lld: invalid (i=%d, j=%d)", (long long)e, i, j);
+      return fail(ADPSGD_E_INVALID, buf);
+    }
+    if (j >= 0 && !is_neighbour(c, i, j)) {
+      snprintf(buf, sizeof buf, "event %lld: (%d,%d) is not an edge", (long long)e, i, j);
+      return fail(ADPSGD_E_NOT_NEIGHBOURS, buf);
+    }
+    if (j >= 0 && c->role[i] == c->role[j]) return fail(ADPSGD_E_NOT_BIPARTITE, "event pairs same roles");
+    if (tau < 0 || tau > c->T || tau > e) {
+      snprintf(buf, sizeof buf, "event %lld: tau=%d exceeds min(k, T=%d) (P:601-602)", (long long)e, tau, c->T);
+      return fail(ADPSGD_E_STALENESS, buf);
+    }
+    if (need_local && (!c->is_local(i) || (j >= 0 && !c->is_local(j))))
+      return fail(ADPSGD_E_UNSUPPORTED, "host executor needs every worker local (world_size 1)");
+  }
+  return ADPSGD_OK;
+}
+
+// ----------------------------------------------------------- host replay ----
+adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, const int32_t* bidx,
+                          cudaStream_t s) {
+  ST(validate_events(c, ev, K, true));
+  const bool has_model = c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_EXTERNAL;
+  for (int64_t e = 0; e < K; ++e)
+    if (!(ev[e].flags & ADPSGD_EV_NO_GRAD) && !has_model && c->model == ADPSGD_MODEL_EXTERNAL)
+      return fail(ADPSGD_E_UNSUPPORTED, "replay with gradients needs a built-in model");
+  unsigned long long k0;
+  ST(host_ticket(c, &k0));
+  const int slots = c->T + 1;
+  bool need_slots = false;
+  std::vector<std::vector<int64_t>> reads(K);
+  for (int64_t e = 0; e < K; ++e) {
+    const bool grad = has_model && !(ev[e].flags & ADPSGD_EV_NO_GRAD);
+    if (!grad) continue;
+    if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0) continue;   // fused inline
+    need_slots = true;
+    reads[e - ev[e].tau].push_back(e);   // gradient at X_{e - tau}
+  }
+  if (need_slots) ST(ensure_gslots(c, slots));
+  const bool sampled = c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG ||
+                       c->model == ADPSGD_MODEL_MLP;
+  if (sampled && bidx) {
+    const size_t need = (size_t)K * c->M;
+    if (c->batch_cap < need) {
+      if (c->d_batch) cudaFree(c->d_batch);
+      c->d_batch = nullptr;
+      CU(cudaMalloc(&c->d_batch, sizeof(int) * need));
+      c->batch_cap = need;
+    }
+    for (size_t t = 0; t < need; ++t)
+      if (bidx[t] < 0 || bidx[t] >= c->S) return fail(ADPSGD_E_INVALID, "batch index out of range");
+    CU(cudaMemcpyAsync(c->d_batch, bidx, sizeof(int) * need, cudaMemcpyHostToDevice, s));
+  }
+  for (int64_t e = 0; e < K; ++e) {
+    for (int64_t kp : reads[e]) {     // stale reads that happen before event e
+      float* slot = c->gslots + (kp % slots) * c->d_pad;
+      const int* idx = (sampled && bidx) ? c->d_batch + kp * c->M : nullptr;
+      ST(model_grad(c, c->row(ev[kp].i), slot, k0 + kp, idx, s));
+    }
+    const int i = ev[e].i, j = ev[e].j;
+    const bool grad = has_model && !(ev[e].flags & ADPSGD_EV_NO_GRAD);
+    int mode = kGradNone;
+    const float* g = nullptr;
+    if (grad) {
+      if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0) mode = kGradQuadInline;
+      else { mode = kGradExternal; g = c->gslots + (e % slots) * c->d_pad; }
+    }
+    if (j >= 0 || mode != kGradNone) {
+      CU(launch_event(c->row(i), j >= 0 ? c->row(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma,
+                      c->q, k0 + e, mode, s));
+      ++c->launches;
+    }
+  }
+  c->host_k = k0 + K;
+  CU(launch_set_u64(&c->gctl0->ticket, c->host_k, s));
+  ++c->launches;
+  return ADPSGD_OK;
+}
+
+// --------------------------------------------------------- engine helpers --
+adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, cudaStream_t s) {
+  EngineParams p{};
+  p.workers = c->d_workers;
+  p.nbrs = c->d_nbrs;
+  p.n = c->n;
+  p.n_local = c->n_local;
+  p.slots = c->d_slots;
+  p.local_ids = c->d_local_ids;
+  p.gctl0 = c->gctl0;
+  p.gctl = c->gctl;
+  p.log = c->log0;
+  p.log_cap = c->log_cap;
+  p.target = target;
+  p.mode = mode;
+  p.model = (int)c->model == ADPSGD_MODEL_QUADRATIC ? 2 : 0;
+  p.my_rank = c->rank;
+  p.rev = c->d_rev;
+  p.q = c->q;
+  p.gamma = c->gamma;
+  p.d = c->d;
+  p.n4 = c->n4;
+  p.compute_ns = c->compute_ns;
+  p.seed = make_uint2((uint32_t)(c->seed ^ 0x5bd1e995u), (uint32_t)(c->seed >> 32) ^ c->run_counter);
+  p.watchdog_ns = 60ull * 1000000000ull;
+  int dev_sms = 0;
+  CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
+  int occ = engine_max_ctas_per_sm(c->engine_threads);
+  if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
+  int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
+  CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
+  CU(launch_engine(p, cps * dev_sms, c->engine_threads, s));
+  ++c->launches;
+  ++c->run_counter;
+  c->host_k_valid = false;
+  return ADPSGD_OK;
+}
+
+adpsgd_status reset_slots(adpsgd_ctx* c, cudaStream_t s) {
+  c->h_slots.assign(c->n_local, Slot{});
+  for (int l = 0; l < c->n_local; ++l) {
+    Slot& x = c->h_slots[l];
+    x.tag = 0;
+    x.pending_j = -2;
+    x.nb_ctr = c->run_counter << 20;
+    x.j = -1;
+  }
+  CU(cudaMemcpyAsync(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice, s));
+  CU(cudaStreamSynchronize(s));
+  return ADPSGD_OK;
+}
+
+adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cudaStream_t s) {
+  if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+  if (c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_QUADRATIC)
+    return fail(ADPSGD_E_UNSUPPORTED, "engine replay supports models NONE and QUADRATIC");
+  ST(validate_events(c, ev, K, false));
+  for (int64_t e = 0; e < K; ++e)
+    if (ev[e].tau != 0) return fail(ADPSGD_E_UNSUPPORTED, "engine replay needs tau = 0 (use HOST)");
+  // quiescent read of every worker's epoch (peer memory via UVA) and of k
+  CU(cudaDeviceSynchronize());
+  std::vector<unsigned int> ep(c->n);
+  for (int w = 0; w < c->n; ++w) {
+    const WorkerCtl* cw = c->is_local(w) ? c->ctl + c->worker_local[w]
+                                         : reinterpret_cast<WorkerCtl*>(c->peer_ctl[c->worker_rank[w]]) +
+                                               c->worker_local[w];
+    CU(cudaMemcpy(&ep[w], &cw->epoch, sizeof(unsigned int), cudaMemcpyDeviceToHost));
+  }
+  unsigned long long k0;
+  ST(read_ticket(c, &k0));
+  std::vector<std::vector<ReplayEv>> per(c->n_local);
+  for (int64_t e = 0; e < K; ++e) {
+    const int i = ev[e].i, j = ev[e].j;
+    ReplayEv r{};
+    r.k = (long long)(k0 + e);
+    r.j = j;
+    r.flags = ev[e].flags;
+    r.e_i = ep[i];
+    r.e_j = j >= 0 ? ep[j] : 0;
+    ep[i]++;
+    if (j >= 0) ep[j]++;
+    if (c->is_local(i)) per[c->worker_local[i]].push_back(r);
+  }
+  c->h_rev.clear();
+  ST(reset_slots(c, s));
+  for (int l = 0; l < c->n_local; ++l) {
+    c->h_slots[l].ev_cur = (long long)c->h_rev.size();
+    c->h_rev.insert(c->h_rev.end(), per[l].begin(), per[l].end());
+    c->h_slots[l].ev_end = (long long)c->h_rev.size();
+  }
+  if (c->rev_cap < c->h_rev.size() + 1) {
+    if (c->d_rev) cudaFree(c->d_rev);
+    c->d_rev = nullptr;
+    CU(cudaMalloc(&c->d_rev, sizeof(ReplayEv) * (c->h_rev.size() + 1)));
+    c->rev_cap = c->h_rev.size() + 1;
+  }
+  if (!c->h_rev.empty())
+    CU(cudaMemcpy(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice));
+  CU(cudaMemcpy(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice));
+  return engine_launch(c, 1, 0, s);
+}
+
+adpsgd_status destroy_impl(adpsgd_ctx* c) {
+  if (!c) return ADPSGD_OK;
+  cudaSetDevice(c->device);
+  cudaDeviceSynchronize();
+  if (c->comm) ncclCommDestroy(c->comm);
+  for (size_t r = 0; r < c->peer_models.size(); ++r) {
+    if ((int)r == c->rank) continue;
+    if (c->peer_models[r]) cudaIpcCloseMemHandle(c->peer_models[r]);
+    if (c->peer_ctl[r]) cudaIpcCloseMemHandle(c->peer_ctl[r]);
+  }
+  for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
+  void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids, c->d_slots,
+                  c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
+                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum};
+  for (void* b : bufs) if (b) cudaFree(b);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+  return ADPSGD_OK;
+}
+
+adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
+                        const adpsgd_config* cfg, adpsgd_ctx** out) {
+  if (!g || !cfg || !out) return fail(ADPSGD_E_INVALID, "null argument");
+  if (n_workers != g->n) return fail(ADPSGD_E_INVALID, "n_workers != graph.n");
+  if (d < 1 || d > (1LL << 31) - 64) return fail(ADPSGD_E_INVALID, "d out of range");
+  if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
+    return fail(ADPSGD_E_INVALID, "rank/world_size");
+  if (cfg->batch_M < 0 || cfg->staleness_cap_T < 0) return fail(ADPSGD_E_INVALID, "M/T < 0");
+  std::unique_ptr<adpsgd_ctx> c(new adpsgd_ctx());
+  c->rank = cfg->rank;
+  c->world = cfg->world_size;
+  c->device = cfg->device;
+  c->n = n_workers;
+  c->d = d;
+  c->d_pad = (d + 63) / 64 * 64;
+  c->n4 = c->d_pad / 4;
+  c->model = cfg->model;
+  c->gamma = cfg->gamma;
+  c->M = cfg->batch_M > 0 ? cfg->batch_M : 1;
+  c->T = cfg->staleness_cap_T;
+  c->seed = cfg->seed;
+  c->q.data_key = cfg->quad_data_key;
+  c->q.noise_key = cfg->quad_noise_key;
+  c->q.Mf = (float)c->M;
+  c->q.s = cfg->quad_noise_s;
+  c->compute_ns = cfg->compute_ns;
+  c->engine_cps = cfg->engine_ctas_per_sm;
+  c->engine_threads = cfg->engine_threads > 0 ? cfg->engine_threads : 512;
+  if (c->engine_threads % 32 || c->engine_threads > 512) return fail(ADPSGD_E_INVALID, "engine_threads");
+  if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
+  if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
+  ST(check_graph(c.get(), g));
+  // placement
+  c->worker_rank.assign(c->n, 0);
+  for (int w = 0; w < c->n; ++w) {
+    if (cfg->placement == 0) c->worker_rank[w] = (int)((long long)w * c->world / c->n);
+    else if (cfg->placement == 1) c->worker_rank[w] = w % c->world;
+    else if (cfg->placement == 2) {
+      if (!cfg->worker_rank) return fail(ADPSGD_E_INVALID, "explicit placement needs worker_rank");
+      c->worker_rank[w] = cfg->worker_rank[w];
+      if (c->worker_rank[w] < 0 || c->worker_rank[w] >= c->world) return fail(ADPSGD_E_INVALID, "worker_rank");
+    } else return fail(ADPSGD_E_INVALID, "placement");
+  }
+  c->worker_local.assign(c->n, 0);
+  std::vector<int> cnt(c->world, 0);
+  for (int w = 0; w < c->n; ++w) {
+    c->worker_local[w] = cnt[c->worker_rank[w]]++;
+    if (c->worker_rank[w] == c->rank) c->local_ids.push_back(w);
+  }
+  c->n_local = (int)c->local_ids.size();
+  if (c->n_local > kMaxLocal) return fail(ADPSGD_E_UNSUPPORTED, "more than 128 workers on one GPU");
+  c->straggle.assign(c->n, 1.0f);
+  if (cfg->straggler)
+    for (int w = 0; w < c->n; ++w) {
+      if (!(cfg->straggler[w] >= 1.0f)) return fail(ADPSGD_E_INVALID, "straggler factors must be >= 1");
+      c->straggle[w] = cfg->straggler[w];
+    }
+  // model data
+  if (c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG || c->model == ADPSGD_MODEL_MLP) {
+    if (cfg->n_samples < 1 || !cfg->data_A) return fail(ADPSGD_E_INVALID, "dataset required");
+    c->S = cfg->n_samples;
+    if (c->model == ADPSGD_MODEL_MLP) {
+      c->mlp = MlpShape{cfg->mlp_in, cfg->mlp_hid, cfg->mlp_out};
+      const long long dim = (long long)c->mlp.n_hid * c->mlp.n_in + c->mlp.n_hid +
+                            (long long)c->mlp.n_out * c->mlp.n_hid + c->mlp.n_out;
+      if (dim != d || !cfg->data_y) return fail(ADPSGD_E_INVALID, "mlp dims do not match d / labels missing");
+      c->feat = c->mlp.n_in;
+    } else {
+      if (!cfg->data_b) return fail(ADPSGD_E_INVALID, "data_b required");
+      c->feat = (int)d;
+    }
+    if (c->M > 1024) return fail(ADPSGD_E_UNSUPPORTED, "batch_M > 1024");
+  }
+  CU(cudaSetDevice(c->device));
+  CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  // models
+  CU(cudaMalloc(&c->models, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+  CU(cudaMemset(c->models, 0, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+  CU(cudaMalloc(&c->dx0, sizeof(float) * c->d_pad));
+  CU(cudaMemset(c->dx0, 0, sizeof(float) * c->d_pad));
+  if (cfg->x0) CU(cudaMemcpy(c->dx0, cfg->x0, sizeof(float) * d, cudaMemcpyHostToDevice));
+  if (cfg->x0_per_worker) {
+    for (int l = 0; l < c->n_local; ++l)
+      CU(cudaMemcpy(c->models + (long long)l * c->d_pad, cfg->x0_per_worker + (long long)c->local_ids[l] * d,
+                    sizeof(float) * d, cudaMemcpyHostToDevice));
+  } else if (c->n_local) {
+    CU(launch_init_rows(c->models, c->n_local, c->d_pad, c->d, c->dx0, c->stream));
+  }
+  // control arena: WorkerCtl[n_local] | GlobalCtl | (rank 0) log ring
+  c->gctl_offset = sizeof(WorkerCtl) * std::max(1, c->n_local);
+  c->log_offset = c->gctl_offset + sizeof(GlobalCtl);
+  c->ctl_bytes = c->log_offset + (c->rank == 0 ? sizeof(LogEntry) * c->log_cap : 0);
+  CU(cudaMalloc(&c->ctl_arena, c->ctl_bytes));
+  CU(cudaMemset(c->ctl_arena, 0, c->ctl_bytes));
+  c->ctl = reinterpret_cast<WorkerCtl*>(c->ctl_arena);
+  c->gctl = reinterpret_cast<GlobalCtl*>(c->ctl_arena + c->gctl_offset);
+  c->log = c->rank == 0 ? reinterpret_cast<LogEntry*>(c->ctl_arena + c->log_offset) : nullptr;
+  if (c->rank == 0) { c->gctl0 = c->gctl; c->log0 = c->log; }
+  // datasets (every rank: Strategy-1)
+  if (c->S) {
+    CU(cudaMalloc(&c->dA, sizeof(float) * (size_t)c->S * c->feat));
+    CU(cudaMemcpy(c->dA, cfg->data_A, sizeof(float) * (size_t)c->S * c->feat, cudaMemcpyHostToDevice));
+    if (cfg->data_b) {
+      CU(cudaMalloc(&c->db, sizeof(float) * c->S));
+      CU(cudaMemcpy(c->db, cfg->data_b, sizeof(float) * c->S, cudaMemcpyHostToDevice));
+    }
+    if (cfg->data_y) {
+      for (int s = 0; s < c->S; ++s)
+        if (cfg->data_y[s] < 0 || cfg->data_y[s] >= c->mlp.n_out) return fail(ADPSGD_E_INVALID, "label range");
+      CU(cudaMalloc(&c->dy, sizeof(int) * c->S));
+      CU(cudaMemcpy(c->dy, cfg->data_y, sizeof(int) * c->S, cudaMemcpyHostToDevice));
+    }
+  }
+  // tables
+  CU(cudaMalloc(&c->d_workers, sizeof(WorkerDesc) * c->n));
+  CU(cudaMalloc(&c->d_nbrs, sizeof(int) * std::max<size_t>(1, c->nb_flat.size())));
+  if (!c->nb_flat.empty())
+    CU(cudaMemcpy(c->d_nbrs, c->nb_flat.data(), sizeof(int) * c->nb_flat.size(), cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&c->d_local_ids, sizeof(int) * std::max(1, c->n_local)));
+  if (c->n_local)
+    CU(cudaMemcpy(c->d_local_ids, c->local_ids.data(), sizeof(int) * c->n_local, cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&c->d_slots, sizeof(Slot) * std::max(1, c->n_local)));
+  CU(cudaMemset(c->d_slots, 0, sizeof(Slot) * std::max(1, c->n_local)));
+  CU(cudaMalloc(&c->sum64, sizeof(double) * c->d_pad));
+  CU(cudaMalloc(&c->mk_acc, sizeof(double)));
+  c->peer_models.assign(c->world, nullptr);
+  c->peer_ctl.assign(c->world, nullptr);
+  c->peer_imported.assign(c->world, false);
+  c->peer_models[c->rank] = c->models;
+  c->peer_ctl[c->rank] = c->ctl_arena;
+  c->peer_imported[c->rank] = true;
+  c->last_evt.assign(c->n, nullptr);
+  for (auto& e : c->last_evt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  c->step_ctr.assign(c->n, 0);
+  c->launches += 1;
+  if (c->world == 1) {
+    ST(upload_workers(c.get()));
+    c->connected = true;
+  }
+  CU(cudaStreamSynchronize(c->stream));
+  *out = c.release();
+  return ADPSGD_OK;
+}
+
+}  // namespace
+
+#define GUARD(body)                                                                   \
+  try {                                                                               \
+    body                                                                              \
+  } catch (const std::bad_alloc&) {                                                   \
+    return fail(ADPSGD_E_OOM, "host allocation failed");                              \
+  } catch (...) {                                                                     \
+    return fail(ADPSGD_E_INVALID, "internal exception");                              \
+  }
+
+#define CTX_CHECK(c)                                                                  \
+  if (!(c)) return fail(ADPSGD_E_INVALID, "null context");                           \
+  CU(cudaSetDevice((c)->device));
+
+extern "C" {
+
+int32_t adpsgd_abi_version(void) { return ADPSGD_ABI_VERSION; }
+const char* adpsgd_last_error(void) { return g_err.c_str(); }
+
+adpsgd_status adpsgd_init(const adpsgd_graph* g, int32_t n_workers, int64_t d,
+                          const adpsgd_config* cfg, adpsgd_ctx** out) {
+  GUARD(return init_impl(g, n_workers, d, cfg, out);)
+}
+
+adpsgd_status adpsgd_destroy(adpsgd_ctx* ctx) { GUARD(return destroy_impl(ctx);) }
+
+adpsgd_status adpsgd_peer_info_size(int64_t* bytes) {
+  if (!bytes) return fail(ADPSGD_E_INVALID, "null");
+  *bytes = (int64_t)sizeof(PeerBlob);
+  return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_export_peer_info(adpsgd_ctx* c, void* buf, int64_t cap, int64_t* n_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!buf || cap < (int64_t)sizeof(PeerBlob)) return fail(ADPSGD_E_INVALID, "buffer too small");
+    PeerBlob b{};
+    b.magic = kBlobMagic;
+    b.version = ADPSGD_ABI_VERSION;
+    b.rank = c->rank;
+    b.n_local = c->n_local;
+    b.d_pad = c->d_pad;
+    b.gctl_offset = (int64_t)c->gctl_offset;
+    b.log_offset = (int64_t)c->log_offset;
+    b.log_cap = c->log_cap;
+    CU(cudaIpcGetMemHandle(&b.models, c->models));
+    CU(cudaIpcGetMemHandle(&b.ctl, c->ctl_arena));
+    memcpy(buf, &b, sizeof b);
+    if (n_out) *n_out = (int64_t)sizeof b;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* buf, int64_t n) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!buf || n < (int64_t)sizeof(PeerBlob) || rank < 0 || rank >= c->world)
+      return fail(ADPSGD_E_INVALID, "bad peer blob");
+    if (rank == c->rank) return ADPSGD_OK;
+    PeerBlob b;
+    memcpy(&b, buf, sizeof b);
+    if (b.magic != kBlobMagic || b.rank != rank || b.d_pad != c->d_pad)
+      return fail(ADPSGD_E_INVALID, "peer blob mismatch (magic/rank/d)");
+    void* pm = nullptr;
+    void* pc = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&pm, b.models, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer models over NVLink: ") + cudaGetErrorString(e));
+    e = cudaIpcOpenMemHandle(&pc, b.ctl, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess)
+      return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer control: ") + cudaGetErrorString(e));
+    c->peer_models[rank] = static_cast<float*>(pm);
+    c->peer_ctl[rank] = static_cast<char*>(pc);
+    c->peer_imported[rank] = true;
+    if (rank == 0) {
+      c->gctl0 = reinterpret_cast<GlobalCtl*>(c->peer_ctl[0] + b.gctl_offset);
+      c->log0 = reinterpret_cast<LogEntry*>(c->peer_ctl[0] + b.log_offset);
+      c->log_cap = b.log_cap;
+    }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_nccl_unique_id(void* buf128) {
+  if (!buf128) return fail(ADPSGD_E_INVALID, "null");
+  ncclUniqueId id;
+  NC(ncclGetUniqueId(&id));
+  static_assert(sizeof(id) == 128, "ncclUniqueId size");
+  memcpy(buf128, &id, sizeof id);
+  return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_connect(adpsgd_ctx* c, const void* nccl_id) {
+  GUARD({
+    CTX_CHECK(c);
+    for (int r = 0; r < c->world; ++r)
+      if (!c->peer_imported[r]) return fail(ADPSGD_E_STATE, "peer info of some rank not imported");
+    ST(upload_workers(c));
+    if (c->world > 1) {
+      if (!nccl_id) return fail(ADPSGD_E_INVALID, "nccl_id required when world_size > 1");
+      ncclUniqueId id;
+      memcpy(&id, nccl_id, sizeof id);
+      NC(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+    }
+    c->connected = true;
+    c->host_k_valid = false;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (i < 0 || j < 0 || i >= c->n || j >= c->n || i == j) return fail(ADPSGD_E_INVALID, "i/j");
+    if (!is_neighbour(c, i, j)) return fail(ADPSGD_E_NOT_NEIGHBOURS, "not an edge");
+    if (!c->is_local(i) || !c->is_local(j)) return fail(ADPSGD_E_UNSUPPORTED, "gossip needs local workers");
+    std::lock_guard<std::mutex> lk(c->mu);
+    cudaStream_t st = c->use(s);
+    CU(cudaStreamWaitEvent(st, c->last_evt[i], 0));
+    CU(cudaStreamWaitEvent(st, c->last_evt[j], 0));
+    CU(launch_event(c->row(i), c->row(j), nullptr, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradNone, st));
+    ++c->launches;
+    CU(cudaEventRecord(c->last_evt[i], st));
+    CU(cudaEventRecord(c->last_evt[j], st));
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_step(adpsgd_ctx* c, int32_t w, const float* grad, adpsgd_stream s,
+                          int64_t* ticket_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (w < 0 || w >= c->n) return fail(ADPSGD_E_INVALID, "worker");
+    if (c->world != 1) return fail(ADPSGD_E_UNSUPPORTED, "adpsgd_step needs world_size 1 (use adpsgd_run)");
+    if (!grad && (c->model == ADPSGD_MODEL_NONE || c->model == ADPSGD_MODEL_EXTERNAL))
+      return fail(ADPSGD_E_INVALID, "no gradient: pass grad or configure a built-in model");
+    std::lock_guard<std::mutex> lk(c->mu);
+    int j = -1;
+    if (c->role[w] == 0 && !c->nb[w].empty()) {
+      uint64_t st = c->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(w + 1)) ^ (c->step_ctr[w]++ << 20);
+      const uint64_t r = splitmix64(st);
+      j = c->nb[w][(size_t)((r >> 32) * c->nb[w].size() >> 32)];
+    }
+    unsigned long long k;
+    ST(host_ticket(c, &k));
+    cudaStream_t st = c->use(s);
+    CU(cudaStreamWaitEvent(st, c->last_evt[w], 0));
+    if (j >= 0) CU(cudaStreamWaitEvent(st, c->last_evt[j], 0));
+    int mode = kGradExternal;
+    const float* g = grad;
+    if (!grad) {
+      if (c->model == ADPSGD_MODEL_QUADRATIC) mode = kGradQuadInline;
+      else {
+        if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+        float* gb = c->gstep + (long long)c->worker_local[w] * c->d_pad;
+        ST(model_grad(c, c->row(w), gb, k, nullptr, st));
+        g = gb;
+      }
+    }
+    CU(launch_event(c->row(w), j >= 0 ? c->row(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma, c->q,
+                    k, mode, st));
+    CU(launch_step_commit(c->gctl0, c->ctl + c->worker_local[w], c->log0, c->log_cap, (long long)k, w, j,
+                          0u, 1, st));
+    c->launches += 2;
+    CU(cudaEventRecord(c->last_evt[w], st));
+    if (j >= 0) CU(cudaEventRecord(c->last_evt[j], st));
+    c->host_k = k + 1;
+    if (ticket_out) *ticket_out = (int64_t)k;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_replay(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, const int32_t* bidx,
+                            uint32_t flags, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (K < 0 || (K > 0 && !ev)) return fail(ADPSGD_E_INVALID, "schedule");
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    if (K == 0) return ADPSGD_OK;
+    const bool engine = (flags & ADPSGD_REPLAY_ENGINE) || (!(flags & ADPSGD_REPLAY_HOST) && c->world > 1);
+    std::lock_guard<std::mutex> lk(c->mu);
+    if (engine) return replay_engine(c, ev, K, c->use(s));
+    return replay_host(c, ev, K, bidx, c->use(s));
+  })
+}
+
+adpsgd_status adpsgd_run(adpsgd_ctx* c, int64_t n_updates, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    if (c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_QUADRATIC)
+      return fail(ADPSGD_E_UNSUPPORTED, "free-running engine supports models NONE and QUADRATIC");
+    if (n_updates < 0) return fail(ADPSGD_E_INVALID, "n_updates");
+    std::lock_guard<std::mutex> lk(c->mu);
+    unsigned long long k0;
+    ST(read_ticket(c, &k0));
+    cudaStream_t st = c->use(s);
+    ST(reset_slots(c, st));
+    return engine_launch(c, 0, k0 + (unsigned long long)n_updates, st);
+  })
+}
+
+adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!out) return fail(ADPSGD_E_INVALID, "out");
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    cudaStream_t st = c->use(s);
+    CU(launch_consensus_sum(c->models, c->n_local, c->d_pad, c->d, c->sum64, st));
+    ++c->launches;
+    if (c->world > 1) NC(ncclAllReduce(c->sum64, c->sum64, (size_t)c->d, ncclFloat64, ncclSum, c->comm, st));
+    CU(launch_consensus_finalize(c->sum64, c->n, c->d, out, st));
+    ++c->launches;
+    if (mk_out) {
+      CU(cudaMemsetAsync(c->mk_acc, 0, sizeof(double), st));
+      CU(launch_consensus_mk(c->models, c->n_local, c->d_pad, c->d, c->sum64, c->n, c->mk_acc, st));
+      ++c->launches;
+      if (c->world > 1) NC(ncclAllReduce(c->mk_acc, c->mk_acc, 1, ncclFloat64, ncclSum, c->comm, st));
+      double acc = 0.0;
+      CU(cudaMemcpyAsync(&acc, c->mk_acc, sizeof(double), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      *mk_out = acc / (double)c->n;
+    }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_allreduce_reset(adpsgd_ctx* c, const float* host_x) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!c->xr) {
+      CU(cudaMalloc(&c->xr, sizeof(float) * c->d_pad));
+      CU(cudaMalloc(&c->gsum, sizeof(float) * c->d_pad));
+    }
+    CU(cudaMemcpy(c->xr, c->dx0, sizeof(float) * c->d_pad, cudaMemcpyDeviceToDevice));
+    if (host_x) CU(cudaMemcpy(c->xr, host_x, sizeof(float) * c->d, cudaMemcpyHostToDevice));
+    c->ar_k = 0;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_allreduce_sgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (c->model != ADPSGD_MODEL_QUADRATIC) return fail(ADPSGD_E_UNSUPPORTED, "baseline uses the quadratic");
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    if (!c->xr) ST(adpsgd_allreduce_reset(c, nullptr));
+    cudaStream_t st = c->use(s);
+    float smax = 1.0f;
+    for (int w : c->local_ids) smax = std::max(smax, c->straggle[w]);
+    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns);
+    for (int64_t r = 0; r < n_rounds; ++r) {
+      if (delay) { CU(launch_delay(delay, st)); ++c->launches; }
+      CU(launch_ar_grad_sum(c->xr, c->gsum, c->d, c->n4, c->q, c->ar_k, c->n_local, c->d_local_ids, st));
+      if (c->world > 1)
+        NC(ncclAllReduce(c->gsum, c->gsum, (size_t)c->d_pad, ncclFloat32, ncclSum, c->comm, st));
+      CU(launch_ar_update(c->xr, c->gsum, c->gamma, c->n, c->d, c->n4, st));
+      c->launches += 2;
+      c->ar_k += (unsigned long long)c->n;
+    }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_allreduce_read_model(adpsgd_ctx* c, float* host_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!host_out || !c->xr) return fail(ADPSGD_E_STATE, "no baseline replica");
+    CU(cudaStreamSynchronize(c->stream));
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(host_out, c->xr, sizeof(float) * c->d, cudaMemcpyDeviceToHost));
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_sync(adpsgd_ctx* c) {
+  GUARD({
+    CTX_CHECK(c);
+    CU(cudaDeviceSynchronize());
+    unsigned int err = 0;
+    CU(cudaMemcpy(&err, &c->gctl->error, sizeof err, cudaMemcpyDeviceToHost));
+    if (err) {
+      CU(cudaMemset(&c->gctl->error, 0, sizeof err));
+      return fail((adpsgd_status)err, "device-side error latched (e.g. watchdog timeout)");
+    }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_read_model(adpsgd_ctx* c, int32_t w, float* host_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (w < 0 || w >= c->n || !host_out) return fail(ADPSGD_E_INVALID, "worker/out");
+    if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "worker not local to this rank");
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(host_out, c->row(w), sizeof(float) * c->d, cudaMemcpyDeviceToHost));
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_write_model(adpsgd_ctx* c, int32_t w, const float* host_in) {
+  GUARD({
+    CTX_CHECK(c);
+    if (w < 0 || w >= c->n || !host_in) return fail(ADPSGD_E_INVALID, "worker/in");
+    if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "worker not local to this rank");
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(c->row(w), host_in, sizeof(float) * c->d, cudaMemcpyHostToDevice));
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_model_device_ptr(adpsgd_ctx* c, int32_t w, float** p) {
+  if (!c || !p || w < 0 || w >= c->n || !c->is_local(w)) return fail(ADPSGD_E_INVALID, "worker");
+  *p = c->row(w);
+  return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_worker_rank(adpsgd_ctx* c, int32_t w, int32_t* r) {
+  if (!c || !r || w < 0 || w >= c->n) return fail(ADPSGD_E_INVALID, "worker");
+  *r = c->worker_rank[w];
+  return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_get_ticket(adpsgd_ctx* c, int64_t* k) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!k || !c->gctl0) return fail(ADPSGD_E_STATE, "not connected");
+    unsigned long long v;
+    ST(read_ticket(c, &v));
+    *k = (int64_t)v;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_read_log(adpsgd_ctx* c, int64_t k_from, adpsgd_log_entry* out, int64_t cap,
+                              int64_t* n_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!out || cap < 0 || k_from < 0 || !c->log0) return fail(ADPSGD_E_INVALID, "args / no log");
+    unsigned long long kt;
+    ST(read_ticket(c, &kt));
+    long long avail = (long long)kt - k_from;
+    if (avail < 0) avail = 0;
+    long long n = std::min<long long>(std::min<long long>(avail, cap), c->log_cap);
+    for (long long t = 0; t < n;) {
+      const long long pos = (k_from + t) % c->log_cap;
+      const long long run = std::min(n - t, c->log_cap - pos);
+      CU(cudaMemcpy(out + t, c->log0 + pos, sizeof(LogEntry) * run, cudaMemcpyDeviceToHost));
+      t += run;
+    }
+    if (n_out) *n_out = n;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_read_update_counts(adpsgd_ctx* c, int64_t* out_n) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!out_n) return fail(ADPSGD_E_INVALID, "out");
+    CU(cudaDeviceSynchronize());
+    std::vector<WorkerCtl> h(std::max(1, c->n_local));
+    CU(cudaMemcpy(h.data(), c->ctl, sizeof(WorkerCtl) * c->n_local, cudaMemcpyDeviceToHost));
+    for (int l = 0; l < c->n_local; ++l) out_n[l] = (int64_t)h[l].updates;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_get_stats(adpsgd_ctx* c, adpsgd_stats* o) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!o) return fail(ADPSGD_E_INVALID, "out");
+    CU(cudaDeviceSynchronize());
+    GlobalCtl g;
+    CU(cudaMemcpy(&g, c->gctl, sizeof g, cudaMemcpyDeviceToHost));
+    unsigned long long kt = 0;
+    if (c->gctl0) CU(cudaMemcpy(&kt, &c->gctl0->ticket, sizeof kt, cudaMemcpyDeviceToHost));
+    o->ticket = (int64_t)kt;
+    o->local_events = (int64_t)g.st_events;
+    o->local_pair_events = (int64_t)g.st_pair;
+    o->local_cross_events = (int64_t)g.st_cross;
+    o->local_bytes = g.st_bytes;
+    o->local_nvlink_bytes = g.st_nvl_bytes;
+    o->engine_busy_ns = (double)g.st_busy_ns;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_reset_stats(adpsgd_ctx* c) {
+  GUARD({
+    CTX_CHECK(c);
+    CU(cudaDeviceSynchronize());
+    GlobalCtl g;
+    CU(cudaMemcpy(&g, c->gctl, sizeof g, cudaMemcpyDeviceToHost));
+    g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = 0;
+    g.st_bytes = g.st_nvl_bytes = 0.0;
+    CU(cudaMemcpy(c->gctl, &g, sizeof g, cudaMemcpyHostToDevice));
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_launch_count(adpsgd_ctx* c, int64_t* out) {
+  if (!c || !out) return fail(ADPSGD_E_INVALID, "null");
+  *out = c->launches;
+  return ADPSGD_OK;
+}
+
+}  // extern "C"

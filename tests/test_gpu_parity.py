@@ -1,0 +1,303 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the
+same seeded inputs (-m gpu).  Bars:
+  * pure-gossip replay and the synthetic quadratic (no reductions): bit-exact;
+  * lsq / logreg replay: |x_gpu - x_orc| <= 1e-4 * max(|x_orc|, rms(x_orc)) (reading c11);
+  * consensus mean: <= 1 ulp; M_k: 1e-9 relative;
+  * free-running engine: its event log replayed through the oracle reproduces
+    the GPU models bitwise; column sum within the c10 tolerances.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    from paper_1710_06952_b200 import build
+    build.build()
+    import paper_1710_06952_b200 as P
+    return P
+
+
+def torch_out(d):
+    import torch
+    return torch.empty(d, dtype=torch.float32, device="cuda")
+
+
+def read_all(ctx):
+    return np.stack([ctx.read_model(w) for w in range(ctx.n)])
+
+
+def c11_ok(x_gpu, x_orc, tol=1e-4):
+    rms = np.sqrt(np.mean(x_orc.astype(np.float64) ** 2, axis=1, keepdims=True))
+    bound = tol * np.maximum(np.abs(x_orc), rms)
+    return np.abs(x_gpu.astype(np.float64) - x_orc) <= bound
+
+
+def log_events(log):
+    return np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+
+
+# ------------------------------------------------------------ pure gossip ---
+@pytest.mark.parametrize("d", [1 << 20, 1000, 4099, 1])
+@pytest.mark.parametrize("path", [1, 2])
+def test_pure_gossip_replay_bit_exact(P, d, path):
+    """Config 2 (n=16 bipartite ring), pure averaging, bit-exact vs the oracle;
+    ragged d (not a multiple of 4 / 64) and d=1 as edge cases; HOST and ENGINE."""
+    n = 16
+    e, r = synth.ring(n)
+    K = 4000 if d == 1 << 20 else 600
+    for seed in ([0, 1] if d == 1 << 20 else [3]):
+        X0 = synth.x0_uniform(n, d, seed=100 + seed)
+        ev, _ = synth.schedule_iid(n, e, K=K, seed=seed, no_grad=True)
+        ctx = P.Context(e, n, d, role=r, x0_per_worker=X0)
+        ctx.replay(ev, flags=path)
+        ctx.sync()
+        Xg = read_all(ctx)
+        Xo, _ = O.replay(O.OracleProblem(), X0, e, r, ev)
+        assert np.array_equal(Xg.view(np.uint32), Xo.view(np.uint32)), (seed, path)
+        ctx.destroy()
+
+
+def test_empty_and_partnerless_events(P):
+    n, d = 4, 300
+    e, r = synth.ring(n)
+    X0 = synth.x0_uniform(n, d, seed=5)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0)
+    ctx.replay(np.zeros((0, 4), np.int32))                       # empty schedule
+    ctx.replay([[2, -1, 0, P.EV_NO_GRAD]])                          # W = I, no gradient
+    ctx.sync()
+    assert np.array_equal(read_all(ctx), X0)
+    assert ctx.ticket() == 1                                     # k still advances
+    ctx.destroy()
+
+
+def test_replay_errors(P):
+    n, d = 4, 64
+    e, r = synth.ring(n)
+    ctx = P.Context(e, n, d, role=r, T=1, model=P.MODEL_QUADRATIC, gamma=0.1, quad_keys=(1, 2))
+    with pytest.raises(P.AdpsgdError) as ei:
+        ctx.replay([[0, 2, 0, 0]])
+    assert ei.value.code == 4
+    with pytest.raises(P.AdpsgdError) as ei:
+        ctx.replay([[0, 1, 0, 0], [1, 0, 2, 0]])
+    assert ei.value.code == 5
+    with pytest.raises(P.AdpsgdError) as ei:
+        ctx.replay([[0, 1, 1, 0]])                              # tau > k
+    assert ei.value.code == 5
+    ctx.destroy()
+
+
+# ------------------------------------------------------ synthetic quadratic --
+@pytest.mark.parametrize("d,n,K,T", [(100003, 8, 300, 3), (4096, 4, 2000, 4)])
+def test_quadratic_replay_bit_exact_with_staleness(P, d, n, K, T):
+    """Quadratic gradients (elementwise, no reductions) with stale reads
+    tau ~ U{0..T}: bit-exact vs the oracle's Alg. 1."""
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(4)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    ev, _ = synth.schedule_iid(n, e, K=K, T=T, seed=7, local_prob=0.2)
+    ctx = P.Context(e, n, d, role=r, T=T, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s)
+    ctx.replay(ev)
+    ctx.sync()
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev, T=T)
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    ctx.destroy()
+
+
+def test_quadratic_engine_replay_full_size(P):
+    """BASELINE size d = 25.6M, n = 8, tau = 0, through the persistent engine
+    (the launch configuration bench.py times): bit-exact vs the oracle."""
+    n, d, K = 8, 25_600_000, 24
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(5)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    ev, _ = synth.schedule_iid(n, e, K=K, seed=11, local_prob=0.3)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s)
+    ctx.replay(ev, flags=P.REPLAY_ENGINE)
+    ctx.sync()
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev)
+    for w in range(n):
+        assert np.array_equal(ctx.read_model(w).view(np.uint32), Xo[w].view(np.uint32)), w
+    ctx.destroy()
+
+
+# -------------------------------------------------------- lsq / logreg -------
+@pytest.mark.parametrize("kind", ["lsq", "logreg"])
+def test_config1_replay_within_1e4(P, kind):
+    """Config 1: n=4 ring, d=1024, M=32, T=4, 2000 steps, explicit batches:
+    max relative error <= 1e-4 per parameter (reading c11)."""
+    n, d, M, K, T = 4, 1024, 32, 2000, 4
+    e, r = synth.ring(n)
+    if kind == "lsq":
+        A, b = synth.lsq_data(S=8192, d=d, seed=1)
+        model, okind, gamma = P.MODEL_LSQ, O.MODEL_LSQ, 0.5
+    else:
+        A, b = synth.logreg_data(S=8192, d=d, seed=2)
+        model, okind, gamma = P.MODEL_LOGREG, O.MODEL_LOGREG, 0.5
+    ev, bi = synth.schedule_iid(n, e, K=K, T=T, M=M, S=8192, seed=42)
+    ctx = P.Context(e, n, d, role=r, T=T, model=model, gamma=gamma, batch_M=M, data_A=A, data_b=b)
+    ctx.replay(ev, batch_idx=bi)
+    ctx.sync()
+    Xg = read_all(ctx)
+    prob = O.OracleProblem(okind, M=M, gamma=gamma, A=A, b=b)
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev, bi, T=T)
+    ok = c11_ok(Xg, Xo)
+    assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum())
+    assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * 0.1
+    ctx.destroy()
+
+
+def test_device_batch_sampling_matches_oracle_philox(P):
+    """batch_idx = NULL: both sides draw idx = (Philox(seed; k, m, BATCH).x * S) >> 32."""
+    n, d, M, K = 4, 256, 8, 200
+    e, r = synth.ring(n)
+    A, b = synth.lsq_data(S=512, d=d, seed=3)
+    seed = 0x1234_5678_9ABC
+    ev, _ = synth.schedule_iid(n, e, K=K, seed=1)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_LSQ, gamma=0.1, batch_M=M, data_A=A, data_b=b, seed=seed)
+    ctx.replay(ev)
+    ctx.sync()
+    prob = O.OracleProblem(O.MODEL_LSQ, M=M, gamma=0.1, A=A, b=b,
+                           batch_key=(seed & 0xFFFFFFFF, seed >> 32))
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev)
+    assert c11_ok(read_all(ctx), Xo).all()
+    ctx.destroy()
+
+
+# -------------------------------------------------------- consensus output ---
+def test_consensus_mean_within_one_ulp(P):
+    n, d = 16, 1 << 20
+    e, r = synth.ring(n)
+    X0 = synth.x0_uniform(n, d, seed=9) * np.float32(1000.0)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0)
+    out = torch_out(d)
+    mk = ctx.consensus_mean(out.data_ptr())
+    xg = out.cpu().numpy()
+    xo, mko = O.consensus_mean(X0)
+    ulp = np.abs(xg.view(np.int32).astype(np.int64) - xo.view(np.int32).astype(np.int64))
+    assert ulp.max() <= 1
+    assert abs(mk - mko) <= 1e-9 * mko
+    ctx.destroy()
+
+
+# ------------------------------------------------------ free-running engine --
+@pytest.mark.parametrize("model", ["none", "quadratic"])
+def test_free_running_log_replays_bitwise(P, model):
+    """Free-running engine (device try-locks, tickets): its event log, replayed
+    through the oracle, reproduces every GPU model bitwise."""
+    n, d, U = 8, 1 << 18, 3000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(6)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    X0 = synth.x0_uniform(n, d, seed=12)
+    kw = dict(model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s) \
+        if model == "quadratic" else {}
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, seed=77, **kw)
+    ctx.run(U)
+    ctx.sync()
+    assert ctx.ticket() == U
+    log = ctx.read_log(0)
+    assert len(log) == U and np.array_equal(log["k"], np.arange(U))
+    Xg = read_all(ctx)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s) \
+        if model == "quadratic" else O.OracleProblem()
+    Xo, _ = O.replay(prob, X0, e, r, log_events(log))
+    assert np.array_equal(Xg.view(np.uint32), Xo.view(np.uint32))
+    if model == "none":
+        S0 = X0.astype(np.float64).sum(0)
+        S1 = Xg.astype(np.float64).sum(0)
+        assert np.linalg.norm(S1 - S0) / np.linalg.norm(S0) <= 1e-5
+        assert np.max(np.abs(S1 - S0) / np.abs(X0.astype(np.float64)).sum(0)) <= 1e-5
+    else:
+        cnt = ctx.update_counts()
+        assert sum(cnt.values()) == U
+    ctx.destroy()
+
+
+def test_free_running_straggler_locality(P):
+    """One worker 10x slower: it makes ~10x fewer updates while
+    the others keep their pace."""
+    n, d = 8, 1 << 16
+    e, r = synth.ring(n)
+    st = synth.stragglers(n, slow_worker=0, slow=10.0)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(1, 2),
+                    straggler=st, compute_ns=200_000)
+    ctx.run(4000)
+    ctx.sync()
+    c = ctx.update_counts()
+    others = np.mean([c[w] for w in range(1, n)])
+    assert c[0] < others / 5
+    assert sum(c.values()) == 4000
+    ctx.destroy()
+
+
+def test_full_size_free_running_parity(P):
+    """BASELINE workload (d = 25.6M, n = 8 on one GPU, 10x straggler), the
+    configuration bench.py times: log replay through the oracle is bitwise."""
+    n, d, U = 8, 25_600_000, 32
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(7)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk),
+                    quad_noise_s=s, straggler=synth.stragglers(n), compute_ns=50_000)
+    ctx.run(U)
+    ctx.sync()
+    log = ctx.read_log(0)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, log_events(log))
+    for w in range(n):
+        assert np.array_equal(ctx.read_model(w).view(np.uint32), Xo[w].view(np.uint32)), w
+    ctx.destroy()
+
+
+# --------------------------------------------------------- step / gossip ----
+def test_step_and_gossip_match_oracle(P):
+    n, d = 4, 5000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(8)
+    X0 = synth.x0_uniform(n, d, seed=3)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.05, batch_M=4,
+                    quad_keys=(dk, nk), quad_noise_s=0.2, seed=5)
+    for t in range(40):
+        ctx.step(t % n)
+    ctx.sync()
+    log = ctx.read_log(0)
+    assert len(log) == 40
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=4, gamma=0.05, data_key=dk, noise_key=nk, noise_s=0.2)
+    Xo, _ = O.replay(prob, X0, e, r, log_events(log))
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    ctx.gossip(0, 1)
+    ctx.sync()
+    Xo2, _ = O.replay(O.OracleProblem(), Xo, e, r, [[0, 1, 0, 1]])
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo2.view(np.uint32))
+    ctx.destroy()
+
+
+# ---------------------------------------------------- AllReduce baseline ----
+def test_allreduce_sgd_matches_oracle(P):
+    n, d, R = 8, 10007, 20
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(9)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk),
+                    quad_noise_s=0.5)
+    ctx.allreduce_reset()
+    ctx.allreduce_sgd(R)
+    xg = ctx.allreduce_read_model()
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=0.5)
+    x = np.zeros(d, np.float32)
+    for rr in range(R):
+        G = np.stack([O.gradient(prob, x, k=rr * n + w) for w in range(n)])
+        x = O.allreduce_update(x, G, 0.01)
+    np.testing.assert_allclose(xg, x, rtol=1e-5, atol=1e-6)
+    ctx.destroy()
