@@ -1,0 +1,347 @@
+#!/usr/bin/env python
+"""bench.py -- AD-PSGD hot path on B200: gossip-steps/s at 25.6M parameters.
+
+Workload (BASELINE.json configs[3], "config 4"): a ResNet-50-sized flat model,
+d = 25,600,000 fp32, synthetic quadratic gradients (M = 32, sigma = 0.1,
+gamma = 0.01), n = 8 workers per GPU on one bipartite ring (block placement),
+worker 0 slowed 10x, emulated per-gradient compute t_c.
+One STEP = the system commits U gradient updates through the free-running
+persistent engine (stale-free fused gradient, pair average over HBM/NVLink,
+device try-locks, tickets) followed by the consensus output x_bar.
+
+Contract: python bench.py --gpus N --steps K --warmup W [--impl reference]
+prints ONE JSON line on rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+D_FULL = 25_600_000
+M_BATCH = 32
+SIGMA = 0.1
+GAMMA = 0.01
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--d", type=int, default=D_FULL)
+    ap.add_argument("--workers-per-gpu", type=int, default=8)
+    ap.add_argument("--updates-per-step", type=int, default=0, help="0 = 32 per worker")
+    ap.add_argument("--compute-us", type=float, default=50.0, help="emulated t_c of a 1x worker")
+    ap.add_argument("--straggler", type=float, default=10.0)
+    ap.add_argument("--placement", type=int, default=0)
+    ap.add_argument("--no-extras", action="store_true", help="skip baseline/no-straggler/cpu legs")
+    ap.add_argument("--cpu-events", type=int, default=12)
+    return ap.parse_args()
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled DURING the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev, self.rows, self.proc = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.dev), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            p = [x.strip() for x in line.split(",")]
+            if len(p) == 6:
+                self.rows.append(p)
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+# --------------------------------------------------------- CPU oracle legs --
+def oracle_sample(n, d, events, seed=5):
+    """Time the oracle (as it stands) on `events` events of the same workload."""
+    import numpy as np
+    import synth
+    from oracle import oracle as O
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(seed)
+    s = float(np.float32(SIGMA * math.sqrt(3 * M_BATCH)))
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=M_BATCH, gamma=GAMMA, data_key=dk, noise_key=nk, noise_s=s)
+    ev, _ = synth.schedule_iid(n, e, K=events, seed=seed, local_prob=0.0)
+    X = np.zeros((n, d), np.float32)
+    t0 = time.perf_counter()
+    O.replay(prob, X, e, r, ev)
+    dt = time.perf_counter() - t0
+    pairs = int((ev[:, 1] >= 0).sum())
+    return pairs, dt
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle (this tier's reference arm), rank 0 only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    n = a.workers_per_gpu * a.gpus
+    per_step = 2
+    for _ in range(a.warmup):
+        oracle_sample(n, a.d, per_step)
+    tot_pairs, tot_t = 0, 0.0
+    for _ in range(a.steps):
+        p, t = oracle_sample(n, a.d, per_step)
+        tot_pairs += p
+        tot_t += t
+    v = tot_pairs / tot_t
+    line = {"impl": "reference", "metric": "gossip-steps/s", "value": v, "unit": "gossip-steps/s",
+            "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": 1e3 * tot_t / a.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "data": "synthetic",
+            "config": {"workload": f"config4: quadratic d={a.d}, n={n} ring, M={M_BATCH}, oracle sample",
+                       "parallelism": "none (1 CPU core)"},
+            "cpu_baseline": {"value": v, "unit": "gossip-steps/s", "cores": 1, "kind": "oracle",
+                             "sample": f"{per_step} events of n={n}, d={a.d} per step"},
+            "e2e": {"value": v, "unit": "gossip-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line))
+
+
+# ---------------------------------------------------------------- our arm --
+def main():
+    a = parse()
+    if a.impl == "reference":
+        return run_reference(a)
+    import numpy as np
+    import torch
+    import synth
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_1710_06952_b200 import build as B
+    if rank == 0:
+        B.build()
+    if dist:
+        dist.barrier()
+    import paper_1710_06952_b200 as P
+
+    n = a.workers_per_gpu * world
+    d = a.d
+    U = a.updates_per_step or 32 * n
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(5)
+    s = float(np.float32(SIGMA * math.sqrt(3 * M_BATCH)))
+    strag = synth.stragglers(n, slow_worker=0, slow=a.straggler)
+    cns = int(a.compute_us * 1000)
+
+    def make_ctx(st):
+        return P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=a.placement,
+                         model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
+                         quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16)
+
+    stream = torch.cuda.Stream()
+    out = torch.empty(d, dtype=torch.float32, device="cuda")
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    def maxr(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def sumr(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t)
+        return float(t.item())
+
+    def step(ctx, eng=None):
+        if eng:
+            eng[0].record(stream)
+        ctx.run(U, stream)
+        if eng:
+            eng[1].record(stream)
+        ctx.consensus_mean(out.data_ptr(), with_mk=False, stream=stream)
+
+    def timed(ctx, K, W, engine_events=False):
+        for _ in range(W):
+            step(ctx)
+        torch.cuda.synchronize()
+        ctx.sync()
+        barrier()
+        st0 = ctx.stats()
+        l0 = ctx.launch_count()
+        engs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                for _ in range(K)] if engine_events else [None] * K
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        torch.cuda.synchronize()
+        barrier()
+        with ClockSampler(local) as clk:
+            t0.record(stream)
+            for k in range(K):
+                step(ctx, engs[k])
+            t1.record(stream)
+            torch.cuda.synchronize()
+        ctx.sync()
+        barrier()
+        ms = maxr(t0.elapsed_time(t1))
+        st1 = ctx.stats()
+        eng_ms = sum(x[0].elapsed_time(x[1]) for x in engs) / K if engine_events else None
+        return ms, st0, st1, ctx.launch_count() - l0, clk.summary(), eng_ms
+
+    # ------------------------------------------------ main leg: straggler --
+    ctx = make_ctx(strag)
+    ms, st0, st1, launches, clocks, eng_ms = timed(ctx, a.steps, a.warmup, engine_events=True)
+    pairs = sumr(st1["local_pair_events"] - st0["local_pair_events"])
+    events = sumr(st1["local_events"] - st0["local_events"])
+    loc_bytes = st1["local_bytes"] - st0["local_bytes"]
+    nvl_bytes = sumr(st1["local_nvlink_bytes"] - st0["local_nvlink_bytes"])
+    sec = ms / 1e3
+    gossip_s = pairs / sec
+    upd_s = events / sec
+    # roofline of the dominant kernel (k_engine): algorithmic bytes / launch duration
+    pk = peaks()
+    hbm_peak = pk.get("hbm_gbs", 6650.0)
+    eng_s = eng_ms / 1e3
+    achieved = loc_bytes / a.steps / eng_s / 1e9
+    # e2e: public API with host timing, M_k read back to the host every step
+    for _ in range(2):
+        ctx.run(U)
+        ctx.consensus_mean(out.data_ptr(), with_mk=True)
+    barrier()
+    st_e = ctx.stats()
+    te0 = time.perf_counter()
+    for _ in range(a.steps):
+        ctx.run(U)
+        mk = ctx.consensus_mean(out.data_ptr(), with_mk=True)
+    te = maxr(time.perf_counter() - te0)
+    pairs_e = sumr(ctx.stats()["local_pair_events"] - st_e["local_pair_events"])
+    n_local = len(ctx.local_workers())
+    cnts = ctx.update_counts()
+    ctx.destroy()
+
+    extras = {}
+    if not a.no_extras:
+        # same workload without the straggler
+        c2 = make_ctx(None)
+        ms2, s20, s21, _, _, _ = timed(c2, max(3, a.steps // 2), 2)
+        extras["no_straggler"] = {
+            "gossip_steps_per_s": sumr(s21["local_pair_events"] - s20["local_pair_events"]) / (ms2 / 1e3),
+            "updates_per_s": sumr(s21["local_events"] - s20["local_events"]) / (ms2 / 1e3)}
+        # AllReduce-SGD baseline (NCCL), with and without the straggler
+        ar = {}
+        for tag, stv in (("straggler", strag), ("no_straggler", None)):
+            c3 = make_ctx(stv)
+            c3.allreduce_reset()
+            R = max(4, U // n)
+            c3.allreduce_sgd(2, stream)
+            torch.cuda.synchronize()
+            barrier()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta.record(stream)
+            c3.allreduce_sgd(R, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            msa = maxr(ta.elapsed_time(tb))
+            ar[tag] = {"updates_per_s": R * n / (msa / 1e3), "samples_per_s": R * n * M_BATCH / (msa / 1e3),
+                       "rounds_per_s": R / (msa / 1e3)}
+            c3.destroy()
+            barrier()
+        extras["allreduce_sgd_baseline"] = ar
+        extras["adpsgd_vs_allreduce_updates_ratio_straggler"] = upd_s / ar["straggler"]["updates_per_s"]
+
+    cpu = None
+    if rank == 0 and world == 1 and not a.no_extras:
+        pairs_c, dt_c = oracle_sample(n, d, a.cpu_events)
+        cpu = {"value": pairs_c / dt_c, "unit": "gossip-steps/s", "cores": 1, "kind": "oracle",
+               "sample": f"{a.cpu_events} iid events (ring n={n}, d={d}) of the oracle's Alg. 1 replay"}
+
+    line = {
+        "metric": "gossip-steps/s", "value": gossip_s, "unit": "gossip-steps/s", "n_gpus": world,
+        "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+        "config": {"workload": f"config4: quadratic d={d} fp32, n={n} workers ({a.workers_per_gpu}/GPU) on a "
+                               f"bipartite ring, M={M_BATCH}, worker 0 x{a.straggler}, t_c={a.compute_us}us; "
+                               f"step = {U} committed updates + consensus mean",
+                   "global_batch": U * M_BATCH, "parallelism": f"gossip over {world} GPU(s), "
+                   f"{'block' if a.placement == 0 else 'interleave'} placement",
+                   "l2": "inputs larger than L2 (n x 102.4 MB models)"},
+        "updates_per_s": upd_s, "samples_per_s": upd_s * M_BATCH,
+        "nvlink": {"algorithmic_bytes_per_s": nvl_bytes / sec, "per_gpu_per_direction_gbs":
+                   nvl_bytes / sec / 2 / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / 2 / max(world, 1) / 900e9},
+        "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": None,
+                     "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,
+                     "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
+        "clocks": clocks,
+        "e2e": {"value": pairs_e / te, "unit": "gossip-steps/s",
+                "h2d_bytes_per_step": 136 * n_local * world, "d2h_bytes_per_step": 16 * world,
+                "note": "public API (Context.run + consensus_mean with M_k read back), host wall clock"},
+        "gpu_launches": launches,
+        "update_counts_rank0": cnts,
+    }
+    line.update(extras)
+    if cpu:
+        line["cpu_baseline"] = cpu
+    if rank == 0:
+        print(json.dumps(line))
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -844,6 +844,9 @@ adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, a
     if (!out) return fail(ADPSGD_E_INVALID, "out");
     if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
     cudaStream_t st = c->use(s);
+    // quiesce: every rank's engine (and its P2P stores into our rows) has
+    // finished once this tiny all-reduce completes on our stream
+    if (c->world > 1) NC(ncclAllReduce(c->mk_acc, c->mk_acc, 1, ncclFloat64, ncclSum, c->comm, st));
     CU(launch_consensus_sum(c->models, c->n_local, c->d_pad, c->d, c->sum64, st));
     ++c->launches;
     if (c->world > 1) NC(ncclAllReduce(c->sum64, c->sum64, (size_t)c->d, ncclFloat64, ncclSum, c->comm, st));

@@ -154,7 +154,7 @@ def test_config1_replay_within_1e4(P, kind):
     Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev, bi, T=T)
     ok = c11_ok(Xg, Xo)
     assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum())
-    assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * 0.1
+    assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * 0.5
     ctx.destroy()
 
 
