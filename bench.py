@@ -36,7 +36,7 @@ GAMMA = 0.01
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=30)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--d", type=int, default=D_FULL)
@@ -63,7 +63,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                                          "-i", str(self.dev), "-lms", "100"], stdout=subprocess.PIPE,
+                                          "-i", str(self.dev), "-lms", "50"], stdout=subprocess.PIPE,
                                          stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -75,7 +75,12 @@ class ClockSampler:
         for line in self.proc.stdout:
             p = [x.strip() for x in line.split(",")]
             if len(p) == 6:
-                self.rows.append(p)
+                self.rows.append([time.perf_counter()] + p)
+
+    def window(self, t0, t1):
+        """keep only samples taken inside the timed region [t0, t1] (host clock)"""
+        inside = [r for r in self.rows if t0 <= r[0] <= t1]
+        self.rows = [r[1:] for r in (inside or self.rows[-1:])]
 
     def __exit__(self, *a):
         if self.proc:
@@ -217,24 +222,28 @@ def main():
         ctx.consensus_mean(out.data_ptr(), with_mk=False, stream=stream)
 
     def timed(ctx, K, W, engine_events=False):
-        for _ in range(W):
-            step(ctx)
-        torch.cuda.synchronize()
-        ctx.sync()
-        barrier()
-        st0 = ctx.stats()
-        l0 = ctx.launch_count()
-        engs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
-                for _ in range(K)] if engine_events else [None] * K
-        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        torch.cuda.synchronize()
-        barrier()
         with ClockSampler(local) as clk:
+            time.sleep(0.3)                     # let nvidia-smi start sampling
+            for _ in range(W):
+                step(ctx)
+            torch.cuda.synchronize()
+            ctx.sync()
+            barrier()
+            st0 = ctx.stats()
+            l0 = ctx.launch_count()
+            engs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+                    for _ in range(K)] if engine_events else [None] * K
+            t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            torch.cuda.synchronize()
+            barrier()
+            h0 = time.perf_counter()
             t0.record(stream)
             for k in range(K):
                 step(ctx, engs[k])
             t1.record(stream)
             torch.cuda.synchronize()
+            h1 = time.perf_counter()
+        clk.window(h0, h1)
         ctx.sync()
         barrier()
         ms = maxr(t0.elapsed_time(t1))
