@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--placement", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip baseline/no-straggler/cpu legs")
     ap.add_argument("--cpu-events", type=int, default=12)
+    ap.add_argument("--engine-variant", type=int, default=0, help="0 TMA-staged, 1 register slices")
+    ap.add_argument("--ctas-per-sm", type=int, default=0)
     return ap.parse_args()
 
 
@@ -190,7 +192,8 @@ def main():
     def make_ctx(st):
         return P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=a.placement,
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
-                         quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16)
+                         quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
+                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm)
 
     stream = torch.cuda.Stream()
     out = torch.empty(d, dtype=torch.float32, device="cuda")

@@ -148,8 +148,8 @@ typedef struct {
 
 /* Synthetic quadratic f(x) = 1/2 sum_c h_c (x_c - x*_c)^2.  The
  * stochastic batch-sum gradient (a SUM over the M samples) is
- *   g_c = fl( fl(M*h_c) * fl(xhat_c - x*_c) ) + fl( s * (2r-1) )
- * where the single uniform draw (2r-1)*s has the variance M*sigma^2 of the sum
+ *   g_c = fl( fl(M*h_c) * fl(xhat_c - x*_c) ) + fl( s * v_c )
+ * with v_c = (u>>9) * 2^-22 - 1 (23-bit uniform grid on [-1,1)); the single draw s*v_c has the variance M*sigma^2 of the sum
  * of M per-sample uniform noises.  Every op is one rounded fp32 op (no FMA):
  * this is the workload's definition, so the oracle evaluates it exactly.    */
 static void quad_data(const oracle_problem* p, int64_t c, float* h, float* xs) {
@@ -174,9 +174,8 @@ int oracle_quadratic_grad(const oracle_problem* p, int64_t d, const float* xhat,
     float h, xs;
     quad_data(p, c, &h, &xs);
     uint32_t u = oracle_lowbias32((uint32_t)c ^ kk);
-    float r = (float)(u >> 8) * (1.0f / 16777216.0f);   /* exact, in [0,1) */
-    float two_r = 2.0f * r;                              /* exact */
-    float v = two_r - 1.0f;                              /* exact */
+    float m = (float)(u >> 9) * (1.0f / 4194304.0f);    /* exact: (u>>9) * 2^-22, in [0,2) */
+    float v = m - 1.0f;                                  /* exact, uniform grid in [-1,1) */
     float noise = p->noise_s * v;
     float mh = Mf * h;
     float diff = xhat[c] - xs;

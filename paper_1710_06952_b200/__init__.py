@@ -54,7 +54,7 @@ class Config(C.Structure):
                 ("data_y", C.c_void_p), ("mlp_in", C.c_int32), ("mlp_hid", C.c_int32),
                 ("mlp_out", C.c_int32), ("x0", C.c_void_p), ("x0_per_worker", C.c_void_p),
                 ("straggler", C.c_void_p), ("compute_ns", C.c_int64), ("engine_ctas_per_sm", C.c_int32),
-                ("engine_threads", C.c_int32), ("log_capacity", C.c_int64)]
+                ("engine_variant", C.c_int32), ("log_capacity", C.c_int64)]
 
 
 class Event(C.Structure):
@@ -130,7 +130,7 @@ class Context:
                  worker_rank=None, gamma=0.0, batch_M=1, T=0, seed=0, model=MODEL_NONE,
                  quad_keys=(0, 0), quad_noise_s=0.0, data_A=None, data_b=None, data_y=None,
                  mlp_dims=(0, 0, 0), x0=None, x0_per_worker=None, straggler=None, compute_ns=0,
-                 engine_ctas_per_sm=0, engine_threads=0, log_capacity=0, connect=True, pg=None):
+                 engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, connect=True, pg=None):
         self.n, self.d, self.rank, self.world = int(n), int(d), int(rank), int(world_size)
         e = _arr(np.asarray(edges).reshape(-1, 2), np.int32)
         r = _arr(role, np.int8)
@@ -152,7 +152,7 @@ class Context:
         x0a, x0w, st = _arr(x0, np.float32), _arr(x0_per_worker, np.float32), _arr(straggler, np.float32)
         keep += [x0a, x0w, st]
         cfg.x0, cfg.x0_per_worker, cfg.straggler = _ptr(x0a), _ptr(x0w), _ptr(st)
-        cfg.compute_ns, cfg.engine_ctas_per_sm, cfg.engine_threads = int(compute_ns), engine_ctas_per_sm, engine_threads
+        cfg.compute_ns, cfg.engine_ctas_per_sm, cfg.engine_variant = int(compute_ns), engine_ctas_per_sm, engine_variant
         cfg.log_capacity = log_capacity
         h = C.c_void_p()
         _chk(lib().adpsgd_init(C.byref(g), self.n, self.d, C.byref(cfg), C.byref(h)), "adpsgd_init")

@@ -95,15 +95,20 @@ __host__ __device__ __forceinline__ uint32_t quad_event_key_h(uint32_t noise_key
   return lb(lb((uint32_t)k ^ noise_key) ^ (uint32_t)(k >> 32));
 }
 
+// The three uniform grids are built from bits instead of I2F + scale (same
+// exact values, no conversion-pipe instructions):
+//   (w>>16) * 2^-16        = bits(0x3f800000 | (w>>16)<<7) - 1
+//   (w&0xffff) * 2^-15 - 1 = bits(0x40000000 | (w&0xffff)<<7) - 3
+//   (u>>9) * 2^-22 - 1     = bits(0x40000000 | u>>9) - 3
+// (each subtraction is exact by Sterbenz).
 __device__ __forceinline__ float quad_grad(float xhat, uint32_t c, uint32_t data_key, uint32_t kk,
                                            float Mf, float s) {
   const uint32_t w = lowbias32(c ^ data_key);
-  const float uh = __fmul_rn(__uint2float_rn(w >> 16), 1.0f / 65536.0f);      // exact
+  const float uh = __fsub_rn(__uint_as_float(0x3f800000u | ((w >> 9) & 0x007fff80u)), 1.0f);
   const float h = __fadd_rn(0.01f, __fmul_rn(0.99f, uh));
-  const float xs = __fsub_rn(__fmul_rn(__uint2float_rn(w & 0xffffu), 1.0f / 32768.0f), 1.0f);
+  const float xs = __fsub_rn(__uint_as_float(0x40000000u | ((w << 7) & 0x007fff80u)), 3.0f);
   const uint32_t u = lowbias32(c ^ kk);
-  const float r = __fmul_rn(__uint2float_rn(u >> 8), 1.0f / 16777216.0f);     // exact
-  const float v = __fsub_rn(__fmul_rn(2.0f, r), 1.0f);                         // exact
+  const float v = __fsub_rn(__uint_as_float(0x40000000u | (u >> 9)), 3.0f);
   const float noise = __fmul_rn(s, v);
   const float det = __fmul_rn(__fmul_rn(Mf, h), __fsub_rn(xhat, xs));
   return __fadd_rn(det, noise);
@@ -177,6 +182,103 @@ __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext,
   a = make_float4(out[0], out[1], out[2], out[3]);
   if (kPair) b = make_float4(mv[0], mv[1], mv[2], mv[3]);
 }
+
+// ------------------------------------------------- bulk-copy (TMA) staging ---
+// cp.async.bulk global->shared copies completing on an mbarrier (complete_tx),
+// so a CTA keeps kStages tiles of x_i / x_j in flight (HBM or NVLink peer
+// addresses alike) without holding them in registers.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  uint32_t ok;
+  do {
+    asm volatile(
+        "{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+        : "=r"(ok)
+        : "r"(smem_u32(b)), "r"(parity)
+        : "memory");
+  } while (!ok);
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+// order this thread's (and, after a barrier + fence, the CTA's) generic-proxy
+// accesses before subsequent async-proxy (bulk copy) accesses
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.global;" ::: "memory");
+}
+
+// Per-CTA staging pipeline state.  `consumed` advances identically in every
+// thread; `bar[s]` completes once per use of stage s (parity = use count & 1).
+template <int kTile4, int kStages>
+struct Stager {
+  float4* buf;      // [kStages][2][kTile4]
+  uint64_t* bar;    // [kStages]
+  uint32_t consumed;
+
+  __device__ __forceinline__ void issue(uint32_t g, const float4* xi4, const float4* xj4, long long base,
+                                        long long hi) {
+    const uint32_t s = g % kStages;
+    const long long cnt = (hi - base) < kTile4 ? (hi - base) : kTile4;
+    const uint32_t bytes = (uint32_t)cnt * 16u;
+    mbar_arrive_tx(bar + s, xj4 ? 2u * bytes : bytes);
+    bulk_g2s(buf + (size_t)s * 2 * kTile4, xi4 + base, bytes, bar + s);
+    if (xj4) bulk_g2s(buf + (size_t)s * 2 * kTile4 + kTile4, xj4 + base, bytes, bar + s);
+  }
+
+  // One event over float4 range [lo, hi) with all threads of the CTA.
+  template <bool kPair, int kGrad>
+  __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long lo, long long hi, long long d,
+                                      float gamma, const QuadParams& q, uint32_t kk) {
+    const long long n_t = (hi - lo + kTile4 - 1) / kTile4;
+    if (n_t <= 0) return;
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      for (long long t = 0; t < n_t && t < kStages; ++t)
+        issue(consumed + (uint32_t)t, xi4, kPair ? xj4 : nullptr, lo + t * kTile4, hi);
+    }
+    for (long long t = 0; t < n_t; ++t) {
+      const uint32_t g = consumed + (uint32_t)t;
+      const uint32_t s = g % kStages;
+      mbar_wait(bar + s, (g / kStages) & 1u);
+      const float4* sa = buf + (size_t)s * 2 * kTile4;
+      const float4* sb = sa + kTile4;
+      const long long base = lo + t * kTile4;
+#pragma unroll
+      for (int u = 0; u < kTile4 / 512; ++u) {
+        const int off = u * (int)blockDim.x + (int)threadIdx.x;
+        const long long idx = base + off;
+        if (off < kTile4 && idx < hi) {
+          float4 a = sa[off];
+          float4 b = kPair ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
+          update4<kPair, kGrad>(a, b, make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
+                                (uint32_t)(idx * 4), d, gamma, q, kk);
+          if (kPair) st_cg4(xj4 + idx, b);
+          st_cg4(xi4 + idx, a);
+        }
+      }
+      __syncthreads();                       // stage s fully read by every thread
+      if (threadIdx.x == 0 && t + kStages < n_t)
+        issue(g + kStages, xi4, kPair ? xj4 : nullptr, lo + (t + kStages) * kTile4, hi);
+    }
+    consumed += (uint32_t)n_t;
+  }
+};
 
 // Process float4 range [lo, hi) of one event with `nthreads` threads of a CTA.
 // Loads of the (possibly remote) partner row are issued first, U-deep, so that

@@ -186,22 +186,42 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
 }
 
-template <bool kPair, int kGrad>
-__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e) {
+constexpr int kTile4 = 1024;             // float4 per stream per stage (16 KB)
+constexpr int kStages = 3;
+constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
+
+template <bool kTma, bool kPair, int kGrad>
+__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e,
+                                      Stager<kTile4, kStages>& stg) {
   const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = lo + per < p.n4 ? lo + per : p.n4;
   const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
-  event_range<kPair, kGrad, kEngineUnroll>(reinterpret_cast<float4*>(e.xi),
-                                           reinterpret_cast<float4*>(e.xj), nullptr, nullptr, lo,
-                                           hi, threadIdx.x, blockDim.x, p.d, p.gamma, p.q, kk);
+  if (kTma) {
+    stg.template run<kPair, kGrad>(reinterpret_cast<float4*>(e.xi), reinterpret_cast<float4*>(e.xj), lo,
+                                   hi, p.d, p.gamma, p.q, kk);
+  } else {
+    event_range<kPair, kGrad, kEngineUnroll>(reinterpret_cast<float4*>(e.xi),
+                                             reinterpret_cast<float4*>(e.xj), nullptr, nullptr, lo,
+                                             hi, threadIdx.x, blockDim.x, p.d, p.gamma, p.q, kk);
+  }
 }
 
+template <bool kTma>
 __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_constant__ EngineParams p) {
+  extern __shared__ __align__(128) unsigned char dyn_smem[];
   __shared__ unsigned int done_seq[kMaxLocal];
   __shared__ int s_pick;
   __shared__ unsigned int s_seq;
   __shared__ SmemSlot s_ev;
+  Stager<kTile4, kStages> stg;
+  stg.buf = reinterpret_cast<float4*>(dyn_smem);
+  stg.bar = reinterpret_cast<uint64_t*>(dyn_smem + (size_t)kStages * 2 * kTile4 * sizeof(float4));
+  stg.consumed = 0;
+  if (kTma && threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(stg.bar + s, 1);
+    mbar_fence_init();
+  }
   for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) done_seq[s] = 0u;
   __syncthreads();
   const int L = p.n_local;
@@ -251,10 +271,10 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     if (pick >= 0) {
       const SmemSlot e = s_ev;
       if (e.pair) {
-        if (e.grad) slice<true, kGradQuadInline>(p, e);
-        else slice<true, kGradNone>(p, e);
+        if (e.grad) slice<kTma, true, kGradQuadInline>(p, e, stg);
+        else slice<kTma, true, kGradNone>(p, e, stg);
       } else if (e.grad) {
-        slice<false, kGradQuadInline>(p, e);
+        slice<kTma, false, kGradQuadInline>(p, e, stg);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -271,16 +291,27 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
 
 }  // namespace
 
-int engine_max_ctas_per_sm(int threads) {
+int engine_max_ctas_per_sm(int threads, int variant) {
   int n = 0;
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine, threads, 0);
+  if (variant == 0) {
+    cudaFuncSetAttribute(k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine<true>, threads, kTmaSmem);
+  } else {
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine<false>, threads, 0);
+  }
   return n;
 }
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s) {
   EngineParams pp = p;
   void* args[] = {&pp};
-  return cudaLaunchCooperativeKernel((const void*)k_engine, dim3(grid), dim3(threads), args, 0, s);
+  if (threads != kEngineThreads) return cudaErrorInvalidValue;
+  if (p.variant == 0) {
+    cudaFuncSetAttribute(k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+    return cudaLaunchCooperativeKernel((const void*)k_engine<true>, dim3(grid), dim3(threads), args,
+                                       kTmaSmem, s);
+  }
+  return cudaLaunchCooperativeKernel((const void*)k_engine<false>, dim3(grid), dim3(threads), args, 0, s);
 }
 
 }  // namespace adp

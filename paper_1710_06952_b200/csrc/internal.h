@@ -59,10 +59,11 @@ struct EngineParams {
   long long compute_ns;
   uint2 seed;
   unsigned long long watchdog_ns;
+  int variant;                     // 0 = bulk-copy (TMA) staged slices, 1 = register slices
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);
-int engine_max_ctas_per_sm(int threads);
+int engine_max_ctas_per_sm(int threads, int variant);
 
 // ---------------------------------------------------- standalone kernels ----
 // Pair/local update with external, inline-quadratic, snapshot-quadratic or no gradient.

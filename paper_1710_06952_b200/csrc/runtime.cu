@@ -79,7 +79,7 @@ struct adpsgd_ctx {
   uint64_t seed = 0;
   QuadParams q{};
   long long compute_ns = 0;
-  int engine_cps = 0, engine_threads = 512;
+  int engine_cps = 0, engine_threads = 512, engine_variant = 0;
   long long log_cap = 1 << 20;
   std::vector<int32_t> edges;
   std::vector<int8_t> role;
@@ -396,7 +396,8 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.watchdog_ns = 60ull * 1000000000ull;
   int dev_sms = 0;
   CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
-  int occ = engine_max_ctas_per_sm(c->engine_threads);
+  p.variant = c->engine_variant;
+  int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
@@ -518,8 +519,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->q.s = cfg->quad_noise_s;
   c->compute_ns = cfg->compute_ns;
   c->engine_cps = cfg->engine_ctas_per_sm;
-  c->engine_threads = cfg->engine_threads > 0 ? cfg->engine_threads : 512;
-  if (c->engine_threads % 32 || c->engine_threads > 512) return fail(ADPSGD_E_INVALID, "engine_threads");
+  c->engine_threads = 512;
+  c->engine_variant = cfg->engine_variant;
+  if (c->engine_variant < 0 || c->engine_variant > 1) return fail(ADPSGD_E_INVALID, "engine_variant");
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   ST(check_graph(c.get(), g));
