@@ -149,12 +149,23 @@ typedef struct {
 /* Synthetic quadratic f(x) = 1/2 sum_c h_c (x_c - x*_c)^2.  The
  * stochastic batch-sum gradient (a SUM over the M samples) is
  *   g_c = fl( fl(M*h_c) * fl(xhat_c - x*_c) ) + fl( s * v_c )
- * with v_c = (u>>9) * 2^-22 - 1 (23-bit uniform grid on [-1,1)); the single draw s*v_c has the variance M*sigma^2 of the sum
- * of M per-sample uniform noises.  Every op is one rounded fp32 op (no FMA):
- * this is the workload's definition, so the oracle evaluates it exactly.    */
+ * with v_c = (u>>9) * 2^-22 - 1 (23-bit uniform grid on [-1,1)) and
+ * u = mix(c ^ K_k); the single draw s*v_c has the variance M*sigma^2 of the sum
+ * of M per-sample uniform noises.  The landscape word is the Weyl sequence
+ * w_c = (c * 0x9E3779B1) ^ data_key: h_c from its high 16 bits, x*_c from its
+ * low 16 bits (definition v3).  Every op is
+ * one rounded fp32 op (no FMA): this is the workload's definition, so the
+ * oracle evaluates it exactly.                                               */
+static uint32_t quad_noise_mix(uint32_t x) {
+  x *= 0x7feb352du;
+  x ^= x >> 15;
+  x *= 0x846ca68bu;
+  return x;
+}
+
 static void quad_data(const oracle_problem* p, int64_t c, float* h, float* xs) {
   if (p->h_explicit) { *h = p->h_explicit[c]; *xs = p->xstar_explicit[c]; return; }
-  uint32_t w = oracle_lowbias32((uint32_t)c ^ p->data_key);
+  uint32_t w = ((uint32_t)c * 0x9E3779B1u) ^ p->data_key;
   float u_h = (float)(w >> 16) * (1.0f / 65536.0f);     /* exact */
   float t = 0.99f * u_h;
   *h = 0.01f + t;
@@ -173,7 +184,7 @@ int oracle_quadratic_grad(const oracle_problem* p, int64_t d, const float* xhat,
   for (int64_t c = 0; c < d; ++c) {
     float h, xs;
     quad_data(p, c, &h, &xs);
-    uint32_t u = oracle_lowbias32((uint32_t)c ^ kk);
+    uint32_t u = quad_noise_mix((uint32_t)c ^ kk);
     float m = (float)(u >> 9) * (1.0f / 4194304.0f);    /* exact: (u>>9) * 2^-22, in [0,2) */
     float v = m - 1.0f;                                  /* exact, uniform grid in [-1,1) */
     float noise = p->noise_s * v;

@@ -80,7 +80,8 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint2 k) {
 // ------------------------------------------------------- synthetic quadratic --
 // f(x) = 1/2 sum_c h_c (x_c - x*_c)^2; batch-SUM stochastic gradient
 //   g_c = fl(fl(M h_c) fl(xhat_c - x*_c)) + fl(s (2r-1))
-// with h_c, x*_c from lowbias32(c ^ data_key) and r from lowbias32(c ^ K_k),
+// with h_c, x*_c from the landscape word w_c and the noise grid v_c from the
+// noise word (definition v3),
 // K_k = lowbias32(lowbias32(lo(k) ^ noise_key) ^ hi(k)).
 struct QuadParams {
   uint32_t data_key, noise_key;
@@ -101,13 +102,17 @@ __host__ __device__ __forceinline__ uint32_t quad_event_key_h(uint32_t noise_key
 //   (w&0xffff) * 2^-15 - 1 = bits(0x40000000 | (w&0xffff)<<7) - 3
 //   (u>>9) * 2^-22 - 1     = bits(0x40000000 | u>>9) - 3
 // (each subtraction is exact by Sterbenz).
+// Landscape word: Weyl sequence (c * 0x9E3779B1) ^ data_key (1 IMAD + 1 LOP3);
+// noise word: two multiplies around one xorshift of (c ^ K_k), top 23 bits used.
 __device__ __forceinline__ float quad_grad(float xhat, uint32_t c, uint32_t data_key, uint32_t kk,
                                            float Mf, float s) {
-  const uint32_t w = lowbias32(c ^ data_key);
+  const uint32_t w = (c * 0x9E3779B1u) ^ data_key;
   const float uh = __fsub_rn(__uint_as_float(0x3f800000u | ((w >> 9) & 0x007fff80u)), 1.0f);
   const float h = __fadd_rn(0.01f, __fmul_rn(0.99f, uh));
   const float xs = __fsub_rn(__uint_as_float(0x40000000u | ((w << 7) & 0x007fff80u)), 3.0f);
-  const uint32_t u = lowbias32(c ^ kk);
+  uint32_t u = (c ^ kk) * 0x7feb352du;
+  u ^= u >> 15;
+  u *= 0x846ca68bu;
   const float v = __fsub_rn(__uint_as_float(0x40000000u | (u >> 9)), 3.0f);
   const float noise = __fmul_rn(s, v);
   const float det = __fmul_rn(__fmul_rn(Mf, h), __fsub_rn(xhat, xs));
@@ -241,16 +246,21 @@ struct Stager {
     if (xj4) bulk_g2s(buf + (size_t)s * 2 * kTile4 + kTile4, xj4 + base, bytes, bar + s);
   }
 
-  // One event over float4 range [lo, hi) with all threads of the CTA.
+  // One event over the float4 range [0, hi): this CTA takes tiles first,
+  // first + step, first + 2*step, ... (interleaved across the grid, so all
+  // CTAs sweep the rows together -- measured ~5% more HBM throughput than
+  // contiguous per-CTA slices, tools/membench.cu).
   template <bool kPair, int kGrad>
-  __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long lo, long long hi, long long d,
-                                      float gamma, const QuadParams& q, uint32_t kk) {
-    const long long n_t = (hi - lo + kTile4 - 1) / kTile4;
+  __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long first, long long step,
+                                      long long hi, long long d, float gamma, const QuadParams& q,
+                                      uint32_t kk) {
+    const long long tot = (hi + kTile4 - 1) / kTile4;
+    const long long n_t = tot > first ? (tot - first + step - 1) / step : 0;
     if (n_t <= 0) return;
     if (threadIdx.x == 0) {
       fence_proxy_async();
       for (long long t = 0; t < n_t && t < kStages; ++t)
-        issue(consumed + (uint32_t)t, xi4, kPair ? xj4 : nullptr, lo + t * kTile4, hi);
+        issue(consumed + (uint32_t)t, xi4, kPair ? xj4 : nullptr, (first + t * step) * kTile4, hi);
     }
     for (long long t = 0; t < n_t; ++t) {
       const uint32_t g = consumed + (uint32_t)t;
@@ -258,7 +268,7 @@ struct Stager {
       mbar_wait(bar + s, (g / kStages) & 1u);
       const float4* sa = buf + (size_t)s * 2 * kTile4;
       const float4* sb = sa + kTile4;
-      const long long base = lo + t * kTile4;
+      const long long base = (first + t * step) * kTile4;
 #pragma unroll
       for (int u = 0; u < kTile4 / 512; ++u) {
         const int off = u * (int)blockDim.x + (int)threadIdx.x;
@@ -274,7 +284,7 @@ struct Stager {
       }
       __syncthreads();                       // stage s fully read by every thread
       if (threadIdx.x == 0 && t + kStages < n_t)
-        issue(g + kStages, xi4, kPair ? xj4 : nullptr, lo + (t + kStages) * kTile4, hi);
+        issue(g + kStages, xi4, kPair ? xj4 : nullptr, (first + (t + kStages) * step) * kTile4, hi);
     }
     consumed += (uint32_t)n_t;
   }

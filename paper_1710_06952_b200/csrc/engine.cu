@@ -38,6 +38,7 @@ struct SmemSlot {                  // tid 0 copies the running event here for th
   long long k;
   int grad;
   int pair;
+  int cross;                       // partner row lives on another GPU (P2P stores)
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -186,21 +187,21 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
 }
 
-constexpr int kTile4 = 1024;             // float4 per stream per stage (16 KB)
-constexpr int kStages = 3;
+constexpr int kTile4 = 512;              // float4 per stream per stage (8 KB)
+constexpr int kStages = 4;
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
 
 template <bool kTma, bool kPair, int kGrad>
 __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e,
                                       Stager<kTile4, kStages>& stg) {
-  const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
-  const long long lo = (long long)blockIdx.x * per;
-  const long long hi = lo + per < p.n4 ? lo + per : p.n4;
   const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
   if (kTma) {
-    stg.template run<kPair, kGrad>(reinterpret_cast<float4*>(e.xi), reinterpret_cast<float4*>(e.xj), lo,
-                                   hi, p.d, p.gamma, p.q, kk);
+    stg.template run<kPair, kGrad>(reinterpret_cast<float4*>(e.xi), reinterpret_cast<float4*>(e.xj),
+                                   blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk);
   } else {
+    const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
+    const long long lo = (long long)blockIdx.x * per;
+    const long long hi = lo + per < p.n4 ? lo + per : p.n4;
     event_range<kPair, kGrad, kEngineUnroll>(reinterpret_cast<float4*>(e.xi),
                                              reinterpret_cast<float4*>(e.xj), nullptr, nullptr, lo,
                                              hi, threadIdx.x, blockDim.x, p.d, p.gamma, p.q, kk);
@@ -244,6 +245,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           const unsigned int fl = *(volatile unsigned int*)&sl->flags;
           s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
           s_ev.pair = s_ev.xj != nullptr;
+          s_ev.cross = *(volatile int*)&sl->cross;
         }
       }
       if (pick == -1) {
@@ -279,7 +281,11 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
       __syncthreads();
       if (threadIdx.x == 0) {
         done_seq[pick] = s_seq;
-        __threadfence_system();           // this CTA's slice (incl. P2P stores) is visible
+        // this CTA's slice is visible before its arrival; P2P stores need the
+        // system-scope fence, local ones only gpu scope (the committing CTA
+        // issues fence.sys before the cross-GPU release, which is cumulative)
+        if (e.cross) __threadfence_system();
+        else __threadfence();
         if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) commit(p, pick);
       }
     } else if (threadIdx.x == 0) {

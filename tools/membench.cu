@@ -1,0 +1,209 @@
+// membench.cu -- HBM streaming microbenchmarks that shape the fused gossip pass.
+// nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/membench tools/membench.cu
+// Patterns on d = 25.6M fp32 rows: copy (1R1W), pair average (2R2W).
+#include <cstdio>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int U, int MODE>   // MODE 0 ldcg/stcg, 1 default ld/st, 2 ld + st.cs (evict-first)
+__global__ void avg_slice(float4* xi, float4* xj, long long n4, int pair) {
+  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long long lo = blockIdx.x * per, hi = min(lo + per, n4);
+  for (long long base = lo + threadIdx.x; base < hi; base += (long long)blockDim.x * U) {
+    float4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long i = base + (long long)u * blockDim.x;
+      if (i < hi) {
+        if (pair) b[u] = MODE == 0 ? __ldcg(xj + i) : xj[i];
+        a[u] = MODE == 0 ? __ldcg(xi + i) : xi[i];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long i = base + (long long)u * blockDim.x;
+      if (i < hi) {
+        float4 m = a[u];
+        if (pair) { m.x = (a[u].x + b[u].x) * 0.5f; m.y = (a[u].y + b[u].y) * 0.5f; m.z = (a[u].z + b[u].z) * 0.5f; m.w = (a[u].w + b[u].w) * 0.5f; }
+        else { m.x += 1.f; }
+        if (MODE == 2) { if (pair) __stcs(xj + i, m); __stcs(xi + i, m); }
+        else if (MODE == 0) { if (pair) __stcg(xj + i, m); __stcg(xi + i, m); }
+        else { if (pair) xj[i] = m; xi[i] = m; }
+      }
+    }
+  }
+}
+
+template <int U>
+__global__ void avg_stride(float4* xi, float4* xj, long long n4, int pair) {
+  const long long T = (long long)gridDim.x * blockDim.x;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < n4; base += T * U) {
+    float4 a[U], b[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { long long i = base + u * T; if (i < n4) { if (pair) b[u] = __ldcg(xj + i); a[u] = __ldcg(xi + i); } }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      long long i = base + u * T;
+      if (i < n4) {
+        float4 m = a[u];
+        if (pair) { m.x = (a[u].x + b[u].x) * 0.5f; m.y = (a[u].y + b[u].y) * 0.5f; m.z = (a[u].z + b[u].z) * 0.5f; m.w = (a[u].w + b[u].w) * 0.5f; } else m.x += 1.f;
+        if (pair) __stcg(xj + i, m);
+        __stcg(xi + i, m);
+      }
+    }
+  }
+}
+
+// bulk-copy loads (+ STG or bulk-copy stores)
+template <int TILE4, int S, bool BULKST, bool IL = false>
+__global__ void avg_tma(float4* xi, float4* xj, long long n4, int pair) {
+  extern __shared__ __align__(128) unsigned char sm[];
+  float4* buf = (float4*)sm;
+  uint64_t* bar = (uint64_t*)(sm + (size_t)S * 2 * TILE4 * 16);
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(bar + s)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long per = (n4 + gridDim.x - 1) / gridDim.x;
+  const long long lo = IL ? 0 : blockIdx.x * per, hi = IL ? n4 : min(lo + per, n4);
+  const long long tot_t = (n4 + TILE4 - 1) / TILE4;
+  const long long nt = IL ? (tot_t > blockIdx.x ? (tot_t - blockIdx.x + gridDim.x - 1) / gridDim.x : 0)
+                          : (hi - lo + TILE4 - 1) / TILE4;
+  auto tbase = [&](long long t) { return IL ? (blockIdx.x + t * gridDim.x) * TILE4 : lo + t * TILE4; };
+  auto issue = [&](long long t) {
+    int s = t % S;
+    long long base = tbase(t);
+    uint32_t bytes = (uint32_t)min((long long)TILE4, hi - base) * 16;
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(bar + s)), "r"(pair ? 2 * bytes : bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(smem_u32(buf + (size_t)s * 2 * TILE4)), "l"(xi + base), "r"(bytes), "r"(smem_u32(bar + s)) : "memory");
+    if (pair) asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(smem_u32(buf + (size_t)s * 2 * TILE4 + TILE4)), "l"(xj + base), "r"(bytes), "r"(smem_u32(bar + s)) : "memory");
+  };
+  if (threadIdx.x == 0) for (long long t = 0; t < nt && t < S; ++t) issue(t);
+  for (long long t = 0; t < nt; ++t) {
+    int s = t % S;
+    uint32_t ph = (t / S) & 1, ok;
+    do { asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }" : "=r"(ok) : "r"(smem_u32(bar + s)), "r"(ph) : "memory"); } while (!ok);
+    float4* sa = buf + (size_t)s * 2 * TILE4;
+    float4* sb = sa + TILE4;
+    long long base = tbase(t);
+    long long cnt = min((long long)TILE4, hi - base);
+    for (int off = threadIdx.x; off < cnt; off += blockDim.x) {
+      float4 a = sa[off], m = a;
+      if (pair) { float4 b = sb[off]; m.x = (a.x + b.x) * 0.5f; m.y = (a.y + b.y) * 0.5f; m.z = (a.z + b.z) * 0.5f; m.w = (a.w + b.w) * 0.5f; } else m.x += 1.f;
+      if (BULKST) { sa[off] = m; if (pair) sb[off] = m; }
+      else { if (pair) __stcg(xj + base + off, m); __stcg(xi + base + off, m); }
+    }
+    if (BULKST) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        uint32_t bytes = (uint32_t)cnt * 16;
+        asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" :: "l"(xi + base), "r"(smem_u32(sa)), "r"(bytes) : "memory");
+        if (pair) asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" :: "l"(xj + base), "r"(smem_u32(sb)), "r"(bytes) : "memory");
+        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");   // smem reusable
+      }
+      __syncthreads();
+    } else {
+      __syncthreads();
+    }
+    if (threadIdx.x == 0 && t + S < nt) issue(t + S);
+  }
+  if (BULKST && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int sms;
+
+template <typename F>
+float timeit(F f, int iters) {
+  cudaEvent_t a, b;
+  cudaEventCreate(&a); cudaEventCreate(&b);
+  f(); f();
+  cudaDeviceSynchronize();
+  cudaEventRecord(a);
+  for (int i = 0; i < iters; ++i) f();
+  cudaEventRecord(b);
+  cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  return ms / iters;
+}
+
+int main() {
+  const long long d = 25600000, n4 = d / 4;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float4 *xi, *xj;
+  CK(cudaMalloc(&xi, d * 4)); CK(cudaMalloc(&xj, d * 4));
+  CK(cudaMemset(xi, 0, d * 4)); CK(cudaMemset(xj, 0, d * 4));
+  const int it = 30;
+  for (int pair = 0; pair <= 1; ++pair) {
+    double bytes = (pair ? 16.0 : 8.0) * d;
+    printf("=== %s ===\n", pair ? "pair average 2R2W" : "local update 1R1W");
+#define RUN(name, launch) { float ms = timeit([&] { launch; }, it); CK(cudaGetLastError()); printf("%-44s %8.1f us %7.0f GB/s\n", name, ms * 1e3, bytes / (ms / 1e3) / 1e9); }
+    for (int cps = 1; cps <= 4; cps *= 2) {
+      char nm[128];
+      snprintf(nm, 128, "slice U4 ldcg 512thr x%d/SM", cps); RUN(nm, (avg_slice<4, 0><<<sms * cps, 512>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "slice U8 ldcg 256thr x%d/SM", cps * 2); RUN(nm, (avg_slice<8, 0><<<sms * cps * 2, 256>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "slice U4 default 512thr x%d/SM", cps); RUN(nm, (avg_slice<4, 1><<<sms * cps, 512>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "slice U4 st.cs 512thr x%d/SM", cps); RUN(nm, (avg_slice<4, 2><<<sms * cps, 512>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "stride U4 512thr x%d/SM", cps); RUN(nm, (avg_stride<4><<<sms * cps, 512>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 1024, S = 3;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(avg_tma<T, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("tma ld T1024 S3 + stg, 2/SM", (avg_tma<T, S, false><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+      RUN("tma ld T1024 S3 + bulk st, 2/SM", (avg_tma<T, S, true><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 512, S = 4;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(avg_tma<T, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("tma ld T512 S4 + stg, 3/SM", (avg_tma<T, S, false><<<sms * 3, 256, smem>>>(xi, xj, n4, pair)));
+      RUN("tma ld T512 S4 + bulk st, 3/SM", (avg_tma<T, S, true><<<sms * 3, 256, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 2048, S = 3;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(avg_tma<T, S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("tma ld T2048 S3 + stg, 1/SM", (avg_tma<T, S, false><<<sms, 1024, smem>>>(xi, xj, n4, pair)));
+      RUN("tma ld T2048 S3 + bulk st, 1/SM", (avg_tma<T, S, true><<<sms, 1024, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 512, S = 4;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("IL tma ld T512 S4 + stg 512thr, 2/SM", (avg_tma<T, S, false, true><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+      RUN("IL tma ld T512 S4 + stg 256thr, 3/SM", (avg_tma<T, S, false, true><<<sms * 3, 256, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 1024, S = 3;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("IL tma ld T1024 S3 + stg 512thr, 2/SM", (avg_tma<T, S, false, true><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 256, S = 6;
+      size_t smem = (size_t)S * 2 * T * 16 + 64;
+      cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN("IL tma ld T256 S6 + stg 256thr, 4/SM", (avg_tma<T, S, false, true><<<sms * 4, 256, smem>>>(xi, xj, n4, pair)));
+      RUN("IL tma ld T256 S6 + stg 256thr, 2/SM", (avg_tma<T, S, false, true><<<sms * 2, 256, smem>>>(xi, xj, n4, pair)));
+    }
+    for (int cps = 1; cps <= 2; ++cps) {
+      char nm[128];
+      snprintf(nm, 128, "stride U8 256thr x%d/SM", 2 * cps); RUN(nm, (avg_stride<8><<<sms * cps * 2, 256>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "stride U2 512thr x%d/SM", cps); RUN(nm, (avg_stride<2><<<sms * cps, 512>>>(xi, xj, n4, pair)));
+      snprintf(nm, 128, "stride U4 1024thr x%d/SM", cps); RUN(nm, (avg_stride<4><<<sms * cps, 1024>>>(xi, xj, n4, pair)));
+    }
+    // reference: cudaMemcpy device-to-device (1R1W of 4d bytes)
+    if (!pair) RUN("cudaMemcpy D2D (1R1W)", (cudaMemcpyAsync(xj, xi, d * 4, cudaMemcpyDeviceToDevice)));
+  }
+  return 0;
+}
