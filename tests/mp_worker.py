@@ -1,0 +1,132 @@
+"""Multi-process (one rank per GPU) parity worker, launched by tests/test_multigpu.py
+through torch.distributed.run.  Rank 0 compares against the oracle and exits
+non-zero on any mismatch.
+
+Checks:
+  1. engine replay of a pure-gossip schedule whose ring edges cross GPUs
+     (interleave placement: every edge is an NVLink edge) -- bitwise;
+  2. engine replay with the quadratic (block placement) -- bitwise;
+  3. free-running engine, quadratic: the device event log replayed through the
+     oracle reproduces every rank's models bitwise;
+  4. consensus mean (NCCL fp64 all-reduce) within 1 ulp;
+  5. AllReduce-SGD baseline (NCCL fp32) within 1e-5 relative.
+"""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import synth
+import paper_1710_06952_b200 as P
+
+
+def gather_models(ctx):
+    mine = {w: ctx.read_model(w) for w in ctx.local_workers()}
+    allm = [None] * ctx.world
+    dist.all_gather_object(allm, mine)
+    X = np.zeros((ctx.n, ctx.d), np.float32)
+    for m in allm:
+        for w, x in m.items():
+            X[w] = x
+    return X
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fails = []
+    if rank == 0:
+        from oracle import oracle as O
+    n = 8 * world
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(3)
+    s = float(np.float32(0.1 * math.sqrt(96)))
+    prob_q = None
+    if rank == 0:
+        prob_q = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+
+    # 1. pure gossip replay over NVLink (interleave: every edge crosses GPUs)
+    d = 1 << 20
+    X0 = synth.x0_uniform(n, d, seed=21)
+    ev, _ = synth.schedule_iid(n, e, K=1500, seed=4, no_grad=True)
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1, x0_per_worker=X0)
+    ctx.replay(ev, flags=P.REPLAY_ENGINE)
+    ctx.sync()
+    dist.barrier()
+    st = ctx.stats()
+    X = gather_models(ctx)
+    cross = [None] * world
+    dist.all_gather_object(cross, st["local_cross_events"])
+    if rank == 0:
+        Xo, _ = O.replay(O.OracleProblem(), X0, e, r, ev)
+        if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
+            fails.append("pure-gossip engine replay over NVLink not bit-exact")
+        if sum(cross) != 1500:
+            fails.append(f"expected every event to cross GPUs, got {sum(cross)}")
+    # 4. consensus mean (NCCL fp64)
+    out = torch.empty(d, dtype=torch.float32, device="cuda")
+    mk = ctx.consensus_mean(out.data_ptr())
+    if rank == 0:
+        xo, mko = O.consensus_mean(Xo)
+        ulp = np.abs(out.cpu().numpy().view(np.int32).astype(np.int64) - xo.view(np.int32).astype(np.int64))
+        if ulp.max() > 1:
+            fails.append(f"consensus mean {ulp.max()} ulp")
+        if abs(mk - mko) > 1e-9 * mko:
+            fails.append(f"M_k {mk} vs {mko}")
+    ctx.destroy()
+    dist.barrier()
+
+    # 2./3. quadratic: engine replay then free-running, block placement
+    d = 1 << 20
+    ev, _ = synth.schedule_iid(n, e, K=400, seed=8, local_prob=0.3)
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=0,
+                    model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
+                    straggler=synth.stragglers(n), compute_ns=20_000, seed=9)
+    ctx.replay(ev, flags=P.REPLAY_ENGINE)
+    ctx.sync()
+    dist.barrier()
+    X = gather_models(ctx)
+    if rank == 0:
+        Xo, _ = O.replay(prob_q, np.zeros((n, d), np.float32), e, r, ev)
+        if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
+            fails.append("quadratic engine replay (block placement) not bit-exact")
+    ctx.run(3000)
+    ctx.sync()
+    dist.barrier()
+    X2 = gather_models(ctx)
+    if rank == 0:
+        log = ctx.read_log(400)
+        evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+        if len(log) != 3000:
+            fails.append(f"log has {len(log)} entries")
+        Xo2, _ = O.replay(prob_q, Xo, e, r, evs, k0=400)
+        if not np.array_equal(X2.view(np.uint32), Xo2.view(np.uint32)):
+            bad = np.where((X2 != Xo2).any(1))[0]
+            fails.append(f"free-running multi-GPU log replay not bit-exact (workers {bad.tolist()})")
+    # 5. AllReduce-SGD baseline over NCCL
+    ctx.allreduce_reset()
+    ctx.allreduce_sgd(5)
+    xa = ctx.allreduce_read_model()
+    if rank == 0:
+        x = np.zeros(d, np.float32)
+        for rr in range(5):
+            G = np.stack([O.gradient(prob_q, x, k=rr * n + w) for w in range(n)])
+            x = O.allreduce_update(x, G, 0.01)
+        if not np.allclose(xa, x, rtol=1e-5, atol=1e-6):
+            fails.append(f"allreduce baseline max err {np.abs(xa - x).max()}")
+    ctx.destroy()
+    dist.barrier()
+    if rank == 0:
+        print("MULTIGPU", "FAIL" if fails else "OK", fails, flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if (rank == 0 and fails) else 0)
+
+
+if __name__ == "__main__":
+    main()
