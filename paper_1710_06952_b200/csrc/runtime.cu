@@ -131,7 +131,7 @@ struct adpsgd_ctx {
   std::vector<cudaEvent_t> last_evt;
   std::vector<uint64_t> step_ctr;
   unsigned long long host_k = 0;
-  bool host_k_valid = true;
+  std::vector<unsigned int> epochs;  // per-worker committed-replay-event counts (mirror)
   long long launches = 0;
   unsigned int run_counter = 0;
   std::vector<Slot> h_slots;
@@ -233,11 +233,7 @@ adpsgd_status read_ticket(adpsgd_ctx* c, unsigned long long* k) {
 }
 
 adpsgd_status host_ticket(adpsgd_ctx* c, unsigned long long* k) {
-  if (!c->host_k_valid) {
-    ST(read_ticket(c, &c->host_k));
-    c->host_k_valid = true;
-  }
-  *k = c->host_k;
+  *k = c->host_k;          // authoritative on every rank (see replay_engine)
   return ADPSGD_OK;
 }
 
@@ -404,7 +400,6 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   CU(launch_engine(p, cps * dev_sms, c->engine_threads, s));
   ++c->launches;
   ++c->run_counter;
-  c->host_k_valid = false;
   return ADPSGD_OK;
 }
 
@@ -429,17 +424,12 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   ST(validate_events(c, ev, K, false));
   for (int64_t e = 0; e < K; ++e)
     if (ev[e].tau != 0) return fail(ADPSGD_E_UNSUPPORTED, "engine replay needs tau = 0 (use HOST)");
-  // quiescent read of every worker's epoch (peer memory via UVA) and of k
-  CU(cudaDeviceSynchronize());
-  std::vector<unsigned int> ep(c->n);
-  for (int w = 0; w < c->n; ++w) {
-    const WorkerCtl* cw = c->is_local(w) ? c->ctl + c->worker_local[w]
-                                         : reinterpret_cast<WorkerCtl*>(c->peer_ctl[c->worker_rank[w]]) +
-                                               c->worker_local[w];
-    CU(cudaMemcpy(&ep[w], &cw->epoch, sizeof(unsigned int), cudaMemcpyDeviceToHost));
-  }
-  unsigned long long k0;
-  ST(read_ticket(c, &k0));
+  // k and the epochs are tracked identically on every rank (they only change
+  // through collective calls whose effect is known: a replay advances k by K
+  // and the epochs by the schedule, a run ends at exactly its target), so no
+  // rank reads device state that another rank's engine may already be moving.
+  std::vector<unsigned int>& ep = c->epochs;
+  const unsigned long long k0 = c->host_k;
   std::vector<std::vector<ReplayEv>> per(c->n_local);
   for (int64_t e = 0; e < K; ++e) {
     const int i = ev[e].i, j = ev[e].j;
@@ -469,7 +459,9 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   if (!c->h_rev.empty())
     CU(cudaMemcpy(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice));
-  return engine_launch(c, 1, 0, s);
+  ST(engine_launch(c, 1, 0, s));
+  c->host_k = k0 + (unsigned long long)K;
+  return ADPSGD_OK;
 }
 
 adpsgd_status destroy_impl(adpsgd_ctx* c) {
@@ -627,6 +619,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->last_evt.assign(c->n, nullptr);
   for (auto& e : c->last_evt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   c->step_ctr.assign(c->n, 0);
+  c->epochs.assign(c->n, 0u);
   c->launches += 1;
   if (c->world == 1) {
     ST(upload_workers(c.get()));
@@ -743,7 +736,6 @@ adpsgd_status adpsgd_connect(adpsgd_ctx* c, const void* nccl_id) {
       NC(ncclCommInitRank(&c->comm, c->world, id, c->rank));
     }
     c->connected = true;
-    c->host_k_valid = false;
     return ADPSGD_OK;
   })
 }
@@ -832,11 +824,13 @@ adpsgd_status adpsgd_run(adpsgd_ctx* c, int64_t n_updates, adpsgd_stream s) {
       return fail(ADPSGD_E_UNSUPPORTED, "free-running engine supports models NONE and QUADRATIC");
     if (n_updates < 0) return fail(ADPSGD_E_INVALID, "n_updates");
     std::lock_guard<std::mutex> lk(c->mu);
-    unsigned long long k0;
-    ST(read_ticket(c, &k0));
+    // the run ends with the ticket at exactly k0 + n_updates on every rank
+    const unsigned long long k0 = c->host_k;
     cudaStream_t st = c->use(s);
     ST(reset_slots(c, st));
-    return engine_launch(c, 0, k0 + (unsigned long long)n_updates, st);
+    ST(engine_launch(c, 0, k0 + (unsigned long long)n_updates, st));
+    c->host_k = k0 + (unsigned long long)n_updates;
+    return ADPSGD_OK;
   })
 }
 
