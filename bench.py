@@ -332,8 +332,10 @@ def main():
                    f"{'block' if a.placement == 0 else 'interleave'} placement",
                    "l2": "inputs larger than L2 (n x 102.4 MB models)"},
         "updates_per_s": upd_s, "samples_per_s": upd_s * M_BATCH,
+        # every byte that crosses NVLink leaves one GPU: per-GPU egress = total / world
         "nvlink": {"algorithmic_bytes_per_s": nvl_bytes / sec, "per_gpu_per_direction_gbs":
-                   nvl_bytes / sec / 2 / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / 2 / max(world, 1) / 900e9},
+                   nvl_bytes / sec / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / max(world, 1) / 900e9,
+                   "frac_of_measured_peer_copy_770": nvl_bytes / sec / max(world, 1) / 770e9},
         "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": None,
                      "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,

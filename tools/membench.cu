@@ -2,6 +2,7 @@
 // nvcc -O3 -std=c++17 -gencode arch=compute_100a,code=sm_100a -o tools/membench tools/membench.cu
 // Patterns on d = 25.6M fp32 rows: copy (1R1W), pair average (2R2W).
 #include <cstdio>
+#include <chrono>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -118,6 +119,7 @@ __global__ void avg_tma(float4* xi, float4* xj, long long n4, int pair) {
 }
 
 int sms;
+#define RUN2(name, launch, bytes) { float ms = timeit([&] { launch; }, it); CK(cudaGetLastError()); printf("%-48s %8.1f us %7.0f GB/s\n", name, ms * 1e3, (bytes) / (ms / 1e3) / 1e9); }
 
 template <typename F>
 float timeit(F f, int iters) {
@@ -133,7 +135,82 @@ float timeit(F f, int iters) {
   return ms / iters;
 }
 
-int main() {
+// remote-row microbenchmarks: x_j on GPU 1, kernel on GPU 0 (NVLink P2P)
+template <int U>
+__global__ void peer_read(const float4* src, float4* dst, long long n4) {   // remote -> local copy
+  const long long T = (long long)gridDim.x * blockDim.x;
+  for (long long base = blockIdx.x * (long long)blockDim.x + threadIdx.x; base < n4; base += T * U) {
+    float4 v[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) { long long i = base + u * T; if (i < n4) v[u] = __ldcg(src + i); }
+#pragma unroll
+    for (int u = 0; u < U; ++u) { long long i = base + u * T; if (i < n4) __stcg(dst + i, v[u]); }
+  }
+}
+
+int peer_main() {
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (ndev < 2) { printf("peer: need 2 GPUs\n"); return 0; }
+  const long long d = 25600000, n4 = d / 4;
+  float4 *xi, *xj, *buf;
+  CK(cudaSetDevice(1));
+  CK(cudaMalloc(&xj, d * 4)); CK(cudaMemset(xj, 0, d * 4));
+  CK(cudaSetDevice(0));
+  CK(cudaDeviceEnablePeerAccess(1, 0));
+  CK(cudaMalloc(&xi, d * 4)); CK(cudaMalloc(&buf, d * 4));
+  CK(cudaMemset(xi, 0, d * 4));
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const int it = 20;
+  printf("=== NVLink: x_j on GPU1, kernels on GPU0 (GB/s per direction over NVLink) ===\n");
+  double bytes = 4.0 * d;
+  RUN2("peer LDG remote->local copy U4 2/SM", (peer_read<4><<<sms * 2, 512>>>(xj, buf, n4)), bytes);
+  RUN2("peer LDG remote->local copy U8 4/SM", (peer_read<8><<<sms * 4, 512>>>(xj, buf, n4)), bytes);
+  RUN2("peer STG local->remote copy U4 2/SM", (peer_read<4><<<sms * 2, 512>>>(buf, xj, n4)), bytes);
+  RUN2("cudaMemcpyPeer 1->0", (cudaMemcpyPeerAsync(buf, 0, xj, 1, d * 4)), bytes);
+  RUN2("pair avg ldg/stg remote xj, stride U4 2/SM", (avg_stride<4><<<sms * 2, 512>>>(xi, xj, n4, 1)), bytes);
+  RUN2("pair avg ldg/stg remote xj, stride U8 4/SM", (avg_stride<8><<<sms * 4, 512>>>(xi, xj, n4, 1)), bytes);
+  {
+    constexpr int T = 512, S = 4;
+    size_t smem = (size_t)S * 2 * T * 16 + 64;
+    cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    cudaFuncSetAttribute(avg_tma<T, S, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    RUN2("pair avg IL tma T512 S4 + stg, 2/SM", (avg_tma<T, S, false, true><<<sms * 2, 512, smem>>>(xi, xj, n4, 1)), bytes);
+    RUN2("pair avg IL tma T512 S4 + bulk st, 2/SM", (avg_tma<T, S, true, true><<<sms * 2, 512, smem>>>(xi, xj, n4, 1)), bytes);
+  }
+  // bidirectional: both GPUs push (or pull) 4d to/from each other at once
+  float4 *yi, *ybuf;
+  CK(cudaSetDevice(1));
+  CK(cudaDeviceEnablePeerAccess(0, 0));
+  CK(cudaMalloc(&yi, d * 4)); CK(cudaMalloc(&ybuf, d * 4));
+  cudaStream_t s1; CK(cudaStreamCreate(&s1));
+  CK(cudaSetDevice(0));
+  cudaStream_t s0; CK(cudaStreamCreate(&s0));
+  cudaEvent_t e0, e1; cudaEventCreate(&e0); cudaEventCreate(&e1);
+  for (int mode = 0; mode < 2; ++mode) {
+    auto both = [&] {
+      if (mode == 0) {   // writes: GPU0 -> GPU1 buffer, GPU1 -> GPU0 buffer
+        cudaSetDevice(0); peer_read<4><<<sms * 2, 512, 0, s0>>>(xi, ybuf, n4);
+        cudaSetDevice(1); peer_read<4><<<sms * 2, 512, 0, s1>>>(yi, buf, n4);
+      } else {           // reads: GPU0 pulls GPU1's row, GPU1 pulls GPU0's row
+        cudaSetDevice(0); peer_read<4><<<sms * 2, 512, 0, s0>>>(yi, buf, n4);
+        cudaSetDevice(1); peer_read<4><<<sms * 2, 512, 0, s1>>>(xi, ybuf, n4);
+      }
+      cudaSetDevice(0);
+    };
+    both(); cudaDeviceSynchronize(); cudaSetDevice(1); cudaDeviceSynchronize(); cudaSetDevice(0);
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < it; ++r) both();
+    cudaDeviceSynchronize(); cudaSetDevice(1); cudaDeviceSynchronize(); cudaSetDevice(0);
+    double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / it;
+    printf("%-48s %8.1f us %7.0f GB/s per direction\n", mode == 0 ? "bidirectional push (both GPUs write peer)" :
+           "bidirectional pull (both GPUs read peer)", s * 1e6, bytes / s / 1e9);
+  }
+  return 0;
+}
+
+int main(int argc, char** argv) {
+  if (argc > 1) return peer_main();
   const long long d = 25600000, n4 = d / 4;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   float4 *xi, *xj;
