@@ -228,17 +228,26 @@ __device__ __forceinline__ void fence_proxy_async() {
   asm volatile("fence.proxy.async.global;" ::: "memory");
 }
 
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+
 // Per-CTA staging pipeline state.  `consumed` advances identically in every
-// thread; `bar[s]` completes once per use of stage s (parity = use count & 1).
-template <int kTile4, int kStages>
+// thread.  full[s] completes once per use of stage s (TMA bytes landed);
+// empty[s] completes once per use when every warp has copied the stage to
+// registers (one arrival per warp), so no CTA-wide barrier sits in the loop.
+template <int kTile4, int kStages, bool kWarpEmpty = true>
 struct Stager {
   float4* buf;      // [kStages][2][kTile4]
-  uint64_t* bar;    // [kStages]
+  uint64_t* bar;    // [kStages] full
+  uint64_t* empty;  // [kStages] empty
   uint32_t consumed;
 
+  // tile use g goes into stage g % kStages once use g - kStages has been drained
   __device__ __forceinline__ void issue(uint32_t g, const float4* xi4, const float4* xj4, long long base,
                                         long long hi) {
     const uint32_t s = g % kStages;
+    if (kWarpEmpty && g >= kStages) mbar_wait(empty + s, ((g / kStages) - 1u) & 1u);
     const long long cnt = (hi - base) < kTile4 ? (hi - base) : kTile4;
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_arrive_tx(bar + s, xj4 ? 2u * bytes : bytes);
@@ -269,20 +278,30 @@ struct Stager {
       const float4* sa = buf + (size_t)s * 2 * kTile4;
       const float4* sb = sa + kTile4;
       const long long base = (first + t * step) * kTile4;
+      constexpr int kPer = kTile4 / 512;
+      float4 a[kPer], b[kPer];
 #pragma unroll
-      for (int u = 0; u < kTile4 / 512; ++u) {
-        const int off = u * (int)blockDim.x + (int)threadIdx.x;
-        const long long idx = base + off;
-        if (off < kTile4 && idx < hi) {
-          float4 a = sa[off];
-          float4 b = kPair ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
-          update4<kPair, kGrad>(a, b, make_float4(0.f, 0.f, 0.f, 0.f), make_float4(0.f, 0.f, 0.f, 0.f),
-                                (uint32_t)(idx * 4), d, gamma, q, kk);
-          if (kPair) st_cg4(xj4 + idx, b);
-          st_cg4(xi4 + idx, a);
+      for (int u = 0; u < kPer; ++u) {
+        const int off = u * 512 + (int)threadIdx.x;
+        a[u] = sa[off];
+        b[u] = kPair ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (kWarpEmpty) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);   // this warp is done with stage s
+      } else {
+        __syncthreads();                                        // stage s read by every thread
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const long long idx = base + u * 512 + (int)threadIdx.x;
+        if (idx < hi) {
+          update4<kPair, kGrad>(a[u], b[u], make_float4(0.f, 0.f, 0.f, 0.f),
+                                make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d, gamma, q, kk);
+          if (kPair) st_cg4(xj4 + idx, b[u]);
+          st_cg4(xi4 + idx, a[u]);
         }
       }
-      __syncthreads();                       // stage s fully read by every thread
       if (threadIdx.x == 0 && t + kStages < n_t)
         issue(g + kStages, xi4, kPair ? xj4 : nullptr, (first + (t + kStages) * step) * kTile4, hi);
     }

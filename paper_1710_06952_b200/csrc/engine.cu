@@ -189,13 +189,19 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
 
 constexpr int kTile4 = 512;              // float4 per stream per stage (8 KB)
 constexpr int kStages = 4;
-constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
+constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * kStages * sizeof(uint64_t);
 
-template <bool kTma, bool kPair, int kGrad>
-__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e,
-                                      Stager<kTile4, kStages>& stg) {
+// engine variants: 0 = bulk-copy staged, CTA barrier per tile (default);
+// 1 = register slices (no staging); 2 = bulk-copy staged, per-warp empty
+// mbarriers.  tools/ab_engine.py on a fixed 512-event mix at d = 25.6M:
+// 5404 / 4996 / 5324 GB/s (variant 0 / 1 / 2).
+template <int kVar>
+using EngineStager = Stager<kTile4, kStages, kVar == 2>;
+
+template <int kVar, bool kPair, int kGrad>
+__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, EngineStager<kVar>& stg) {
   const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
-  if (kTma) {
+  if (kVar != 1) {
     stg.template run<kPair, kGrad>(reinterpret_cast<float4*>(e.xi), reinterpret_cast<float4*>(e.xj),
                                    blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk);
   } else {
@@ -208,19 +214,23 @@ __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e,
   }
 }
 
-template <bool kTma>
+template <int kVar>
 __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_constant__ EngineParams p) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
   __shared__ unsigned int done_seq[kMaxLocal];
   __shared__ int s_pick;
   __shared__ unsigned int s_seq;
   __shared__ SmemSlot s_ev;
-  Stager<kTile4, kStages> stg;
+  EngineStager<kVar> stg;
   stg.buf = reinterpret_cast<float4*>(dyn_smem);
   stg.bar = reinterpret_cast<uint64_t*>(dyn_smem + (size_t)kStages * 2 * kTile4 * sizeof(float4));
+  stg.empty = stg.bar + kStages;
   stg.consumed = 0;
-  if (kTma && threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) mbar_init(stg.bar + s, 1);
+  if (kVar != 1 && threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(stg.bar + s, 1);
+      mbar_init(stg.empty + s, kEngineThreads / 32);
+    }
     mbar_fence_init();
   }
   for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) done_seq[s] = 0u;
@@ -273,10 +283,10 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     if (pick >= 0) {
       const SmemSlot e = s_ev;
       if (e.pair) {
-        if (e.grad) slice<kTma, true, kGradQuadInline>(p, e, stg);
-        else slice<kTma, true, kGradNone>(p, e, stg);
+        if (e.grad) slice<kVar, true, kGradQuadInline>(p, e, stg);
+        else slice<kVar, true, kGradNone>(p, e, stg);
       } else if (e.grad) {
-        slice<kTma, false, kGradQuadInline>(p, e, stg);
+        slice<kVar, false, kGradQuadInline>(p, e, stg);
       }
       __syncthreads();
       if (threadIdx.x == 0) {
@@ -297,14 +307,22 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
 
 }  // namespace
 
+namespace {
+const void* engine_fn(int variant, size_t* smem) {
+  switch (variant) {
+    case 1: *smem = 0; return (const void*)k_engine<1>;
+    case 2: *smem = kTmaSmem; return (const void*)k_engine<2>;
+    default: *smem = kTmaSmem; return (const void*)k_engine<0>;
+  }
+}
+}  // namespace
+
 int engine_max_ctas_per_sm(int threads, int variant) {
   int n = 0;
-  if (variant == 0) {
-    cudaFuncSetAttribute(k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine<true>, threads, kTmaSmem);
-  } else {
-    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, k_engine<false>, threads, 0);
-  }
+  size_t smem = 0;
+  const void* fn = engine_fn(variant, &smem);
+  if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem);
   return n;
 }
 
@@ -312,12 +330,10 @@ cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStre
   EngineParams pp = p;
   void* args[] = {&pp};
   if (threads != kEngineThreads) return cudaErrorInvalidValue;
-  if (p.variant == 0) {
-    cudaFuncSetAttribute(k_engine<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
-    return cudaLaunchCooperativeKernel((const void*)k_engine<true>, dim3(grid), dim3(threads), args,
-                                       kTmaSmem, s);
-  }
-  return cudaLaunchCooperativeKernel((const void*)k_engine<false>, dim3(grid), dim3(threads), args, 0, s);
+  size_t smem = 0;
+  const void* fn = engine_fn(p.variant, &smem);
+  if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
 }
 
 }  // namespace adp

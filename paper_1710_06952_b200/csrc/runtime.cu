@@ -513,7 +513,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->engine_cps = cfg->engine_ctas_per_sm;
   c->engine_threads = 512;
   c->engine_variant = cfg->engine_variant;
-  if (c->engine_variant < 0 || c->engine_variant > 1) return fail(ADPSGD_E_INVALID, "engine_variant");
+  if (c->engine_variant < 0 || c->engine_variant > 2) return fail(ADPSGD_E_INVALID, "engine_variant");
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   ST(check_graph(c.get(), g));
