@@ -241,6 +241,14 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* ctx);
 /* Number of kernels this context launched since creation (bench gpu_launches). */
 adpsgd_status adpsgd_launch_count(adpsgd_ctx* ctx, int64_t* out);
 
+/* Diagnostics: the MLP's tensor-core GEMM on its own.
+ * C[M x N] = A[M x K] . B[N x K]^T, fp32 row-major DEVICE pointers on the current
+ * device, computed as 3xTF32 (hi*hi + hi*lo + lo*hi) with tcgen05.mma into TMEM,
+ * split-K over `splits` CTAs per tile (partials summed in a fixed order).
+ * Requires M % 128 == 0, N % 128 == 0, K % (32 * splits) == 0.  Synchronous.   */
+adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
+                                 int32_t splits);
+
 #ifdef __cplusplus
 }
 #endif

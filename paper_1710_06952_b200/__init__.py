@@ -31,7 +31,8 @@ EXPORTED = ["adpsgd_abi_version", "adpsgd_last_error", "adpsgd_init", "adpsgd_de
             "adpsgd_run", "adpsgd_consensus_mean", "adpsgd_allreduce_sgd", "adpsgd_allreduce_read_model",
             "adpsgd_allreduce_reset", "adpsgd_sync", "adpsgd_read_model", "adpsgd_write_model",
             "adpsgd_model_device_ptr", "adpsgd_worker_rank", "adpsgd_get_ticket", "adpsgd_read_log",
-            "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count"]
+            "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count",
+            "adpsgd_gemm_tf32x3"]
 
 
 class AdpsgdError(RuntimeError):
@@ -95,6 +96,7 @@ def lib():
             "adpsgd_get_ticket": ([P, P], I32), "adpsgd_read_log": ([P, I64, P, I64, P], I32),
             "adpsgd_read_update_counts": ([P, P], I32), "adpsgd_get_stats": ([P, P], I32),
             "adpsgd_reset_stats": ([P], I32), "adpsgd_launch_count": ([P, P], I32),
+            "adpsgd_gemm_tf32x3": ([P, P, P, I32, I32, I32, I32], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -121,6 +123,12 @@ def _stream(s):
     if s is None:
         return None
     return C.c_void_p(int(getattr(s, "cuda_stream", s)))
+
+
+def gemm_tf32x3(A_ptr, B_ptr, C_ptr, M, N, K, splits=1):
+    """Diagnostics: C = A . B^T on tcgen05 (3xTF32), device pointers (see adpsgd.h)."""
+    _chk(lib().adpsgd_gemm_tf32x3(C.c_void_p(A_ptr), C.c_void_p(B_ptr), C.c_void_p(C_ptr), M, N, K, splits),
+         "gemm_tf32x3")
 
 
 class Context:

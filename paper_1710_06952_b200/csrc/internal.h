@@ -2,7 +2,9 @@
 // the kernel translation units (kernels.cu, engine.cu).  Not part of the ABI.
 #pragma once
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 #include "device.cuh"
 
 namespace adp {
@@ -96,6 +98,17 @@ cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, lo
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t s);
 cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d, const float* x0,
                              cudaStream_t s);
+
+// 3xTF32 tcgen05 GEMM (gemm.cu): C = A . B^T, A [M x K], B [N x K] row-major fp32,
+// operands pre-split into tf32 hi/lo planes and described by SWIZZLE_128B tensor maps
+struct GemmOperands {
+  CUtensorMap Ah, Al, Bh, Bl;
+};
+cudaError_t make_tmap_k_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols, int box_rows);
+cudaError_t launch_split_tf32(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
+cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long long n, cudaStream_t s);
+cudaError_t launch_gemm_tf32x3(const GemmOperands& op, float* C, int M, int N, int K, int splits, int bn,
+                               cudaStream_t s);
 
 // MLP (kind 5): tcgen05-backed gradient (mlp.cu)
 struct MlpShape { int n_in, n_hid, n_out; };

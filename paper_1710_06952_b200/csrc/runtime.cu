@@ -632,9 +632,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
 
 }  // namespace
 
-#define GUARD(body)                                                                   \
+#define GUARD(...)                                                                    \
   try {                                                                               \
-    body                                                                              \
+    __VA_ARGS__                                                                       \
   } catch (const std::bad_alloc&) {                                                   \
     return fail(ADPSGD_E_OOM, "host allocation failed");                              \
   } catch (...) {                                                                     \
@@ -1039,6 +1039,32 @@ adpsgd_status adpsgd_launch_count(adpsgd_ctx* c, int64_t* out) {
   if (!c || !out) return fail(ADPSGD_E_INVALID, "null");
   *out = c->launches;
   return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
+                                 int32_t splits) {
+  GUARD({
+    if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(ADPSGD_E_INVALID, "gemm args");
+    if (M % 128 || N % 128 || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
+    const size_t na = (size_t)M * K, nb = (size_t)N * K;
+    float* buf = nullptr;
+    CU(cudaMalloc(&buf, sizeof(float) * (2 * na + 2 * nb + (size_t)splits * M * N)));
+    float *ah = buf, *al = ah + na, *bh = al + na, *bl = bh + nb, *part = bl + nb;
+    GemmOperands op;
+    adpsgd_status st = ADPSGD_OK;
+    cudaError_t e = launch_split_tf32(A, ah, al, (long long)na, nullptr);
+    if (e == cudaSuccess) e = launch_split_tf32(B, bh, bl, (long long)nb, nullptr);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Ah, ah, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Al, al, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bh, bh, N, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bl, bl, N, K, 128);
+    if (e == cudaSuccess) e = launch_gemm_tf32x3(op, splits > 1 ? part : C, M, N, K, splits, 128, nullptr);
+    if (e == cudaSuccess && splits > 1) e = launch_sum_planes(part, C, splits, (long long)M * N, nullptr);
+    if (e == cudaSuccess) e = cudaDeviceSynchronize();
+    if (e != cudaSuccess) st = fail(ADPSGD_E_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
+    cudaFree(buf);
+    return st;
+  })
 }
 
 }  // extern "C"
