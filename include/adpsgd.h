@@ -81,7 +81,7 @@ typedef enum {
   ADPSGD_MODEL_QUADRATIC = 2, /* synthetic quadratic, procedural data             */
   ADPSGD_MODEL_LSQ = 3,       /* least squares F = 1/2 (a.x - b)^2                            */
   ADPSGD_MODEL_LOGREG = 4,    /* logistic F = log(1 + exp(-y a.x)), y in {-1,+1}             */
-  ADPSGD_MODEL_MLP = 5        /* 2-layer ReLU MLP + softmax cross-entropy (R18)     */
+  ADPSGD_MODEL_MLP = 5        /* 2-layer tanh MLP + softmax cross-entropy (R18)     */
 } adpsgd_model_kind;
 
 typedef struct {

@@ -253,8 +253,9 @@ static int logreg_grad(const oracle_problem* p, int64_t d, const float* xhat, co
   return ORC_OK;
 }
 
-/* 2-layer MLP n_in -> n_hid (ReLU) -> n_out, softmax cross-entropy summed over
- * the batch (reading R18).  Flat parameter layout
+/* 2-layer MLP n_in -> n_hid (tanh) -> n_out, softmax cross-entropy summed over
+ * the batch (reading R18; tanh as in SPEC's small-mlp: a smooth
+ * activation has no floating-point-decided mask).  Flat parameter layout
  * [W1 (n_hid x n_in, out x in) | b1 | W2 (n_out x n_hid) | b2].  Plain fp64
  * loops, rounded once to fp32.  Returns the batch loss (fp64) via loss_out. */
 static int mlp_grad(const oracle_problem* p, const float* xhat, const int32_t* idx, float* g,
@@ -280,7 +281,7 @@ static int mlp_grad(const oracle_problem* p, const float* xhat, const int32_t* i
     for (int64_t u = 0; u < H; ++u) {
       double s = (double)b1[u];
       for (int64_t c = 0; c < I; ++c) s += (double)W1[u * I + c] * (double)a[c];
-      z1[u] = s; h1[u] = s > 0.0 ? s : 0.0;
+      z1[u] = s; h1[u] = tanh(s);
     }
     double zmax = -INFINITY;
     for (int64_t o = 0; o < O; ++o) {
@@ -299,7 +300,7 @@ static int mlp_grad(const oracle_problem* p, const float* xhat, const int32_t* i
     for (int64_t u = 0; u < H; ++u) {
       double s = 0.0;
       for (int64_t o = 0; o < O; ++o) s += (double)W2[o * H + u] * dz2[o];
-      dz1[u] = z1[u] > 0.0 ? s : 0.0;
+      dz1[u] = s * (1.0 - h1[u] * h1[u]);
     }
     for (int64_t u = 0; u < H; ++u) {
       gb1[u] += dz1[u];

@@ -112,9 +112,18 @@ cudaError_t launch_gemm_tf32x3(const GemmOperands& op, float* C, int M, int N, i
 
 // MLP (kind 5): tcgen05-backed gradient (mlp.cu)
 struct MlpShape { int n_in, n_hid, n_out; };
-cudaError_t launch_mlp_grad(const MlpShape& sh, const float* X, const int* y, int S,
-                            const int* idx, int M, uint2 batch_key, unsigned long long k,
-                            const float* w, float* g, float* scratch, cudaStream_t s);
+struct MlpWork {                   // scratch carve-up + tensor maps, built once per context
+  MlpShape sh;
+  int M, splits;
+  float *xh, *xl, *th, *tl, *w1h, *w1l, *z1p, *hbuf, *dz1, *dz2, *dth, *dtl;
+  int* idx;
+  GemmOperands g1, g2;
+};
 size_t mlp_scratch_floats(const MlpShape& sh, int M);
+bool mlp_supported(const MlpShape& sh, int M);
+cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch);
+cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx,
+                            uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s);
+constexpr int kMlpLaunches = 7;
 
 }  // namespace adp

@@ -118,6 +118,7 @@ struct adpsgd_ctx {
   float* gstep = nullptr;            // per-local-worker gradient buffers (adpsgd_step)
   float* mlp_scratch = nullptr;
   size_t mlp_scratch_n = 0;
+  MlpWork mlp_work{};
   int* d_batch = nullptr;
   size_t batch_cap = 0;
   double* sum64 = nullptr;
@@ -254,6 +255,7 @@ adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c) {
   c->mlp_scratch = nullptr;
   CU(cudaMalloc(&c->mlp_scratch, sizeof(float) * need));
   c->mlp_scratch_n = need;
+  CU(mlp_plan(c->mlp_work, c->mlp, c->M, c->mlp_scratch));   // tensor maps over the scratch planes
   return ADPSGD_OK;
 }
 
@@ -271,13 +273,12 @@ adpsgd_status model_grad(adpsgd_ctx* c, const float* xhat, float* g, unsigned lo
       break;
     case ADPSGD_MODEL_MLP:
       ST(ensure_mlp_scratch(c));
-      CU(launch_mlp_grad(c->mlp, c->dA, c->dy, c->S, idx_dev, c->M, c->seed2(), k, xhat, g,
-                         c->mlp_scratch, s));
+      CU(launch_mlp_grad(c->mlp_work, c->dA, c->dy, c->S, idx_dev, c->seed2(), k, xhat, g, s));
       break;
     default:
       return fail(ADPSGD_E_UNSUPPORTED, "model has no built-in gradient");
   }
-  c->launches += (c->model == ADPSGD_MODEL_MLP) ? 6 : 1;
+  c->launches += (c->model == ADPSGD_MODEL_MLP) ? kMlpLaunches : 1;
   return ADPSGD_OK;
 }
 
@@ -551,6 +552,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
       const long long dim = (long long)c->mlp.n_hid * c->mlp.n_in + c->mlp.n_hid +
                             (long long)c->mlp.n_out * c->mlp.n_hid + c->mlp.n_out;
       if (dim != d || !cfg->data_y) return fail(ADPSGD_E_INVALID, "mlp dims do not match d / labels missing");
+      if (!mlp_supported(c->mlp, c->M))
+        return fail(ADPSGD_E_UNSUPPORTED, "MLP tensor-core path needs batch_M, mlp_in, mlp_hid multiples of 128 "
+                                          "and mlp_out <= 32");
       c->feat = c->mlp.n_in;
     } else {
       if (!cfg->data_b) return fail(ADPSGD_E_INVALID, "data_b required");

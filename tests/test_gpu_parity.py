@@ -301,3 +301,30 @@ def test_allreduce_sgd_matches_oracle(P):
         x = O.allreduce_update(x, G, 0.01)
     np.testing.assert_allclose(xg, x, rtol=1e-5, atol=1e-6)
     ctx.destroy()
+
+
+# ------------------------------------------------------------- MLP (tcgen05) --
+@pytest.mark.parametrize("dims,K,T", [((256, 128, 10), 2000, 2), ((3072, 512, 10), 6, 1)])
+def test_mlp_replay_within_1e4(P, dims, K, T):
+    """Config 3 MLP gradients (3xTF32 tcgen05 GEMMs) with stale reads: after K
+    replayed events every parameter within reading R11 of the fp64 oracle."""
+    I, H, Ocl = dims
+    n, M = 4, 128
+    e, r = synth.ring(n)
+    X, y = synth.mlp_data(S=2048 if I == 256 else 4096, n_in=I, n_out=Ocl, s=0.02 if I == 3072 else 0.3, seed=3)
+    x0 = synth.mlp_init(I, H, Ocl, seed=4)
+    d = x0.size
+    gamma = 0.002 if I == 3072 else 0.01
+    ev, bi = synth.schedule_iid(n, e, K=K, T=T, M=M, S=X.shape[0], seed=21)
+    ctx = P.Context(e, n, d, role=r, T=T, model=P.MODEL_MLP, gamma=gamma, batch_M=M, data_A=X, data_y=y,
+                    mlp_dims=dims, x0=x0)
+    ctx.replay(ev, batch_idx=bi)
+    ctx.sync()
+    Xg = read_all(ctx)
+    prob = O.OracleProblem(O.MODEL_MLP, M=M, gamma=gamma, A=X, y=y, dims=dims)
+    Xo, _ = O.replay(prob, np.tile(x0, (n, 1)), e, r, ev, bi, T=T)
+    ok = c11_ok(Xg, Xo)
+    assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum())
+    if K >= 1000:
+        assert O.full_loss(prob, Xo.mean(0)) < 0.7 * O.full_loss(prob, x0)
+    ctx.destroy()
