@@ -241,6 +241,23 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* ctx);
 /* Number of kernels this context launched since creation (bench gpu_launches). */
 adpsgd_status adpsgd_launch_count(adpsgd_ctx* ctx, int64_t* out);
 
+/* ------------------------------------------------ host-only planning ------
+ * Pure host functions (no device work, usable without a GPU) that expose the
+ * multi-rank planning adpsgd_init / adpsgd_replay perform internally.       */
+/* Worker -> rank placement and each worker's index among its rank's workers
+ * (placement 0 block, 1 interleave, 2 explicit from worker_rank_in).          */
+adpsgd_status adpsgd_plan_placement(int32_t n, int32_t world_size, int32_t placement,
+                                    const int32_t* worker_rank_in, int32_t* worker_rank_out,
+                                    int32_t* local_index_out);
+/* The engine-replay plan of `rank`: the events whose updating worker i lives on
+ * `rank`, grouped by local worker, each as int64[6] {k, i, j, flags, e_i, e_j}
+ * where e_i / e_j are the epochs (counts of earlier schedule events touching
+ * i / j, starting from `epochs`) the device waits for.  `epochs` (n entries) is
+ * advanced in place exactly as on every rank.  out may be NULL to query n_out. */
+adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t rank, const adpsgd_event* schedule,
+                                 int64_t K, int64_t k0, uint32_t* epochs, int64_t* out, int64_t cap,
+                                 int64_t* n_out);
+
 /* Diagnostics: the MLP's tensor-core GEMM on its own.
  * C[M x N] = A[M x K] . B[N x K]^T, fp32 row-major DEVICE pointers on the current
  * device, computed as 3xTF32 (hi*hi + hi*lo + lo*hi) with tcgen05.mma into TMEM,

@@ -32,7 +32,7 @@ EXPORTED = ["adpsgd_abi_version", "adpsgd_last_error", "adpsgd_init", "adpsgd_de
             "adpsgd_allreduce_reset", "adpsgd_sync", "adpsgd_read_model", "adpsgd_write_model",
             "adpsgd_model_device_ptr", "adpsgd_worker_rank", "adpsgd_get_ticket", "adpsgd_read_log",
             "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count",
-            "adpsgd_gemm_tf32x3"]
+            "adpsgd_gemm_tf32x3", "adpsgd_plan_placement", "adpsgd_plan_replay"]
 
 
 class AdpsgdError(RuntimeError):
@@ -97,6 +97,8 @@ def lib():
             "adpsgd_read_update_counts": ([P, P], I32), "adpsgd_get_stats": ([P, P], I32),
             "adpsgd_reset_stats": ([P], I32), "adpsgd_launch_count": ([P, P], I32),
             "adpsgd_gemm_tf32x3": ([P, P, P, I32, I32, I32, I32], I32),
+            "adpsgd_plan_placement": ([I32, I32, I32, P, P, P], I32),
+            "adpsgd_plan_replay": ([I32, P, I32, P, I64, I64, P, P, I64, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -123,6 +125,42 @@ def _stream(s):
     if s is None:
         return None
     return C.c_void_p(int(getattr(s, "cuda_stream", s)))
+
+
+def plan_placement(n, world_size, placement=0, worker_rank=None):
+    """Host-only: (worker_rank[n], local_index[n]) exactly as adpsgd_init places workers."""
+    wr_in = _arr(worker_rank, np.int32)
+    wr, wl = np.zeros(n, np.int32), np.zeros(n, np.int32)
+    _chk(lib().adpsgd_plan_placement(n, world_size, placement, _ptr(wr_in), _ptr(wr), _ptr(wl)), "plan_placement")
+    return wr, wl
+
+
+def plan_replay(worker_rank, rank, events, k0=0, epochs=None):
+    """Host-only: this rank's engine-replay plan, rows (k, i, j, flags, e_i, e_j);
+    returns (plan, advanced epoch mirror)."""
+    wr = _arr(worker_rank, np.int32)
+    n = wr.size
+    ev = _arr(np.asarray(events).reshape(-1, 4), np.int32)
+    ep = np.zeros(n, np.uint32) if epochs is None else np.array(epochs, np.uint32)
+    m = C.c_int64()
+    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, _ptr(ep), None, 0, C.byref(m)),
+         "plan_replay")
+    out = np.zeros((m.value, 6), np.int64)
+    ep2 = np.zeros(n, np.uint32) if epochs is None else np.array(epochs, np.uint32)
+    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, _ptr(ep2), _ptr(out), m.value,
+                                  C.byref(m)), "plan_replay")
+    return out, ep2
+
+
+def exchange_peer_blobs(mine: bytes, rank: int, world: int, make_nccl_id=None, pg=None):
+    """The N > 1 wiring protocol: all-gather every rank's CUDA-IPC blob and
+    broadcast rank 0's NCCL id (torch.distributed, any backend)."""
+    import torch.distributed as dist
+    allb = [None] * world
+    dist.all_gather_object(allb, mine, group=pg)
+    obj = [make_nccl_id() if (rank == 0 and make_nccl_id) else None]
+    dist.broadcast_object_list(obj, src=0, group=pg)
+    return allb, obj[0]
 
 
 def gemm_tf32x3(A_ptr, B_ptr, C_ptr, M, N, K, splits=1):
@@ -178,17 +216,17 @@ class Context:
         n = C.c_int64()
         _chk(lib().adpsgd_export_peer_info(self._h, buf, sz.value, C.byref(n)), "export_peer_info")
         mine = bytes(buf[:n.value])
-        allb = [None] * self.world
-        dist.all_gather_object(allb, mine, group=pg)
+
+        def make_id():
+            nid = (C.c_ubyte * 128)()
+            _chk(lib().adpsgd_nccl_unique_id(nid), "nccl_unique_id")
+            return bytes(nid)
+
+        allb, nccl_id = exchange_peer_blobs(mine, self.rank, self.world, make_id, pg)
         for r, blob in enumerate(allb):
             if r != self.rank:
                 _chk(lib().adpsgd_import_peer_info(self._h, r, blob, len(blob)), "import_peer_info")
-        nid = (C.c_ubyte * 128)()
-        if self.rank == 0:
-            _chk(lib().adpsgd_nccl_unique_id(nid), "nccl_unique_id")
-        obj = [bytes(nid) if self.rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0, group=pg)
-        nid2 = (C.c_ubyte * 128).from_buffer_copy(obj[0])
+        nid2 = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
         _chk(lib().adpsgd_connect(self._h, nid2), "connect")
         dist.barrier(group=pg)
 

@@ -418,6 +418,49 @@ adpsgd_status reset_slots(adpsgd_ctx* c, cudaStream_t s) {
   return ADPSGD_OK;
 }
 
+// ---------------------------------------------------------- host planning --
+// worker -> rank (0 block: contiguous ring segments; 1 interleave; 2 explicit)
+adpsgd_status compute_placement(int n, int world, int placement, const int32_t* explicit_rank,
+                                std::vector<int>& wr, std::vector<int>& wl) {
+  if (n < 1 || world < 1) return fail(ADPSGD_E_INVALID, "n / world_size");
+  wr.assign(n, 0);
+  for (int w = 0; w < n; ++w) {
+    if (placement == 0) wr[w] = (int)((long long)w * world / n);
+    else if (placement == 1) wr[w] = w % world;
+    else if (placement == 2) {
+      if (!explicit_rank) return fail(ADPSGD_E_INVALID, "explicit placement needs worker_rank");
+      wr[w] = explicit_rank[w];
+      if (wr[w] < 0 || wr[w] >= world) return fail(ADPSGD_E_INVALID, "worker_rank out of range");
+    } else return fail(ADPSGD_E_INVALID, "placement");
+  }
+  wl.assign(n, 0);
+  std::vector<int> cnt(world, 0);
+  for (int w = 0; w < n; ++w) wl[w] = cnt[wr[w]]++;
+  return ADPSGD_OK;
+}
+
+// Engine-replay plan: event k waits until epoch[i] == e_i(k) and epoch[j] ==
+// e_j(k), the numbers of earlier schedule events touching i and j (so every
+// worker sees the schedule's order).  Every rank runs this on the same schedule
+// and the same epoch mirror, and keeps the events whose updating worker is local.
+void plan_replay(const std::vector<int>& wr, const std::vector<int>& wl, int rank, int n_local,
+                 const adpsgd_event* ev, int64_t K, unsigned long long k0, std::vector<unsigned int>& ep,
+                 std::vector<std::vector<ReplayEv>>& per) {
+  per.assign(n_local, {});
+  for (int64_t e = 0; e < K; ++e) {
+    const int i = ev[e].i, j = ev[e].j;
+    ReplayEv r{};
+    r.k = (long long)(k0 + e);
+    r.j = j;
+    r.flags = ev[e].flags;
+    r.e_i = ep[i];
+    r.e_j = j >= 0 ? ep[j] : 0;
+    ep[i]++;
+    if (j >= 0) ep[j]++;
+    if (wr[i] == rank) per[wl[i]].push_back(r);
+  }
+}
+
 adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cudaStream_t s) {
   if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
   if (c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_QUADRATIC)
@@ -429,21 +472,9 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   // through collective calls whose effect is known: a replay advances k by K
   // and the epochs by the schedule, a run ends at exactly its target), so no
   // rank reads device state that another rank's engine may already be moving.
-  std::vector<unsigned int>& ep = c->epochs;
   const unsigned long long k0 = c->host_k;
-  std::vector<std::vector<ReplayEv>> per(c->n_local);
-  for (int64_t e = 0; e < K; ++e) {
-    const int i = ev[e].i, j = ev[e].j;
-    ReplayEv r{};
-    r.k = (long long)(k0 + e);
-    r.j = j;
-    r.flags = ev[e].flags;
-    r.e_i = ep[i];
-    r.e_j = j >= 0 ? ep[j] : 0;
-    ep[i]++;
-    if (j >= 0) ep[j]++;
-    if (c->is_local(i)) per[c->worker_local[i]].push_back(r);
-  }
+  std::vector<std::vector<ReplayEv>> per;
+  plan_replay(c->worker_rank, c->worker_local, c->rank, c->n_local, ev, K, k0, c->epochs, per);
   c->h_rev.clear();
   ST(reset_slots(c, s));
   for (int l = 0; l < c->n_local; ++l) {
@@ -519,22 +550,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   ST(check_graph(c.get(), g));
   // placement
-  c->worker_rank.assign(c->n, 0);
-  for (int w = 0; w < c->n; ++w) {
-    if (cfg->placement == 0) c->worker_rank[w] = (int)((long long)w * c->world / c->n);
-    else if (cfg->placement == 1) c->worker_rank[w] = w % c->world;
-    else if (cfg->placement == 2) {
-      if (!cfg->worker_rank) return fail(ADPSGD_E_INVALID, "explicit placement needs worker_rank");
-      c->worker_rank[w] = cfg->worker_rank[w];
-      if (c->worker_rank[w] < 0 || c->worker_rank[w] >= c->world) return fail(ADPSGD_E_INVALID, "worker_rank");
-    } else return fail(ADPSGD_E_INVALID, "placement");
-  }
-  c->worker_local.assign(c->n, 0);
-  std::vector<int> cnt(c->world, 0);
-  for (int w = 0; w < c->n; ++w) {
-    c->worker_local[w] = cnt[c->worker_rank[w]]++;
+  ST(compute_placement(c->n, c->world, cfg->placement, cfg->worker_rank, c->worker_rank, c->worker_local));
+  for (int w = 0; w < c->n; ++w)
     if (c->worker_rank[w] == c->rank) c->local_ids.push_back(w);
-  }
   c->n_local = (int)c->local_ids.size();
   if (c->n_local > kMaxLocal) return fail(ADPSGD_E_UNSUPPORTED, "more than 128 workers on one GPU");
   c->straggle.assign(c->n, 1.0f);
@@ -1043,6 +1061,58 @@ adpsgd_status adpsgd_launch_count(adpsgd_ctx* c, int64_t* out) {
   if (!c || !out) return fail(ADPSGD_E_INVALID, "null");
   *out = c->launches;
   return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_plan_placement(int32_t n, int32_t world_size, int32_t placement,
+                                    const int32_t* worker_rank_in, int32_t* worker_rank_out,
+                                    int32_t* local_index_out) {
+  GUARD({
+    if (!worker_rank_out || !local_index_out) return fail(ADPSGD_E_INVALID, "null output");
+    std::vector<int> wr, wl;
+    ST(compute_placement(n, world_size, placement, worker_rank_in, wr, wl));
+    for (int w = 0; w < n; ++w) { worker_rank_out[w] = wr[w]; local_index_out[w] = wl[w]; }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t rank, const adpsgd_event* schedule,
+                                 int64_t K, int64_t k0, uint32_t* epochs, int64_t* out, int64_t cap,
+                                 int64_t* n_out) {
+  GUARD({
+    if (n < 1 || !worker_rank || !epochs || K < 0 || (K > 0 && !schedule) || k0 < 0 || !n_out)
+      return fail(ADPSGD_E_INVALID, "plan_replay args");
+    std::vector<int> wr(worker_rank, worker_rank + n), wl(n, 0);
+    int world = 0;
+    for (int w = 0; w < n; ++w) world = std::max(world, wr[w] + 1);
+    std::vector<int> cnt(std::max(world, 1), 0);
+    for (int w = 0; w < n; ++w) {
+      if (wr[w] < 0) return fail(ADPSGD_E_INVALID, "worker_rank");
+      wl[w] = cnt[wr[w]]++;
+    }
+    for (int64_t e = 0; e < K; ++e)
+      if (schedule[e].i < 0 || schedule[e].i >= n || schedule[e].j < -1 || schedule[e].j >= n)
+        return fail(ADPSGD_E_INVALID, "event index");
+    const int n_local = rank >= 0 && rank < (int)cnt.size() ? cnt[rank] : 0;
+    std::vector<unsigned int> ep(epochs, epochs + n);
+    std::vector<std::vector<ReplayEv>> per;
+    plan_replay(wr, wl, rank, n_local, schedule, K, (unsigned long long)k0, ep, per);
+    int64_t m = 0;
+    for (auto& lst : per) m += (int64_t)lst.size();
+    if (out && cap < m) return fail(ADPSGD_E_INVALID, "output capacity");
+    int64_t t = 0;
+    if (out)
+      for (int l = 0; l < n_local; ++l) {
+        int w = 0;
+        while (!(wr[w] == rank && wl[w] == l)) ++w;
+        for (const ReplayEv& r : per[l]) {
+          int64_t* o = out + 6 * t++;
+          o[0] = r.k; o[1] = w; o[2] = r.j; o[3] = r.flags; o[4] = r.e_i; o[5] = r.e_j;
+        }
+      }
+    for (int w = 0; w < n; ++w) epochs[w] = ep[w];
+    *n_out = m;
+    return ADPSGD_OK;
+  })
 }
 
 adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
