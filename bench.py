@@ -156,6 +156,36 @@ def run_reference(a):
     print(json.dumps(line))
 
 
+def mlp_leg(P, synth, torch, events=64):
+    """Config 3 (BASELINE configs[2]): 2-layer MLP 3072 -> 512 -> 10, M = 128,
+    n = 8 workers co-located on this GPU, stale reads tau ~ U{0..4}; gradients
+    on tcgen05 (3xTF32).  Replay of a fixed schedule through the HOST executor."""
+    I, H, O, M, n, T = 3072, 512, 10, 128, 8, 4
+    X, y = synth.mlp_data(S=8192, n_in=I, n_out=O, s=0.02, seed=3)
+    x0 = synth.mlp_init(I, H, O, seed=4)
+    e, r = synth.ring(n)
+    ev, bi = synth.schedule_iid(n, e, K=events + 8, T=T, M=M, S=8192, seed=7)
+    ctx = P.Context(e, n, x0.size, role=r, T=T, model=P.MODEL_MLP, gamma=0.002, batch_M=M, data_A=X,
+                    data_y=y, mlp_dims=(I, H, O), x0=x0)
+    ctx.replay(ev[:8], batch_idx=bi[:8])
+    ctx.sync()
+    s = torch.cuda.Stream()
+    t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    l0 = ctx.launch_count()
+    t0.record(s)
+    ctx.replay(ev[8:], batch_idx=bi[8:], stream=s)
+    t1.record(s)
+    torch.cuda.synchronize()
+    sec = t0.elapsed_time(t1) / 1e3
+    flops = 2.0 * 2 * M * I * H + 2.0 * 3 * M * H * O      # the two big GEMMs + the N=10 layer
+    launches = ctx.launch_count() - l0
+    ctx.destroy()
+    return {"workload": f"config3: MLP {I}->{H}->{O}, M={M}, n={n} ring on 1 GPU, tau~U{{0..{T}}}, "
+                        f"{events} replayed events", "updates_per_s": events / sec,
+            "samples_per_s": events * M / sec, "ms_per_update": 1e3 * sec / events,
+            "algorithmic_tflops": flops * events / sec / 1e12, "kernel_launches": launches}
+
+
 # ---------------------------------------------------------------- our arm --
 def main():
     a = parse()
@@ -314,6 +344,8 @@ def main():
             barrier()
         extras["allreduce_sgd_baseline"] = ar
         extras["adpsgd_vs_allreduce_updates_ratio_straggler"] = upd_s / ar["straggler"]["updates_per_s"]
+        if world == 1:
+            extras["mlp_config3"] = mlp_leg(P, synth, torch)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_extras:
