@@ -23,9 +23,16 @@ struct alignas(128) WorkerCtl {
   unsigned int epoch;              // committed events touching this worker (replay order)
   unsigned long long updates;      // committed gradient updates made by this worker (p_i)
   unsigned long long gossips;      // pair averages initiated by / applied to this worker
-  unsigned int pad[26];
+  // push request (cross-GPU pair events, two-sided NVLink protocol): the GPU
+  // computing an event asks this worker's home GPU to push the row to it
+  unsigned int req_tag;            // (request seq << 2) | state, written remotely (release.sys)
+  int req_consumer;                // worker whose landing buffer receives the row
+  unsigned int req_tag16;          // consumer's event seq (low 16 bits) for the counters
+  unsigned int pad[23];
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
+
+constexpr int kMaxGrid = 1024;     // per-CTA push counters per landing buffer
 
 // One per rank; rank 0's `ticket` is the system-wide virtual counter k.
 struct alignas(128) GlobalCtl {
@@ -36,7 +43,9 @@ struct alignas(128) GlobalCtl {
   unsigned long long st_busy_ns;
   double st_bytes, st_nvl_bytes;
   unsigned int abort_flag;
-  unsigned int pad[13];
+  unsigned int pad0;
+  unsigned long long committed;    // rank 0: events committed system-wide (== ticket when quiescent)
+  unsigned int pad[10];
 };
 
 struct LogEntry {                  // == adpsgd_log_entry
@@ -51,6 +60,8 @@ struct LogEntry {                  // == adpsgd_log_entry
 struct WorkerDesc {
   float* x;                        // model row, d_pad floats
   WorkerCtl* ctl;
+  float* land;                     // landing row (partner rows pushed here), null if world 1
+  unsigned int* pcnt;              // kMaxGrid per-CTA push counters of the landing row
   int rank;                        // home rank
   int role;                        // 0 active, 1 passive
   int nb_off, nb_cnt;              // CSR neighbour range
@@ -259,17 +270,31 @@ struct Stager {
   // first + step, first + 2*step, ... (interleaved across the grid, so all
   // CTAs sweep the rows together -- measured ~5% more HBM throughput than
   // contiguous per-CTA slices, tools/membench.cu).
+  static __device__ __forceinline__ long long tiles_of(long long first, long long step, long long hi) {
+    const long long tot = (hi + kTile4 - 1) / kTile4;
+    return tot > first ? (tot - first + step - 1) / step : 0;
+  }
+
   template <bool kPair, int kGrad>
   __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long first, long long step,
                                       long long hi, long long d, float gamma, const QuadParams& q,
                                       uint32_t kk) {
-    const long long tot = (hi + kTile4 - 1) / kTile4;
-    const long long n_t = tot > first ? (tot - first + step - 1) / step : 0;
+    run_range<kPair, kGrad>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma, q, kk);
+  }
+
+  // Tiles [t0, t1) of this CTA's list; the partner row is read from xj_src and
+  // the average written to xj_dst (equal for an in-place pair; for a cross-GPU
+  // event xj_src is the local landing row and xj_dst the peer's model row).
+  template <bool kPair, int kGrad>
+  __device__ __forceinline__ void run_range(float4* xi4, const float4* xj_src, float4* xj_dst, long long first,
+                                            long long step, long long hi, long long t0, long long t1,
+                                            long long d, float gamma, const QuadParams& q, uint32_t kk) {
+    const long long n_t = t1 - t0;
     if (n_t <= 0) return;
     if (threadIdx.x == 0) {
       fence_proxy_async();
       for (long long t = 0; t < n_t && t < kStages; ++t)
-        issue(consumed + (uint32_t)t, xi4, kPair ? xj4 : nullptr, (first + t * step) * kTile4, hi);
+        issue(consumed + (uint32_t)t, xi4, kPair ? xj_src : nullptr, (first + (t0 + t) * step) * kTile4, hi);
     }
     for (long long t = 0; t < n_t; ++t) {
       const uint32_t g = consumed + (uint32_t)t;
@@ -277,7 +302,7 @@ struct Stager {
       mbar_wait(bar + s, (g / kStages) & 1u);
       const float4* sa = buf + (size_t)s * 2 * kTile4;
       const float4* sb = sa + kTile4;
-      const long long base = (first + t * step) * kTile4;
+      const long long base = (first + (t0 + t) * step) * kTile4;
       constexpr int kPer = kTile4 / 512;
       float4 a[kPer], b[kPer];
 #pragma unroll
@@ -298,12 +323,58 @@ struct Stager {
         if (idx < hi) {
           update4<kPair, kGrad>(a[u], b[u], make_float4(0.f, 0.f, 0.f, 0.f),
                                 make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d, gamma, q, kk);
-          if (kPair) st_cg4(xj4 + idx, b[u]);
+          if (kPair) st_cg4(xj_dst + idx, b[u]);
           st_cg4(xi4 + idx, a[u]);
         }
       }
       if (threadIdx.x == 0 && t + kStages < n_t)
-        issue(g + kStages, xi4, kPair ? xj4 : nullptr, (first + (t + kStages) * step) * kTile4, hi);
+        issue(g + kStages, xi4, kPair ? xj_src : nullptr, (first + (t0 + t + kStages) * step) * kTile4, hi);
+    }
+    consumed += (uint32_t)n_t;
+  }
+
+  // Push side of a cross-GPU event: copy this CTA's tiles of the local row src
+  // into the consumer's landing row dst (a peer address: NVLink writes only) and
+  // publish progress as cnt = (tag16 << 16) | tiles_done, release at system scope
+  // every kPublish tiles.  Never waits on another GPU.
+  template <int kPublish = 8>
+  __device__ __forceinline__ void push(const float4* src, float4* dst, unsigned int* cnt, unsigned int tag16,
+                                       long long first, long long step, long long hi) {
+    const long long n_t = tiles_of(first, step, hi);
+    if (n_t <= 0) return;
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      for (long long t = 0; t < n_t && t < kStages; ++t)
+        issue(consumed + (uint32_t)t, src, nullptr, (first + t * step) * kTile4, hi);
+    }
+    for (long long t = 0; t < n_t; ++t) {
+      const uint32_t g = consumed + (uint32_t)t;
+      const uint32_t s = g % kStages;
+      mbar_wait(bar + s, (g / kStages) & 1u);
+      const float4* sa = buf + (size_t)s * 2 * kTile4;
+      const long long base = (first + t * step) * kTile4;
+      constexpr int kPer = kTile4 / 512;
+      float4 a[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) a[u] = sa[u * 512 + (int)threadIdx.x];
+      if (kWarpEmpty) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
+      } else {
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const long long idx = base + u * 512 + (int)threadIdx.x;
+        if (idx < hi) st_cg4(dst + idx, a[u]);
+      }
+      if (threadIdx.x == 0 && t + kStages < n_t)
+        issue(g + kStages, src, nullptr, (first + (t + kStages) * step) * kTile4, hi);
+      if ((t + 1) % kPublish == 0 || t + 1 == n_t) {
+        __threadfence_system();                   // every thread's peer stores are performed
+        __syncthreads();
+        if (threadIdx.x == 0) st_release_sys(cnt, (tag16 << 16) | (unsigned int)(t + 1));
+      }
     }
     consumed += (uint32_t)n_t;
   }

@@ -13,15 +13,24 @@
 //   3. take ticket k (CAS on rank 0's counter, bounded by the run's target):
 //      the virtual counter of P:429-432, taken while holding the lock so the
 //      ticket order is the serialisation order (log replay).
-//   4. fused pass over d, split evenly across ALL CTAs of the grid:
-//      m = fl(fl(x_w + x_j)*0.5); x_j <- m (P2P store if remote);
-//      x_w <- fl(m - fl(gamma g)), g = quadratic gradient at the pre-average
-//      x_w (tau = 0) -- Alg. 1 steps 4-6, reading R1.
+//   4. fused pass over d, split across ALL CTAs of the grid (interleaved tiles):
+//      m = fl(fl(x_w + x_j)*0.5); x_j <- m; x_w <- fl(m - fl(gamma g)),
+//      g = quadratic gradient at the pre-average x_w (tau = 0) -- Alg. 1 steps
+//      4-6, reading R1.
 //   5. the CTA finishing the last slice commits: log {k,i,j,0}, counters,
 //      release fence (sys), unlock, schedule the next compute phase.
 // Replay mode (mode 1): the event list of each local worker is consumed in
 // order; event k starts when epoch[i] == e_i(k) and epoch[j] == e_j(k) (device
 // epoch flags, system scope), and commits by bumping both epochs.
+//
+// Cross-GPU pairs (world > 1), two-sided: the GPU computing the event posts a
+// push request on the partner's home GPU, whose engine copies x_j tile by tile
+// into the computing GPU's landing row (NVLink writes) and publishes per-CTA
+// progress counters; the computing CTAs consume tiles as they land (never
+// blocking: they return to the scheduler when nothing has landed) and write the
+// average back into x_j (NVLink writes).  NVLink then carries writes only, in
+// both directions: tools/membench measured 672 GB/s per direction for
+// bidirectional pushes vs 476 GB/s when one GPU both reads and writes its peer.
 #include "internal.h"
 
 namespace adp {
@@ -31,14 +40,22 @@ namespace {
 constexpr int kEngineThreads = 512;
 constexpr int kEngineUnroll = 2;
 constexpr int kExit = -2;
+constexpr int kPickPush = 1 << 20;      // pick codes >= kPickPush: push request of local worker
 
 struct SmemSlot {                  // tid 0 copies the running event here for the CTA
   float* xi;
   float* xj;
+  float* land;
   long long k;
   int grad;
   int pair;
   int cross;                       // partner row lives on another GPU (P2P stores)
+  long long t0, t1;                // tile sub-range (two-sided cross consume)
+  // push request
+  const float* src;
+  float* dst;
+  unsigned int* cnt;
+  unsigned int tag16;
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -62,6 +79,20 @@ __device__ __noinline__ bool take_ticket(const EngineParams& p, unsigned long lo
 __device__ void publish_running(Slot* sl, unsigned int seq) {
   __threadfence();                                   // fields before the tag
   st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
+}
+
+// cross-GPU event (two-sided): ask j's home GPU to push x_j into our landing row
+__device__ void post_push_request(const EngineParams& p, Slot* sl, int w, int j, unsigned int seq) {
+  const WorkerDesc& dw = p.workers[w];
+  const unsigned int tag16 = (seq + 1) & 0xffffu;    // the seq this event is published with
+  sl->tag16 = tag16;
+  sl->land = dw.land;
+  sl->pcnt = dw.pcnt;
+  WorkerCtl* cj = p.workers[j].ctl;                   // peer memory
+  const unsigned int rq = ld_acquire_sys(&cj->req_tag) >> 2;
+  *(volatile int*)&cj->req_consumer = w;
+  *(volatile unsigned int*)&cj->req_tag16 = tag16;
+  st_release_sys(&cj->req_tag, ((rq + 1u) << 2) | kStateRunning);
 }
 
 // Called by tid 0 of some CTA that found no slice to do.  Returns true if it
@@ -103,6 +134,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     sl->xi = dw.x; sl->xj = e.j >= 0 ? p.workers[e.j].x : nullptr;
     sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
     sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
+    if (sl->cross && p.two_sided) post_push_request(p, sl, w, e.j, seq);
     sl->ev_cur = cur + 1;
     sl->t0 = now;
     sl->done = 0;
@@ -143,6 +175,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
   sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
   sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
   sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
+  if (sl->cross && p.two_sided) post_push_request(p, sl, w, j, seq);
   sl->pending_j = -2;
   sl->nb_ctr += 1;
   sl->t0 = now;
@@ -183,6 +216,7 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     const float sw = p.workers[i].straggle;
     sl->ready_ns = now + (unsigned long long)((double)sw * (double)p.compute_ns);
   }
+  atomicAdd_system(&p.gctl0->committed, 1ull);
   const unsigned int seq = sl->tag >> 2;
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
 }
@@ -192,32 +226,39 @@ constexpr int kStages = 4;
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * kStages * sizeof(uint64_t);
 
 // engine variants: 0 = bulk-copy staged, CTA barrier per tile (default);
-// 1 = register slices (no staging); 2 = bulk-copy staged, per-warp empty
-// mbarriers.  tools/ab_engine.py on a fixed 512-event mix at d = 25.6M:
-// 5404 / 4996 / 5324 GB/s (variant 0 / 1 / 2).
+// 1 = register slices (no staging, one-sided cross access); 2 = bulk-copy
+// staged, per-warp empty mbarriers.  tools/ab_engine.py on a fixed 512-event
+// mix at d = 25.6M: 5404 / 4996 / 5324 GB/s (variant 0 / 1 / 2).
 template <int kVar>
 using EngineStager = Stager<kTile4, kStages, kVar == 2>;
 
 template <int kVar, bool kPair, int kGrad>
 __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, EngineStager<kVar>& stg) {
   const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
+  float4* xi4 = reinterpret_cast<float4*>(e.xi);
+  float4* xj4 = reinterpret_cast<float4*>(e.xj);
   if (kVar != 1) {
-    stg.template run<kPair, kGrad>(reinterpret_cast<float4*>(e.xi), reinterpret_cast<float4*>(e.xj),
-                                   blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk);
+    if (e.cross && p.two_sided)             // consume landed tiles [t0, t1); average back to x_j
+      stg.template run_range<kPair, kGrad>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
+                                           gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk);
+    else
+      stg.template run<kPair, kGrad>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk);
   } else {
     const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)blockIdx.x * per;
     const long long hi = lo + per < p.n4 ? lo + per : p.n4;
-    event_range<kPair, kGrad, kEngineUnroll>(reinterpret_cast<float4*>(e.xi),
-                                             reinterpret_cast<float4*>(e.xj), nullptr, nullptr, lo,
-                                             hi, threadIdx.x, blockDim.x, p.d, p.gamma, p.q, kk);
+    event_range<kPair, kGrad, kEngineUnroll>(xi4, xj4, nullptr, nullptr, lo, hi, threadIdx.x, blockDim.x, p.d,
+                                             p.gamma, p.q, kk);
   }
 }
 
 template <int kVar>
 __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_constant__ EngineParams p) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  __shared__ unsigned int done_seq[kMaxLocal];
+  __shared__ unsigned int done_seq[kMaxLocal];   // last event seq this CTA finished, per slot
+  __shared__ unsigned int push_seq[kMaxLocal];   // last push request seq this CTA served, per worker
+  __shared__ unsigned int cons_seq[kMaxLocal];   // event seq cons_cnt refers to
+  __shared__ unsigned int cons_cnt[kMaxLocal];   // tiles of a cross event consumed so far
   __shared__ int s_pick;
   __shared__ unsigned int s_seq;
   __shared__ SmemSlot s_ev;
@@ -233,31 +274,74 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     }
     mbar_fence_init();
   }
-  for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) done_seq[s] = 0u;
+  for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) {
+    done_seq[s] = 0u;
+    cons_seq[s] = 0u;
+    cons_cnt[s] = 0u;
+    push_seq[s] = 0xffffffffu;
+  }
+  __syncthreads();
+  if (p.two_sided)                           // push requests this CTA served in earlier launches
+    for (int l = threadIdx.x; l < p.n_local; l += blockDim.x) push_seq[l] = p.served[l * kMaxGrid + blockIdx.x];
   __syncthreads();
   const int L = p.n_local;
   const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
+  const long long my_tiles = EngineStager<kVar>::tiles_of(blockIdx.x, gridDim.x, p.n4);
   unsigned long long last_progress = globaltimer();
   while (true) {
     if (threadIdx.x == 0) {
       int pick = -1;
       if (ld_acquire_gpu(&p.gctl->abort_flag)) pick = kExit;
+      // 1. push requests from other GPUs (they unblock remote consumers; never wait)
+      if (p.two_sided)
+        for (int t = 0; t < L && pick == -1; ++t) {
+          const int l = (t + rot) % L;
+          WorkerCtl* c = p.workers[p.local_ids[l]].ctl;
+          const unsigned int tag = ld_acquire_sys(&c->req_tag);
+          if ((tag & 3u) == kStateRunning && (tag >> 2) != push_seq[l]) {
+            const int ci = *(volatile int*)&c->req_consumer;
+            s_ev.src = p.workers[p.local_ids[l]].x;
+            s_ev.dst = p.workers[ci].land;
+            s_ev.cnt = p.workers[ci].pcnt + blockIdx.x;
+            s_ev.tag16 = *(volatile unsigned int*)&c->req_tag16;
+            s_seq = tag >> 2;
+            pick = kPickPush + l;
+          }
+        }
+      // 2. running events with work for this CTA
       for (int t = 0; t < L && pick == -1; ++t) {
         const int s = (t + rot) % L;
         const unsigned int tag = ld_acquire_gpu(&p.slots[s].tag);
-        if ((tag & 3u) == kStateRunning && (tag >> 2) != done_seq[s]) {
-          pick = s;
-          s_seq = tag >> 2;
-          Slot* sl = p.slots + s;
-          s_ev.xi = *(float* volatile*)&sl->xi;
-          s_ev.xj = *(float* volatile*)&sl->xj;
-          s_ev.k = *(volatile long long*)&sl->k;
-          const unsigned int fl = *(volatile unsigned int*)&sl->flags;
-          s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
-          s_ev.pair = s_ev.xj != nullptr;
-          s_ev.cross = *(volatile int*)&sl->cross;
+        if ((tag & 3u) != kStateRunning || (tag >> 2) == done_seq[s]) continue;
+        Slot* sl = p.slots + s;
+        const int cross = *(volatile int*)&sl->cross;
+        long long t0 = 0, t1 = 0;
+        if (cross && p.two_sided && kVar != 1) {
+          if (cons_seq[s] != (tag >> 2)) { cons_seq[s] = tag >> 2; cons_cnt[s] = 0u; }
+          const unsigned int tag16 = *(volatile unsigned int*)&sl->tag16;
+          unsigned int avail = 0;
+          if (my_tiles > 0) {
+            const unsigned int v = ld_acquire_sys(*(unsigned int* volatile*)&sl->pcnt + blockIdx.x);
+            avail = (v >> 16) == tag16 ? (v & 0xffffu) : 0u;
+            if (avail <= cons_cnt[s]) continue;              // nothing landed yet: look elsewhere
+          }
+          t0 = cons_cnt[s];
+          t1 = avail;
+          s_ev.land = *(float* volatile*)&sl->land;
         }
+        pick = s;
+        s_seq = tag >> 2;
+        s_ev.xi = *(float* volatile*)&sl->xi;
+        s_ev.xj = *(float* volatile*)&sl->xj;
+        s_ev.k = *(volatile long long*)&sl->k;
+        const unsigned int fl = *(volatile unsigned int*)&sl->flags;
+        s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+        s_ev.pair = s_ev.xj != nullptr;
+        s_ev.cross = cross;
+        s_ev.t0 = t0;
+        s_ev.t1 = t1;
       }
+      // 3. scheduler duty
       if (pick == -1) {
         const unsigned long long now = globaltimer();
         int n_fin = 0;
@@ -269,7 +353,9 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           if (st == kStateFinished) ++n_fin;
           else if (st == kStateIdle) progress |= try_start(p, s, tag, now);
         }
-        if (n_fin == L) pick = kExit;
+        // local work done; with cross-GPU partners stay to serve push requests
+        // until every event of the run is committed system-wide
+        if (n_fin == L && (!p.two_sided || ld_relaxed_sys64(&p.gctl0->committed) >= p.target)) pick = kExit;
         if (progress) last_progress = now;
         else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
       } else {
@@ -280,7 +366,14 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     __syncthreads();
     const int pick = s_pick;
     if (pick == kExit) break;
-    if (pick >= 0) {
+    if (pick >= kPickPush) {
+      const SmemSlot e = s_ev;
+      if (kVar != 1)
+        stg.push(reinterpret_cast<const float4*>(e.src), reinterpret_cast<float4*>(e.dst), e.cnt, e.tag16,
+                 blockIdx.x, gridDim.x, p.n4);
+      __syncthreads();
+      if (threadIdx.x == 0) push_seq[pick - kPickPush] = s_seq;
+    } else if (pick >= 0) {
       const SmemSlot e = s_ev;
       if (e.pair) {
         if (e.grad) slice<kVar, true, kGradQuadInline>(p, e, stg);
@@ -290,24 +383,30 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        done_seq[pick] = s_seq;
-        // this CTA's slice is visible before its arrival; P2P stores need the
-        // system-scope fence, local ones only gpu scope (the committing CTA
-        // issues fence.sys before the cross-GPU release, which is cumulative)
-        if (e.cross) __threadfence_system();
-        else __threadfence();
-        if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) commit(p, pick);
+        bool finished = true;
+        if (e.cross && p.two_sided && kVar != 1) {
+          cons_cnt[pick] = (unsigned int)e.t1;
+          finished = e.t1 >= my_tiles;
+        }
+        if (finished) {
+          done_seq[pick] = s_seq;
+          // this CTA's slice is visible before its arrival; P2P stores need the
+          // system-scope fence, local ones only gpu scope (the committing CTA
+          // issues fence.sys before the cross-GPU release, which is cumulative)
+          if (e.cross) __threadfence_system();
+          else __threadfence();
+          if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) commit(p, pick);
+        }
       }
     } else if (threadIdx.x == 0) {
       __nanosleep(256);
     }
     __syncthreads();
   }
+  if (p.two_sided)
+    for (int l = threadIdx.x; l < p.n_local; l += blockDim.x) p.served[l * kMaxGrid + blockIdx.x] = push_seq[l];
 }
 
-}  // namespace
-
-namespace {
 const void* engine_fn(int variant, size_t* smem) {
   switch (variant) {
     case 1: *smem = 0; return (const void*)k_engine<1>;
@@ -315,6 +414,7 @@ const void* engine_fn(int variant, size_t* smem) {
     default: *smem = kTmaSmem; return (const void*)k_engine<0>;
   }
 }
+
 }  // namespace
 
 int engine_max_ctas_per_sm(int threads, int variant) {
@@ -329,7 +429,7 @@ int engine_max_ctas_per_sm(int threads, int variant) {
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s) {
   EngineParams pp = p;
   void* args[] = {&pp};
-  if (threads != kEngineThreads) return cudaErrorInvalidValue;
+  if (threads != kEngineThreads || grid > kMaxGrid) return cudaErrorInvalidValue;
   size_t smem = 0;
   const void* fn = engine_fn(p.variant, &smem);
   if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);

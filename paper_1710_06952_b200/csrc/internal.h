@@ -28,7 +28,9 @@ struct Slot {                      // per local worker, in local device memory
   int pending_j;                   // chosen partner awaiting its lock; -2 none
   long long ev_cur, ev_end;        // replay cursor into ReplayEv list
   int cross;                       // partner lives on another rank
-  int pad[5];
+  unsigned int tag16;              // push-counter tag of this event (cross, two-sided)
+  float* land;                     // local landing row the partner pushes x_j into (cross)
+  unsigned int* pcnt;              // per-CTA push counters of that landing row (cross)
 };
 
 struct ReplayEv {                  // one schedule event owned by this rank (i local)
@@ -62,6 +64,8 @@ struct EngineParams {
   uint2 seed;
   unsigned long long watchdog_ns;
   int variant;                     // 0 = bulk-copy (TMA) staged slices, 1 = register slices
+  int two_sided;                   // cross-GPU events via partner push (write-only NVLink)
+  unsigned int* served;            // [n_local][kMaxGrid] last push request served per CTA (persistent)
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);

@@ -223,6 +223,7 @@ __global__ void k_init_rows(float* X, int n_rows, long long d_pad, long long d, 
 __global__ void k_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
                               long long k, int i, int j, unsigned int flags, int grad) {
   atomicMax(&gctl0->ticket, (unsigned long long)(k + 1));
+  atomicMax(&gctl0->committed, (unsigned long long)(k + 1));
   if (grad) atomicAdd(&ctl_i->updates, 1ull);
   if (j >= 0) atomicAdd(&ctl_i->gossips, 1ull);
   if (log) {

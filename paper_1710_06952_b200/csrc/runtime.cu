@@ -55,8 +55,9 @@ struct PeerBlob {
   uint32_t magic, version;
   int32_t rank, n_local;
   int64_t d_pad;
-  int64_t gctl_offset, log_offset, log_cap;
-  cudaIpcMemHandle_t models, ctl;
+  int64_t gctl_offset, log_offset, log_cap, pcnt_offset;
+  int32_t has_land, engine_grid;
+  cudaIpcMemHandle_t models, ctl, land;
 };
 
 uint64_t splitmix64(uint64_t& s) {
@@ -95,7 +96,12 @@ struct adpsgd_ctx {
   cudaStream_t stream = nullptr;
   float* models = nullptr;
   char* ctl_arena = nullptr;
-  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0;
+  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0, pcnt_offset = 0;
+  float* land = nullptr;             // landing rows [n_local][d_pad] (world > 1)
+  unsigned int* served = nullptr;    // [n_local][kMaxGrid] push requests served per CTA
+  std::vector<float*> peer_land;
+  std::vector<size_t> peer_pcnt_off;
+  int engine_grid = 0;
   WorkerCtl* ctl = nullptr;
   GlobalCtl* gctl = nullptr;
   LogEntry* log = nullptr;           // rank 0 only (local)
@@ -208,13 +214,17 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
   for (int w = 0; w < c->n; ++w) {
     const int r = c->worker_rank[w];
     WorkerDesc& x = wd[w];
+    const long long l = c->worker_local[w];
     if (r == c->rank) {
       x.x = c->row(w);
-      x.ctl = c->ctl + c->worker_local[w];
+      x.ctl = c->ctl + l;
     } else {
-      x.x = c->peer_models[r] ? c->peer_models[r] + (long long)c->worker_local[w] * c->d_pad : nullptr;
-      x.ctl = c->peer_ctl[r] ? reinterpret_cast<WorkerCtl*>(c->peer_ctl[r]) + c->worker_local[w] : nullptr;
+      x.x = c->peer_models[r] ? c->peer_models[r] + l * c->d_pad : nullptr;
+      x.ctl = c->peer_ctl[r] ? reinterpret_cast<WorkerCtl*>(c->peer_ctl[r]) + l : nullptr;
     }
+    x.land = c->peer_land[r] ? c->peer_land[r] + l * c->d_pad : nullptr;
+    x.pcnt = c->peer_ctl[r] ? reinterpret_cast<unsigned int*>(c->peer_ctl[r] + c->peer_pcnt_off[r]) + l * kMaxGrid
+                            : nullptr;
     x.rank = r;
     x.role = c->role[w];
     x.nb_off = c->nb_off[w];
@@ -362,7 +372,8 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   }
   c->host_k = k0 + K;
   CU(launch_set_u64(&c->gctl0->ticket, c->host_k, s));
-  ++c->launches;
+  CU(launch_set_u64(&c->gctl0->committed, c->host_k, s));
+  c->launches += 2;
   return ADPSGD_OK;
 }
 
@@ -394,11 +405,17 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   int dev_sms = 0;
   CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
   p.variant = c->engine_variant;
+  p.two_sided = (c->world > 1 && p.variant != 1 && c->land) ? 1 : 0;
+  p.served = c->served;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
+  const int grid = cps * dev_sms;
+  // the two-sided protocol pairs CTA b of both GPUs tile by tile: same grid everywhere
+  if (p.two_sided && c->engine_grid && grid != c->engine_grid)
+    return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (two-sided NVLink protocol)");
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
-  CU(launch_engine(p, cps * dev_sms, c->engine_threads, s));
+  CU(launch_engine(p, grid, c->engine_threads, s));
   ++c->launches;
   ++c->run_counter;
   return ADPSGD_OK;
@@ -491,7 +508,7 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   if (!c->h_rev.empty())
     CU(cudaMemcpy(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice));
   CU(cudaMemcpy(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice));
-  ST(engine_launch(c, 1, 0, s));
+  ST(engine_launch(c, 1, k0 + (unsigned long long)K, s));
   c->host_k = k0 + (unsigned long long)K;
   return ADPSGD_OK;
 }
@@ -505,11 +522,12 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
     if ((int)r == c->rank) continue;
     if (c->peer_models[r]) cudaIpcCloseMemHandle(c->peer_models[r]);
     if (c->peer_ctl[r]) cudaIpcCloseMemHandle(c->peer_ctl[r]);
+    if (r < c->peer_land.size() && c->peer_land[r]) cudaIpcCloseMemHandle(c->peer_land[r]);
   }
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
   void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids, c->d_slots,
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
-                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum};
+                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served};
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -595,9 +613,10 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   } else if (c->n_local) {
     CU(launch_init_rows(c->models, c->n_local, c->d_pad, c->d, c->dx0, c->stream));
   }
-  // control arena: WorkerCtl[n_local] | GlobalCtl | (rank 0) log ring
+  // control arena: WorkerCtl[n_local] | GlobalCtl | push counters [n_local][kMaxGrid] | (rank 0) log
   c->gctl_offset = sizeof(WorkerCtl) * std::max(1, c->n_local);
-  c->log_offset = c->gctl_offset + sizeof(GlobalCtl);
+  c->pcnt_offset = c->gctl_offset + sizeof(GlobalCtl);
+  c->log_offset = c->pcnt_offset + sizeof(unsigned int) * kMaxGrid * std::max(1, c->n_local);
   c->ctl_bytes = c->log_offset + (c->rank == 0 ? sizeof(LogEntry) * c->log_cap : 0);
   CU(cudaMalloc(&c->ctl_arena, c->ctl_bytes));
   CU(cudaMemset(c->ctl_arena, 0, c->ctl_bytes));
@@ -634,9 +653,25 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   CU(cudaMalloc(&c->mk_acc, sizeof(double)));
   c->peer_models.assign(c->world, nullptr);
   c->peer_ctl.assign(c->world, nullptr);
+  c->peer_land.assign(c->world, nullptr);
+  c->peer_pcnt_off.assign(c->world, 0);
   c->peer_imported.assign(c->world, false);
+  if (c->world > 1 && c->n_local) {          // two-sided NVLink protocol state
+    CU(cudaMalloc(&c->land, sizeof(float) * c->d_pad * c->n_local));
+    CU(cudaMalloc(&c->served, sizeof(unsigned int) * kMaxGrid * c->n_local));
+    CU(cudaMemset(c->served, 0, sizeof(unsigned int) * kMaxGrid * c->n_local));
+  }
+  {
+    int sms = 0;
+    CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
+    const int occ = engine_max_ctas_per_sm(c->engine_threads, c->engine_variant);
+    const int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
+    c->engine_grid = cps * sms;
+  }
   c->peer_models[c->rank] = c->models;
   c->peer_ctl[c->rank] = c->ctl_arena;
+  c->peer_land[c->rank] = c->land;
+  c->peer_pcnt_off[c->rank] = c->pcnt_offset;
   c->peer_imported[c->rank] = true;
   c->last_evt.assign(c->n, nullptr);
   for (auto& e : c->last_evt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -698,8 +733,12 @@ adpsgd_status adpsgd_export_peer_info(adpsgd_ctx* c, void* buf, int64_t cap, int
     b.gctl_offset = (int64_t)c->gctl_offset;
     b.log_offset = (int64_t)c->log_offset;
     b.log_cap = c->log_cap;
+    b.pcnt_offset = (int64_t)c->pcnt_offset;
+    b.engine_grid = c->engine_grid;
     CU(cudaIpcGetMemHandle(&b.models, c->models));
     CU(cudaIpcGetMemHandle(&b.ctl, c->ctl_arena));
+    b.has_land = c->land ? 1 : 0;
+    if (c->land) CU(cudaIpcGetMemHandle(&b.land, c->land));
     memcpy(buf, &b, sizeof b);
     if (n_out) *n_out = (int64_t)sizeof b;
     return ADPSGD_OK;
@@ -726,6 +765,16 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
       return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer control: ") + cudaGetErrorString(e));
     c->peer_models[rank] = static_cast<float*>(pm);
     c->peer_ctl[rank] = static_cast<char*>(pc);
+    c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
+    if (b.engine_grid != c->engine_grid)
+      return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (different GPU models?)");
+    if (b.has_land) {
+      void* pl = nullptr;
+      e = cudaIpcOpenMemHandle(&pl, b.land, cudaIpcMemLazyEnablePeerAccess);
+      if (e != cudaSuccess)
+        return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer landing rows: ") + cudaGetErrorString(e));
+      c->peer_land[rank] = static_cast<float*>(pl);
+    }
     c->peer_imported[rank] = true;
     if (rank == 0) {
       c->gctl0 = reinterpret_cast<GlobalCtl*>(c->peer_ctl[0] + b.gctl_offset);
