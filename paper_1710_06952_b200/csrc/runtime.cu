@@ -405,7 +405,9 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   int dev_sms = 0;
   CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
   p.variant = c->engine_variant;
-  p.two_sided = (c->world > 1 && p.variant != 1 && c->land) ? 1 : 0;
+  // variant 3 = variant 0 with one-sided cross-GPU access (peer read + peer write)
+  p.two_sided = (c->world > 1 && (p.variant == 0 || p.variant == 2) && c->land) ? 1 : 0;
+  if (p.variant == 3) p.variant = 0;
   p.served = c->served;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
@@ -563,7 +565,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->engine_cps = cfg->engine_ctas_per_sm;
   c->engine_threads = 512;
   c->engine_variant = cfg->engine_variant;
-  if (c->engine_variant < 0 || c->engine_variant > 2) return fail(ADPSGD_E_INVALID, "engine_variant");
+  if (c->engine_variant < 0 || c->engine_variant > 3) return fail(ADPSGD_E_INVALID, "engine_variant");
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   ST(check_graph(c.get(), g));

@@ -328,3 +328,40 @@ def test_mlp_replay_within_1e4(P, dims, K, T):
     if K >= 1000:
         assert O.full_loss(prob, Xo.mean(0)) < 0.7 * O.full_loss(prob, x0)
     ctx.destroy()
+
+
+# ------------------------------------------------- spectral-gap contraction --
+def test_pure_gossip_contracts_at_the_spectral_rate(P):
+    """Config 2 property (north star): on the n = 16 bipartite ring, the seed-mean
+    consensus error E||Y_k||^2/||Y_0||^2 of GPU pure-gossip replays equals the
+    exact second moment tr(T^k(G0))/tr(G0) (reading R9) within 4 SE, stays below
+    the lemma's rho^k + 4 SE, and its fitted per-event log-rate
+    matches log r_T."""
+    from oracle import theory as TH
+    n, d, K, R = 16, 2048, 1600, 48
+    e, r = synth.ring(n)
+    rho = TH.rho(TH.expected_gram(n, e))
+    checkpoints = [100, 400, 800, 1200, 1600]
+    ratios = np.zeros((R, len(checkpoints)))
+    want = np.zeros((R, len(checkpoints)))
+    for s in range(R):
+        X0 = synth.x0_uniform(n, d, seed=500 + s)
+        ev, _ = synth.schedule_iid(n, e, K=K, seed=900 + s, no_grad=True)
+        ctx = P.Context(e, n, d, role=r, x0_per_worker=X0)
+        Y0 = X0.astype(np.float64) - X0.astype(np.float64).mean(0)
+        tr = TH.second_moment_trace(n, e, X0, K)
+        done = 0
+        for c, kc in enumerate(checkpoints):
+            ctx.replay(ev[done:kc], flags=P.REPLAY_HOST)
+            done = kc
+            X = read_all(ctx).astype(np.float64)
+            Y = X - X.mean(0)
+            ratios[s, c] = (Y ** 2).sum() / (Y0 ** 2).sum()
+            want[s, c] = tr[kc] / tr[0]
+        ctx.destroy()
+    m, se = ratios.mean(0), ratios.std(0) / np.sqrt(R)
+    assert np.all(np.abs(m - want.mean(0)) < 4 * se + 1e-12), (m, want.mean(0), se)
+    assert np.all(m <= rho ** np.array(checkpoints) + 4 * se)
+    slope = np.polyfit(checkpoints[1:], np.log(want.mean(0)[1:]), 1)[0]
+    fit = np.polyfit(checkpoints[1:], np.log(m[1:]), 1)[0]
+    assert abs(fit - slope) < 5e-4, (fit, slope)
