@@ -117,7 +117,7 @@ typedef struct {
   int32_t engine_ctas_per_sm; /* 0 = default                                                  */
   int32_t engine_variant;     /* 0 = bulk-copy (TMA) staged, CTA barrier per tile (default)   */
                               /* 1 = register slices; 2 = bulk-copy, per-warp empty barriers; */
-                              /* 3 = variant 0 with one-sided cross-GPU access (peer r+w)     */
+                              /* 3 = variant 0 + two-sided push protocol for cross-GPU pairs  */
   int64_t log_capacity;       /* event-log ring entries on rank 0; 0 = default (1<<20)        */
 } adpsgd_config;
 

@@ -405,8 +405,11 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   int dev_sms = 0;
   CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
   p.variant = c->engine_variant;
-  // variant 3 = variant 0 with one-sided cross-GPU access (peer read + peer write)
-  p.two_sided = (c->world > 1 && (p.variant == 0 || p.variant == 2) && c->land) ? 1 : 0;
+  // variant 3 = variant 0 with the two-sided push protocol for cross-GPU pairs.
+  // tools/ab_nvlink.py (2 B200, every event cross-GPU): one-sided 604/616 GB/s
+  // per GPU per direction vs two-sided 587/579 (pure gossip / quadratic), so
+  // one-sided peer access is the default.
+  p.two_sided = (c->world > 1 && p.variant == 3 && c->land) ? 1 : 0;
   if (p.variant == 3) p.variant = 0;
   p.served = c->served;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
