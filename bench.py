@@ -49,6 +49,7 @@ def parse():
     ap.add_argument("--cpu-events", type=int, default=12)
     ap.add_argument("--engine-variant", type=int, default=0, help="0 TMA-staged, 1 register slices")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
+    ap.add_argument("--topology", default="ring", choices=["ring", "skip"])
     return ap.parse_args()
 
 
@@ -101,6 +102,17 @@ class ClockSampler:
         reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower() == "active"})
         return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(self.rows)}
+
+
+def traffic_per_launch(alg_bytes):
+    """DRAM bytes per engine launch: the dram/algorithmic ratio of the committed
+    ncu --set full capture (profiles/engine_traffic.json) times this launch's
+    algorithmic bytes; None if no capture is committed."""
+    try:
+        t = json.load(open(os.path.join(ROOT, "profiles", "engine_traffic.json")))
+        return {"bytes": alg_bytes * t["dram_bytes_per_algorithmic_byte"], "source": t["source"]}
+    except Exception:
+        return None
 
 
 def peaks():
@@ -214,14 +226,17 @@ def main():
     n = a.workers_per_gpu * world
     d = a.d
     U = a.updates_per_step or 32 * n
-    e, r = synth.ring(n)
+    e, r = synth.skip_ring(n) if a.topology == "skip" else synth.ring(n)
     dk, nk = synth.quad_keys(5)
     s = float(np.float32(SIGMA * math.sqrt(3 * M_BATCH)))
     strag = synth.stragglers(n, slow_worker=0, slow=a.straggler)
     cns = int(a.compute_us * 1000)
 
-    def make_ctx(st):
-        return P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=a.placement,
+    def make_ctx(st, nn=None, ee=None, rr=None):
+        nn = n if nn is None else nn
+        ee = e if ee is None else ee
+        rr = r if rr is None else rr
+        return P.Context(ee, nn, d, role=rr, rank=rank, world_size=world, device=local, placement=a.placement,
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                          quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
                          engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm)
@@ -345,6 +360,47 @@ def main():
             barrier()
         extras["allreduce_sgd_baseline"] = ar
         extras["adpsgd_vs_allreduce_updates_ratio_straggler"] = upd_s / ar["straggler"]["updates_per_s"]
+        # config 5 (BASELINE configs[4]): 16 workers per GPU, heterogeneous stragglers
+        # s_w = 10^U[0,1] plus worker 0 at 10x, AD-PSGD vs the NCCL AllReduce-SGD baseline
+        n5 = 16 * world
+        e5, r5 = synth.ring(n5)
+        st5 = synth.stragglers(n5, seed=99, slow_worker=0, slow=10.0, hetero=True)
+        c5 = make_ctx(st5, n5, e5, r5)
+        U5, reps = 16 * n5, 3
+        c5.run(U5, stream)
+        torch.cuda.synchronize()
+        c5.sync()
+        barrier()
+        s50 = c5.stats()
+        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        ta.record(stream)
+        for _ in range(reps):
+            c5.run(U5, stream)
+        tb.record(stream)
+        torch.cuda.synchronize()
+        c5.sync()
+        barrier()
+        sec5 = maxr(ta.elapsed_time(tb)) / 1e3
+        s51 = c5.stats()
+        c5.allreduce_reset()
+        c5.allreduce_sgd(2, stream)
+        torch.cuda.synchronize()
+        barrier()
+        R5 = 8
+        ta.record(stream)
+        c5.allreduce_sgd(R5, stream)
+        tb.record(stream)
+        torch.cuda.synchronize()
+        sec5ar = maxr(ta.elapsed_time(tb)) / 1e3
+        c5.destroy()
+        barrier()
+        up5 = sumr(s51["local_events"] - s50["local_events"]) / sec5
+        extras["config5"] = {
+            "workload": f"n={n5} (16/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, t_c={a.compute_us}us",
+            "adpsgd_updates_per_s": up5,
+            "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
+            "allreduce_updates_per_s": R5 * n5 / sec5ar,
+            "adpsgd_vs_allreduce_updates_ratio": up5 / (R5 * n5 / sec5ar)}
         if world == 1:
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
 
@@ -370,7 +426,7 @@ def main():
                    nvl_bytes / sec / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / max(world, 1) / 900e9,
                    "frac_of_measured_peer_copy_770": nvl_bytes / sec / max(world, 1) / 770e9},
         "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": None,
+                     "frac": achieved / hbm_peak, "traffic": traffic_per_launch(loc_bytes / a.steps),
                      "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "clocks": clocks,

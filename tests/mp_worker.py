@@ -51,24 +51,31 @@ def main():
     if rank == 0:
         prob_q = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
 
-    # 1. pure gossip replay over NVLink (interleave: every edge crosses GPUs)
+    # 1. pure gossip replay over NVLink (interleave: every edge crosses GPUs),
+    #    two-sided push protocol (variant 3) and the one-sided default (variant 0)
     d = 1 << 20
     X0 = synth.x0_uniform(n, d, seed=21)
     ev, _ = synth.schedule_iid(n, e, K=1500, seed=4, no_grad=True)
-    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1, x0_per_worker=X0)
-    ctx.replay(ev, flags=P.REPLAY_ENGINE)
-    ctx.sync()
-    dist.barrier()
-    st = ctx.stats()
-    X = gather_models(ctx)
-    cross = [None] * world
-    dist.all_gather_object(cross, st["local_cross_events"])
     if rank == 0:
         Xo, _ = O.replay(O.OracleProblem(), X0, e, r, ev)
-        if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
-            fails.append("pure-gossip engine replay over NVLink not bit-exact")
-        if sum(cross) != 1500:
-            fails.append(f"expected every event to cross GPUs, got {sum(cross)}")
+    for variant in (3, 0):
+        ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+                        x0_per_worker=X0, engine_variant=variant)
+        ctx.replay(ev, flags=P.REPLAY_ENGINE)
+        ctx.sync()
+        dist.barrier()
+        st = ctx.stats()
+        X = gather_models(ctx)
+        cross = [None] * world
+        dist.all_gather_object(cross, st["local_cross_events"])
+        if rank == 0:
+            if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
+                fails.append(f"pure-gossip engine replay over NVLink not bit-exact (variant {variant})")
+            if sum(cross) != 1500:
+                fails.append(f"expected every event to cross GPUs, got {sum(cross)}")
+        if variant == 3:
+            ctx.destroy()
+            dist.barrier()
     # 4. consensus mean (NCCL fp64)
     out = torch.empty(d, dtype=torch.float32, device="cuda")
     mk = ctx.consensus_mean(out.data_ptr())

@@ -365,3 +365,24 @@ def test_pure_gossip_contracts_at_the_spectral_rate(P):
     slope = np.polyfit(checkpoints[1:], np.log(want.mean(0)[1:]), 1)[0]
     fit = np.polyfit(checkpoints[1:], np.log(m[1:]), 1)[0]
     assert abs(fit - slope) < 5e-4, (fit, slope)
+
+
+def test_skip_ring_free_running_log_replay(P):
+    """the skip ring (odd offsets 2^i+1 keep the
+    bipartite split) runs through the same engine; log replay is bitwise and
+    its rho is below the plain ring's (faster mixing)."""
+    from oracle import theory as TH
+    n, d, U = 16, 1 << 16, 2000
+    e, r = synth.skip_ring(n)
+    assert TH.rho(TH.expected_gram(n, e)) < TH.rho(TH.expected_gram(n, synth.ring(n)[0])) - 0.03
+    X0 = synth.x0_uniform(n, d, seed=31)
+    dk, nk = synth.quad_keys(12)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=0.3, seed=3)
+    ctx.run(U)
+    ctx.sync()
+    log = ctx.read_log(0)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=0.3)
+    Xo, _ = O.replay(prob, X0, e, r, log_events(log))
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    ctx.destroy()

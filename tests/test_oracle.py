@@ -436,3 +436,13 @@ def test_replay_deterministic():
     X1, m1 = O.replay(p, np.zeros((n, d), np.float32), e, r, ev, bi, T=3, mk_trace=True)
     X2, m2 = O.replay(p, np.zeros((n, d), np.float32), e, r, ev, bi, T=3, mk_trace=True)
     assert X1.tobytes() == X2.tobytes() and m1.tobytes() == m2.tobytes()
+
+
+def test_skip_ring_rho_matches_survey_table():
+    """SURVEY App. A.5 (odd-offset skip ring, law c4): n=8 0.963388, n=16 0.956747,
+    n=32 0.985724; the plain ring's closed form for the same n."""
+    for n, want in [(8, 0.963388), (16, 0.956747), (32, 0.985724)]:
+        e, r = synth.skip_ring(n)
+        st, _ = O.check_graph(n, e, role=r)
+        assert st == 0                                   # bipartite with parity roles
+        assert abs(TH.rho(TH.expected_gram(n, e)) - want) < 5e-7
