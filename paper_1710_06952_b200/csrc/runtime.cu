@@ -233,6 +233,7 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
     x.local = r == c->rank ? c->worker_local[w] : -1;
   }
   CU(cudaMemcpy(c->d_workers, wd.data(), sizeof(WorkerDesc) * c->n, cudaMemcpyHostToDevice));
+  CU(cudaDeviceSynchronize());   // pageable H2D may still be in flight; kernels use non-blocking streams
   return ADPSGD_OK;
 }
 
@@ -253,7 +254,9 @@ adpsgd_status ensure_gslots(adpsgd_ctx* c, int count) {
   if (c->gslots) cudaFree(c->gslots);
   c->gslots = nullptr;
   CU(cudaMalloc(&c->gslots, sizeof(float) * c->d_pad * count));
+  // legacy-stream memset: finish it before any kernel on a non-blocking stream
   CU(cudaMemset(c->gslots, 0, sizeof(float) * c->d_pad * count));
+  CU(cudaDeviceSynchronize());
   c->gslot_n = count;
   return ADPSGD_OK;
 }
@@ -511,8 +514,8 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
     c->rev_cap = c->h_rev.size() + 1;
   }
   if (!c->h_rev.empty())
-    CU(cudaMemcpy(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice));
-  CU(cudaMemcpy(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice));
+    CU(cudaMemcpyAsync(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice, s));
+  CU(cudaMemcpyAsync(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice, s));
   ST(engine_launch(c, 1, k0 + (unsigned long long)K, s));
   c->host_k = k0 + (unsigned long long)K;
   return ADPSGD_OK;
@@ -616,6 +619,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
       CU(cudaMemcpy(c->models + (long long)l * c->d_pad, cfg->x0_per_worker + (long long)c->local_ids[l] * d,
                     sizeof(float) * d, cudaMemcpyHostToDevice));
   } else if (c->n_local) {
+    // the memsets / copies above ran on the legacy stream, which a non-blocking
+    // stream does not wait for: settle them before the first kernel
+    CU(cudaDeviceSynchronize());
     CU(launch_init_rows(c->models, c->n_local, c->d_pad, c->d, c->dx0, c->stream));
   }
   // control arena: WorkerCtl[n_local] | GlobalCtl | push counters [n_local][kMaxGrid] | (rank 0) log
@@ -687,7 +693,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     ST(upload_workers(c.get()));
     c->connected = true;
   }
-  CU(cudaStreamSynchronize(c->stream));
+  CU(cudaDeviceSynchronize());
   *out = c.release();
   return ADPSGD_OK;
 }
@@ -945,8 +951,10 @@ adpsgd_status adpsgd_allreduce_reset(adpsgd_ctx* c, const float* host_x) {
       CU(cudaMalloc(&c->xr, sizeof(float) * c->d_pad));
       CU(cudaMalloc(&c->gsum, sizeof(float) * c->d_pad));
     }
+    CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(c->xr, c->dx0, sizeof(float) * c->d_pad, cudaMemcpyDeviceToDevice));
     if (host_x) CU(cudaMemcpy(c->xr, host_x, sizeof(float) * c->d, cudaMemcpyHostToDevice));
+    CU(cudaDeviceSynchronize());
     c->ar_k = 0;
     return ADPSGD_OK;
   })
@@ -994,6 +1002,7 @@ adpsgd_status adpsgd_sync(adpsgd_ctx* c) {
     CU(cudaMemcpy(&err, &c->gctl->error, sizeof err, cudaMemcpyDeviceToHost));
     if (err) {
       CU(cudaMemset(&c->gctl->error, 0, sizeof err));
+      CU(cudaDeviceSynchronize());
       return fail((adpsgd_status)err, "device-side error latched (e.g. watchdog timeout)");
     }
     return ADPSGD_OK;
@@ -1018,6 +1027,7 @@ adpsgd_status adpsgd_write_model(adpsgd_ctx* c, int32_t w, const float* host_in)
     if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "worker not local to this rank");
     CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(c->row(w), host_in, sizeof(float) * c->d, cudaMemcpyHostToDevice));
+    CU(cudaDeviceSynchronize());
     return ADPSGD_OK;
   })
 }
@@ -1107,6 +1117,7 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* c) {
     g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = 0;
     g.st_bytes = g.st_nvl_bytes = 0.0;
     CU(cudaMemcpy(c->gctl, &g, sizeof g, cudaMemcpyHostToDevice));
+    CU(cudaDeviceSynchronize());
     return ADPSGD_OK;
   })
 }

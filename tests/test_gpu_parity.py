@@ -153,7 +153,8 @@ def test_config1_replay_within_1e4(P, kind):
     prob = O.OracleProblem(okind, M=M, gamma=gamma, A=A, b=b)
     Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev, bi, T=T)
     ok = c11_ok(Xg, Xo)
-    assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum())
+    assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum(), O.full_loss(prob, Xg.mean(0)),
+                      O.full_loss(prob, Xo.mean(0)))
     assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * 0.5
     ctx.destroy()
 
