@@ -499,3 +499,50 @@ int oracle_allreduce_update(int32_t n, int64_t d, float gamma, const float* grad
   }
   return ORC_OK;
 }
+
+/* ------------------------------------------------------------- D-PSGD -----
+ * in every synchronous round all workers compute a minibatch
+ * gradient at their own model and average with their neighbours; the gradients
+ * are then applied.  Reading R19: X <- X W - gamma G with
+ * W = I - L/(deg_max + 1) (L the graph Laplacian), gradients at the pre-mix
+ * models.  fp32 op order (the definition both sides follow):
+ *   acc = fl(w_self_i * x_i); for j in N(i) ascending: acc = fl(acc + fl(w_nb * x_j));
+ *   x_i' = fl(acc - fl(gamma * g_i)),   w_nb = fl32(1/(deg_max+1)),
+ *   w_self_i = fl32(1 - deg_i/(deg_max+1)),  g_i = gradient at x_i for event k_base + i.
+ * X: n x d worker-major, updated in place (all reads see the pre-round X).    */
+int oracle_dpsgd_round(const oracle_problem* p, int32_t n, int64_t d, float* X, int32_t n_edges,
+                       const int32_t* edges, uint64_t k_base) {
+  if (!p || n < 1 || d < 1 || !X) return ORC_E_INVALID;
+  int32_t* deg = (int32_t*)calloc((size_t)n, sizeof(int32_t));
+  float* Xn = (float*)malloc(sizeof(float) * (size_t)n * (size_t)d);
+  float* g = (float*)malloc(sizeof(float) * (size_t)d);
+  if (!deg || !Xn || !g) { free(deg); free(Xn); free(g); return ORC_E_OOM; }
+  int32_t dmax = 0;
+  for (int32_t e = 0; e < n_edges; ++e) { deg[edges[2 * e]]++; deg[edges[2 * e + 1]]++; }
+  for (int32_t i = 0; i < n; ++i) if (deg[i] > dmax) dmax = deg[i];
+  const float w_nb = (float)(1.0 / (double)(dmax + 1));
+  int st = ORC_OK;
+  for (int32_t i = 0; i < n && st == ORC_OK; ++i) {
+    const float w_self = (float)(1.0 - (double)deg[i] / (double)(dmax + 1));
+    const float* xi = X + (int64_t)i * d;
+    if (p->kind != ORC_MODEL_NONE) st = oracle_gradient(p, d, xi, k_base + (uint64_t)i, NULL, g, NULL);
+    int32_t nb[64], nn = 0;                             /* neighbours in ascending order */
+    for (int32_t j = 0; j < n && nn < 64; ++j)
+      if (j != i && is_edge(n_edges, edges, i, j)) nb[nn++] = j;
+    for (int64_t c = 0; c < d; ++c) {
+      float acc = w_self * xi[c];
+      for (int32_t t = 0; t < nn; ++t) {
+        float v = w_nb * X[(int64_t)nb[t] * d + c];
+        acc = acc + v;
+      }
+      if (p->kind != ORC_MODEL_NONE) {
+        float step = p->gamma * g[c];
+        acc = acc - step;
+      }
+      Xn[(int64_t)i * d + c] = acc;
+    }
+  }
+  if (st == ORC_OK) memcpy(X, Xn, sizeof(float) * (size_t)n * (size_t)d);
+  free(deg); free(Xn); free(g);
+  return st;
+}

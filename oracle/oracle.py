@@ -183,3 +183,14 @@ def allreduce_update(x, grads, gamma):
 
 def mlp_dim(n_in, n_hid, n_out) -> int:
     return int(lib().oracle_mlp_dim(n_in, n_hid, n_out))
+
+
+def dpsgd_round(prob: OracleProblem, X, edges, k_base=0):
+    """One synchronous D-PSGD round (reading R19); returns the new X."""
+    X = np.ascontiguousarray(np.array(X, np.float32, copy=True))
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    L = lib()
+    L.oracle_dpsgd_round.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int64, C.c_void_p, C.c_int32,
+                                     C.c_void_p, C.c_uint64]
+    _check(L.oracle_dpsgd_round(prob.ref, X.shape[0], X.shape[1], _p(X), e.shape[0], _p(e), k_base))
+    return X

@@ -446,3 +446,21 @@ def test_skip_ring_rho_matches_survey_table():
         st, _ = O.check_graph(n, e, role=r)
         assert st == 0                                   # bipartite with parity roles
         assert abs(TH.rho(TH.expected_gram(n, e)) - want) < 5e-7
+
+
+def test_dpsgd_spec_example_and_invariants():
+    """S:265: n=2, models (1,3), f=x^2/2, gamma=0.1, W = pair average -> (1.9, 1.7);
+    W = I - L/(deg_max+1) is doubly stochastic: with no gradient the column sum is
+    preserved and a ring contracts to consensus."""
+    p = quad([1.0], [0.0], gamma=0.1)
+    X = O.dpsgd_round(p, [[1.0], [3.0]], [[0, 1]])
+    assert X[0, 0] == np.float32(2.0) - np.float32(0.1) and X[1, 0] == np.float32(2.0) - np.float32(np.float32(0.1) * 3)
+    assert abs(X[0, 0] - 1.9) < 1e-6 and abs(X[1, 0] - 1.7) < 1e-6
+    n, d = 8, 64
+    e, _ = synth.ring(n)
+    X0 = synth.x0_uniform(n, d, seed=2)
+    X = X0
+    for _ in range(200):
+        X = O.dpsgd_round(O.OracleProblem(), X, e)
+    assert np.abs(X.astype(np.float64).sum(0) - X0.astype(np.float64).sum(0)).max() < 1e-4
+    assert np.abs(X - X.mean(0)).max() < 1e-4 * np.abs(X0).max()
