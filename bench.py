@@ -339,27 +339,36 @@ def main():
         extras["no_straggler"] = {
             "gossip_steps_per_s": sumr(s21["local_pair_events"] - s20["local_pair_events"]) / (ms2 / 1e3),
             "updates_per_s": sumr(s21["local_events"] - s20["local_events"]) / (ms2 / 1e3)}
-        # AllReduce-SGD baseline (NCCL), with and without the straggler
-        ar = {}
+        # synchronous baselines (Table 4): AllReduce-SGD (NCCL all-reduce) and
+        # D-PSGD (neighbour averaging, NCCL halo exchange), with and without the straggler
+        ar, dp = {}, {}
         for tag, stv in (("straggler", strag), ("no_straggler", None)):
             c3 = make_ctx(stv)
-            c3.allreduce_reset()
             R = max(4, U // n)
-            c3.allreduce_sgd(2, stream)
-            torch.cuda.synchronize()
-            barrier()
-            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            ta.record(stream)
-            c3.allreduce_sgd(R, stream)
-            tb.record(stream)
-            torch.cuda.synchronize()
-            msa = maxr(ta.elapsed_time(tb))
-            ar[tag] = {"updates_per_s": R * n / (msa / 1e3), "samples_per_s": R * n * M_BATCH / (msa / 1e3),
-                       "rounds_per_s": R / (msa / 1e3)}
+            for kind, out in (("ar", ar), ("dp", dp)):
+                run = c3.allreduce_sgd if kind == "ar" else c3.dpsgd
+                if kind == "ar":
+                    c3.allreduce_reset()
+                else:
+                    c3.dpsgd_reset()
+                run(2, stream)
+                torch.cuda.synchronize()
+                barrier()
+                ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                ta.record(stream)
+                run(R, stream)
+                tb.record(stream)
+                torch.cuda.synchronize()
+                msa = maxr(ta.elapsed_time(tb))
+                out[tag] = {"updates_per_s": R * n / (msa / 1e3), "samples_per_s": R * n * M_BATCH / (msa / 1e3),
+                            "rounds_per_s": R / (msa / 1e3)}
+                barrier()
             c3.destroy()
             barrier()
         extras["allreduce_sgd_baseline"] = ar
+        extras["dpsgd_baseline"] = dp
         extras["adpsgd_vs_allreduce_updates_ratio_straggler"] = upd_s / ar["straggler"]["updates_per_s"]
+        extras["adpsgd_vs_dpsgd_updates_ratio_straggler"] = upd_s / dp["straggler"]["updates_per_s"]
         # config 5 (BASELINE configs[4]): 16 workers per GPU, heterogeneous stragglers
         # s_w = 10^U[0,1] plus worker 0 at 10x, AD-PSGD vs the NCCL AllReduce-SGD baseline
         n5 = 16 * world

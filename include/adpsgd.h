@@ -225,6 +225,17 @@ adpsgd_status adpsgd_allreduce_sgd(adpsgd_ctx* ctx, int64_t n_rounds, adpsgd_str
 adpsgd_status adpsgd_allreduce_read_model(adpsgd_ctx* ctx, float* host_out);
 adpsgd_status adpsgd_allreduce_reset(adpsgd_ctx* ctx, const float* host_x /* d or NULL=x0 */);
 
+/* D-PSGD comparison baseline (Table 4's second column), reading R19:
+ * synchronous rounds X <- X W - gamma G with W = I - L/(deg_max + 1) on the
+ * graph, gradients at each worker's own pre-round model (quadratic, event key
+ * round_base + w).  Runs on its own double-buffered replica of all rows; remote
+ * neighbour rows arrive each round by NCCL send/recv (a halo exchange); every
+ * round waits for its slowest worker (max_w s_w * t_c).  Collective.  fp32 op
+ * order as in the header comment of oracle_dpsgd_round (bit-exact).           */
+adpsgd_status adpsgd_dpsgd(adpsgd_ctx* ctx, int64_t n_rounds, adpsgd_stream s);
+adpsgd_status adpsgd_dpsgd_reset(adpsgd_ctx* ctx, const float* x0_per_worker /* n*d host or NULL = x0 */);
+adpsgd_status adpsgd_dpsgd_read_model(adpsgd_ctx* ctx, int32_t w, float* host_out);
+
 /* -------------------------------------------------------- state access ---- */
 adpsgd_status adpsgd_sync(adpsgd_ctx* ctx);   /* wait for all work; return latched device error */
 adpsgd_status adpsgd_read_model(adpsgd_ctx* ctx, int32_t w, float* host_out);   /* local w */

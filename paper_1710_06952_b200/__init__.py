@@ -32,7 +32,8 @@ EXPORTED = ["adpsgd_abi_version", "adpsgd_last_error", "adpsgd_init", "adpsgd_de
             "adpsgd_allreduce_reset", "adpsgd_sync", "adpsgd_read_model", "adpsgd_write_model",
             "adpsgd_model_device_ptr", "adpsgd_worker_rank", "adpsgd_get_ticket", "adpsgd_read_log",
             "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count",
-            "adpsgd_gemm_tf32x3", "adpsgd_plan_placement", "adpsgd_plan_replay"]
+            "adpsgd_gemm_tf32x3", "adpsgd_plan_placement", "adpsgd_plan_replay", "adpsgd_dpsgd",
+            "adpsgd_dpsgd_reset", "adpsgd_dpsgd_read_model"]
 
 
 class AdpsgdError(RuntimeError):
@@ -99,6 +100,8 @@ def lib():
             "adpsgd_gemm_tf32x3": ([P, P, P, I32, I32, I32, I32], I32),
             "adpsgd_plan_placement": ([I32, I32, I32, P, P, P], I32),
             "adpsgd_plan_replay": ([I32, P, I32, P, I64, I64, P, P, I64, P], I32),
+            "adpsgd_dpsgd": ([P, I64, P], I32), "adpsgd_dpsgd_reset": ([P, P], I32),
+            "adpsgd_dpsgd_read_model": ([P, I32, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -274,6 +277,18 @@ class Context:
     def allreduce_read_model(self):
         out = np.zeros(self.d, np.float32)
         _chk(lib().adpsgd_allreduce_read_model(self._h, _ptr(out)), "allreduce_read_model")
+        return out
+
+    def dpsgd(self, n_rounds, stream=None):
+        _chk(lib().adpsgd_dpsgd(self._h, int(n_rounds), _stream(stream)), "dpsgd")
+
+    def dpsgd_reset(self, x0_per_worker=None):
+        xa = _arr(x0_per_worker, np.float32)
+        _chk(lib().adpsgd_dpsgd_reset(self._h, _ptr(xa)), "dpsgd_reset")
+
+    def dpsgd_read_model(self, w):
+        out = np.zeros(self.d, np.float32)
+        _chk(lib().adpsgd_dpsgd_read_model(self._h, w, _ptr(out)), "dpsgd_read_model")
         return out
 
     # --------------------------------------------------------- state access --

@@ -100,6 +100,10 @@ cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStre
 cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, long long d,
                              long long n4, cudaStream_t s);
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t s);
+constexpr int kDpMaxDeg = 16;
+cudaError_t launch_dpsgd(const float* const* nbr, const int* deg, const float* w_self, float w_nb, const float* xin,
+                         float* xout, int n_local, long long d_pad, long long d, const QuadParams& q, int model,
+                         float gamma, unsigned long long k_base, const int* local_ids, cudaStream_t s);
 cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d, const float* x0,
                              cudaStream_t s);
 

@@ -4,6 +4,8 @@
 // the consensus output and the AllReduce-SGD baseline.
 // The persistent free-running/replay engine lives in engine.cu and reuses the
 // same per-float4 update (device.cuh: event_range / update4).
+#include <algorithm>
+
 #include "internal.h"
 
 namespace adp {
@@ -205,6 +207,33 @@ __global__ void __launch_bounds__(kThreads) k_ar_update(float* __restrict__ x,
   }
 }
 
+// ------------------------------------------------------ D-PSGD baseline ----
+// One synchronous round for this rank's rows (reading R19):
+//   acc = fl(w_self x_i); acc = fl(acc + fl(w_nb x_j)) for j in N(i) ascending;
+//   x_i' = fl(acc - fl(gamma g_i(x_i)))   (quadratic gradient, event k_base + i)
+// in[l*kDpMaxDeg + t] points at neighbour t's pre-round row (local or halo).
+__global__ void __launch_bounds__(kThreads) k_dpsgd(const float* const* __restrict__ nbr, const int* __restrict__ deg,
+                                                    const float* __restrict__ w_self, float w_nb,
+                                                    const float* __restrict__ xin, float* __restrict__ xout,
+                                                    long long d_pad, long long d, QuadParams q, int model,
+                                                    float gamma, unsigned long long k_base,
+                                                    const int* __restrict__ local_ids) {
+  const int l = blockIdx.y;
+  const float* xi = xin + (long long)l * d_pad;
+  float* xo = xout + (long long)l * d_pad;
+  const int nd = deg[l];
+  const float ws = w_self[l];
+  const uint32_t kk = quad_event_key_h(q.noise_key, k_base + (unsigned long long)local_ids[l]);
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d_pad;
+       c += (long long)gridDim.x * blockDim.x) {
+    const float x = __ldcg(xi + c);
+    float acc = __fmul_rn(ws, x);
+    for (int t = 0; t < nd; ++t) acc = __fadd_rn(acc, __fmul_rn(w_nb, __ldcg(nbr[l * kDpMaxDeg + t] + c)));
+    if (model != 0 && c < d) acc = __fsub_rn(acc, __fmul_rn(gamma, quad_grad(x, (uint32_t)c, q.data_key, kk, q.Mf, q.s)));
+    xo[c] = c < d ? acc : 0.0f;
+  }
+}
+
 // straggler / emulated-compute delay: one thread spins on %globaltimer
 __global__ void k_delay(unsigned long long ns) {
   const unsigned long long t0 = globaltimer();
@@ -326,6 +355,15 @@ cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log
 
 cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s) {
   k_set_u64<<<1, 1, 0, s>>>(p, v);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_dpsgd(const float* const* nbr, const int* deg, const float* w_self, float w_nb, const float* xin,
+                         float* xout, int n_local, long long d_pad, long long d, const QuadParams& q, int model,
+                         float gamma, unsigned long long k_base, const int* local_ids, cudaStream_t s) {
+  const int bx = (int)std::min<long long>((d_pad + kThreads - 1) / kThreads, std::max(1LL, 2LL * sm_count() / n_local));
+  k_dpsgd<<<dim3(bx, n_local), kThreads, 0, s>>>(nbr, deg, w_self, w_nb, xin, xout, d_pad, d, q, model, gamma, k_base,
+                                                 local_ids);
   return cudaGetLastError();
 }
 

@@ -131,6 +131,17 @@ struct adpsgd_ctx {
   double* mk_acc = nullptr;
   float *xr = nullptr, *gsum = nullptr;
   unsigned long long ar_k = 0;
+  // D-PSGD baseline (double-buffered rows + halo of remote neighbour rows)
+  float* dp_x[2] = {nullptr, nullptr};
+  float* dp_halo = nullptr;
+  const float** d_dp_nbr[2] = {nullptr, nullptr};
+  int* d_dp_deg = nullptr;
+  float* d_dp_wself = nullptr;
+  float dp_wnb = 0.f;
+  int dp_cur = 0;
+  unsigned long long dp_k = 0;
+  std::vector<int> dp_halo_w;                     // remote rows received each round (ascending id)
+  std::vector<std::pair<int, int>> dp_send;       // (local worker, destination rank), ascending id
   ncclComm_t comm = nullptr;
   bool connected = false;
   // ---- host executor state ----
@@ -535,7 +546,9 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
   void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids, c->d_slots,
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
-                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served};
+                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
+                  c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
+                  c->d_dp_wself};
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -990,6 +1003,128 @@ adpsgd_status adpsgd_allreduce_read_model(adpsgd_ctx* c, float* host_out) {
     CU(cudaStreamSynchronize(c->stream));
     CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(host_out, c->xr, sizeof(float) * c->d, cudaMemcpyDeviceToHost));
+    return ADPSGD_OK;
+  })
+}
+
+static adpsgd_status dpsgd_setup(adpsgd_ctx* c) {
+  if (c->dp_x[0]) return ADPSGD_OK;
+  const size_t rows = (size_t)std::max(1, c->n_local);
+  CU(cudaMalloc(&c->dp_x[0], sizeof(float) * c->d_pad * rows));
+  CU(cudaMalloc(&c->dp_x[1], sizeof(float) * c->d_pad * rows));
+  int dmax = 0;
+  for (int w = 0; w < c->n; ++w) dmax = std::max(dmax, (int)c->nb[w].size());
+  if (dmax > kDpMaxDeg) return fail(ADPSGD_E_UNSUPPORTED, "D-PSGD baseline supports degree <= 16");
+  c->dp_wnb = (float)(1.0 / (double)(dmax + 1));
+  // halo: remote neighbours of local workers (received), local workers needed remotely (sent)
+  std::vector<char> need(c->n, 0);
+  std::vector<std::vector<char>> sendto(c->n, std::vector<char>(c->world, 0));
+  for (int w : c->local_ids)
+    for (int j : c->nb[w])
+      if (!c->is_local(j)) need[j] = 1;
+  for (int w = 0; w < c->n; ++w)
+    if (!c->is_local(w))
+      for (int j : c->nb[w])
+        if (c->is_local(j)) sendto[j][c->worker_rank[w]] = 1;
+  c->dp_halo_w.clear();
+  c->dp_send.clear();
+  std::vector<int> halo_idx(c->n, -1);
+  for (int w = 0; w < c->n; ++w) {
+    if (need[w]) { halo_idx[w] = (int)c->dp_halo_w.size(); c->dp_halo_w.push_back(w); }
+    if (c->is_local(w))
+      for (int r = 0; r < c->world; ++r)
+        if (sendto[w][r]) c->dp_send.emplace_back(w, r);
+  }
+  if (!c->dp_halo_w.empty()) CU(cudaMalloc(&c->dp_halo, sizeof(float) * c->d_pad * c->dp_halo_w.size()));
+  std::vector<int> deg(rows, 0);
+  std::vector<float> wself(rows, 1.f);
+  for (int par = 0; par < 2; ++par) {
+    std::vector<const float*> tab(rows * kDpMaxDeg, nullptr);
+    for (int l = 0; l < c->n_local; ++l) {
+      const int w = c->local_ids[l];
+      deg[l] = (int)c->nb[w].size();
+      wself[l] = (float)(1.0 - (double)deg[l] / (double)(dmax + 1));
+      for (int t = 0; t < deg[l]; ++t) {            // ascending neighbour order (c->nb is sorted)
+        const int j = c->nb[w][t];
+        tab[l * kDpMaxDeg + t] = c->is_local(j) ? c->dp_x[par] + (long long)c->worker_local[j] * c->d_pad
+                                                : c->dp_halo + (long long)halo_idx[j] * c->d_pad;
+      }
+    }
+    CU(cudaMalloc(&c->d_dp_nbr[par], sizeof(const float*) * tab.size()));
+    CU(cudaMemcpy(c->d_dp_nbr[par], tab.data(), sizeof(const float*) * tab.size(), cudaMemcpyHostToDevice));
+  }
+  CU(cudaMalloc(&c->d_dp_deg, sizeof(int) * rows));
+  CU(cudaMemcpy(c->d_dp_deg, deg.data(), sizeof(int) * rows, cudaMemcpyHostToDevice));
+  CU(cudaMalloc(&c->d_dp_wself, sizeof(float) * rows));
+  CU(cudaMemcpy(c->d_dp_wself, wself.data(), sizeof(float) * rows, cudaMemcpyHostToDevice));
+  CU(cudaDeviceSynchronize());
+  return ADPSGD_OK;
+}
+
+adpsgd_status adpsgd_dpsgd_reset(adpsgd_ctx* c, const float* x0_per_worker) {
+  GUARD({
+    CTX_CHECK(c);
+    if (c->model != ADPSGD_MODEL_QUADRATIC && c->model != ADPSGD_MODEL_NONE)
+      return fail(ADPSGD_E_UNSUPPORTED, "D-PSGD baseline uses the quadratic (or no gradient)");
+    ST(dpsgd_setup(c));
+    CU(cudaDeviceSynchronize());
+    for (int l = 0; l < c->n_local; ++l) {
+      float* row = c->dp_x[0] + (long long)l * c->d_pad;
+      CU(cudaMemcpy(row, c->dx0, sizeof(float) * c->d_pad, cudaMemcpyDeviceToDevice));
+      if (x0_per_worker)
+        CU(cudaMemcpy(row, x0_per_worker + (long long)c->local_ids[l] * c->d, sizeof(float) * c->d,
+                      cudaMemcpyHostToDevice));
+    }
+    CU(cudaDeviceSynchronize());
+    c->dp_cur = 0;
+    c->dp_k = 0;
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_dpsgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_stream s) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    if (!c->dp_x[0]) ST(adpsgd_dpsgd_reset(c, nullptr));
+    cudaStream_t st = c->use(s);
+    float smax = 1.0f;
+    for (int w : c->local_ids) smax = std::max(smax, c->straggle[w]);
+    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns);
+    const int model = c->model == ADPSGD_MODEL_QUADRATIC ? 1 : 0;
+    for (int64_t r = 0; r < n_rounds; ++r) {
+      if (delay) { CU(launch_delay(delay, st)); ++c->launches; }     // the round waits for its slowest worker
+      float* xin = c->dp_x[c->dp_cur];
+      if (c->world > 1) {                                            // halo exchange (synchronous round)
+        NC(ncclGroupStart());
+        for (size_t h = 0; h < c->dp_halo_w.size(); ++h)
+          NC(ncclRecv(c->dp_halo + (long long)h * c->d_pad, (size_t)c->d_pad, ncclFloat32,
+                      c->worker_rank[c->dp_halo_w[h]], c->comm, st));
+        for (auto& ps : c->dp_send)
+          NC(ncclSend(xin + (long long)c->worker_local[ps.first] * c->d_pad, (size_t)c->d_pad, ncclFloat32,
+                      ps.second, c->comm, st));
+        NC(ncclGroupEnd());
+      }
+      if (c->n_local) {
+        CU(launch_dpsgd(c->d_dp_nbr[c->dp_cur], c->d_dp_deg, c->d_dp_wself, c->dp_wnb, xin, c->dp_x[1 - c->dp_cur],
+                        c->n_local, c->d_pad, c->d, c->q, model, c->gamma, c->dp_k, c->d_local_ids, st));
+        ++c->launches;
+      }
+      c->dp_cur ^= 1;
+      c->dp_k += (unsigned long long)c->n;
+    }
+    return ADPSGD_OK;
+  })
+}
+
+adpsgd_status adpsgd_dpsgd_read_model(adpsgd_ctx* c, int32_t w, float* host_out) {
+  GUARD({
+    CTX_CHECK(c);
+    if (w < 0 || w >= c->n || !host_out || !c->is_local(w) || !c->dp_x[0])
+      return fail(ADPSGD_E_INVALID, "worker / no D-PSGD state");
+    CU(cudaDeviceSynchronize());
+    CU(cudaMemcpy(host_out, c->dp_x[c->dp_cur] + (long long)c->worker_local[w] * c->d_pad, sizeof(float) * c->d,
+                  cudaMemcpyDeviceToHost));
     return ADPSGD_OK;
   })
 }

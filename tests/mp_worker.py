@@ -116,6 +116,23 @@ def main():
         if not np.array_equal(X2.view(np.uint32), Xo2.view(np.uint32)):
             bad = np.where((X2 != Xo2).any(1))[0]
             fails.append(f"free-running multi-GPU log replay not bit-exact (workers {bad.tolist()})")
+    # 6. D-PSGD baseline: halo exchange of neighbour rows by NCCL send/recv
+    X0d = synth.x0_uniform(n, d, seed=23)
+    ctx.dpsgd_reset(X0d)
+    ctx.dpsgd(4)
+    mine = {w: ctx.dpsgd_read_model(w) for w in ctx.local_workers()}
+    allm = [None] * world
+    dist.all_gather_object(allm, mine)
+    if rank == 0:
+        Xd = np.zeros((n, d), np.float32)
+        for m in allm:
+            for w, x in m.items():
+                Xd[w] = x
+        Xdo = X0d
+        for rr in range(4):
+            Xdo = O.dpsgd_round(prob_q, Xdo, e, k_base=rr * n)
+        if not np.array_equal(Xd.view(np.uint32), Xdo.view(np.uint32)):
+            fails.append("D-PSGD multi-GPU not bit-exact")
     # 5. AllReduce-SGD baseline over NCCL
     ctx.allreduce_reset()
     ctx.allreduce_sgd(5)

@@ -368,6 +368,27 @@ def test_pure_gossip_contracts_at_the_spectral_rate(P):
     assert abs(fit - slope) < 5e-4, (fit, slope)
 
 
+@pytest.mark.parametrize("topo", ["ring", "skip"])
+def test_dpsgd_baseline_bit_exact(P, topo):
+    """D-PSGD baseline (reading R19): synchronous rounds bit-exact
+    against the oracle (fixed fp32 op order, elementwise gradient)."""
+    n, d, R = 16, 10007, 12
+    e, r = synth.ring(n) if topo == "ring" else synth.skip_ring(n)
+    dk, nk = synth.quad_keys(13)
+    X0 = synth.x0_uniform(n, d, seed=41)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.02, batch_M=8, quad_keys=(dk, nk),
+                    quad_noise_s=0.3)
+    ctx.dpsgd_reset(X0)
+    ctx.dpsgd(R)
+    Xg = np.stack([ctx.dpsgd_read_model(w) for w in range(n)])
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=8, gamma=0.02, data_key=dk, noise_key=nk, noise_s=0.3)
+    Xo = X0
+    for rr in range(R):
+        Xo = O.dpsgd_round(prob, Xo, e, k_base=rr * n)
+    assert np.array_equal(Xg.view(np.uint32), Xo.view(np.uint32))
+    ctx.destroy()
+
+
 def test_skip_ring_free_running_log_replay(P):
     """the skip ring (odd offsets 2^i+1 keep the
     bipartite split) runs through the same engine; log replay is bitwise and
