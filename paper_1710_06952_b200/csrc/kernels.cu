@@ -218,19 +218,36 @@ __global__ void __launch_bounds__(kThreads) k_dpsgd(const float* const* __restri
                                                     long long d_pad, long long d, QuadParams q, int model,
                                                     float gamma, unsigned long long k_base,
                                                     const int* __restrict__ local_ids) {
+  __shared__ const float4* snb[kDpMaxDeg];
   const int l = blockIdx.y;
-  const float* xi = xin + (long long)l * d_pad;
-  float* xo = xout + (long long)l * d_pad;
+  const float4* xi = reinterpret_cast<const float4*>(xin + (long long)l * d_pad);
+  float4* xo = reinterpret_cast<float4*>(xout + (long long)l * d_pad);
   const int nd = deg[l];
   const float ws = w_self[l];
   const uint32_t kk = quad_event_key_h(q.noise_key, k_base + (unsigned long long)local_ids[l]);
-  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d_pad;
-       c += (long long)gridDim.x * blockDim.x) {
-    const float x = __ldcg(xi + c);
-    float acc = __fmul_rn(ws, x);
-    for (int t = 0; t < nd; ++t) acc = __fadd_rn(acc, __fmul_rn(w_nb, __ldcg(nbr[l * kDpMaxDeg + t] + c)));
-    if (model != 0 && c < d) acc = __fsub_rn(acc, __fmul_rn(gamma, quad_grad(x, (uint32_t)c, q.data_key, kk, q.Mf, q.s)));
-    xo[c] = c < d ? acc : 0.0f;
+  if (threadIdx.x < nd) snb[threadIdx.x] = reinterpret_cast<const float4*>(nbr[l * kDpMaxDeg + threadIdx.x]);
+  __syncthreads();
+  const long long n4 = d_pad / 4;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += (long long)gridDim.x * blockDim.x) {
+    const float4 x4 = ld_cg4(xi + i);
+    const float xv[4] = {x4.x, x4.y, x4.z, x4.w};
+    float acc[4];
+#pragma unroll
+    for (int e = 0; e < 4; ++e) acc[e] = __fmul_rn(ws, xv[e]);
+    for (int t = 0; t < nd; ++t) {
+      const float4 y4 = ld_cg4(snb[t] + i);
+      const float yv[4] = {y4.x, y4.y, y4.z, y4.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) acc[e] = __fadd_rn(acc[e], __fmul_rn(w_nb, yv[e]));
+    }
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const long long c = i * 4 + e;
+      if (model != 0 && c < d)
+        acc[e] = __fsub_rn(acc[e], __fmul_rn(gamma, quad_grad(xv[e], (uint32_t)c, q.data_key, kk, q.Mf, q.s)));
+      if (c >= d) acc[e] = 0.0f;
+    }
+    st_cg4(xo + i, make_float4(acc[0], acc[1], acc[2], acc[3]));
   }
 }
 
@@ -361,7 +378,9 @@ cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStre
 cudaError_t launch_dpsgd(const float* const* nbr, const int* deg, const float* w_self, float w_nb, const float* xin,
                          float* xout, int n_local, long long d_pad, long long d, const QuadParams& q, int model,
                          float gamma, unsigned long long k_base, const int* local_ids, cudaStream_t s) {
-  const int bx = (int)std::min<long long>((d_pad + kThreads - 1) / kThreads, std::max(1LL, 2LL * sm_count() / n_local));
+  // all rows of the round in one launch: ~2 waves of 512-thread CTAs over the GPU
+  const int bx = (int)std::min<long long>((d_pad / 4 + kThreads - 1) / kThreads,
+                                          std::max(1LL, 4LL * sm_count() / n_local));
   k_dpsgd<<<dim3(bx, n_local), kThreads, 0, s>>>(nbr, deg, w_self, w_nb, xin, xout, d_pad, d, q, model, gamma, k_base,
                                                  local_ids);
   return cudaGetLastError();
