@@ -50,6 +50,8 @@ adpsgd_status fail(adpsgd_status s, const std::string& m) {
   } while (0)
 
 constexpr uint32_t kBlobMagic = 0xADB5D200u;
+constexpr int kPoolStreams = 8;     // replay DAG stream lanes
+constexpr int kEventRing = 4096;    // recycled cudaEvents for the replay DAG
 
 struct PeerBlob {
   uint32_t magic, version;
@@ -124,7 +126,10 @@ struct adpsgd_ctx {
   float* gstep = nullptr;            // per-local-worker gradient buffers (adpsgd_step)
   float* mlp_scratch = nullptr;
   size_t mlp_scratch_n = 0;
-  MlpWork mlp_work{};
+  std::vector<MlpWork> mlp_work;     // one per replay stream lane
+  std::vector<cudaStream_t> pool;    // replay DAG streams
+  std::vector<cudaEvent_t> evring;
+  size_t evnext = 0;
   int* d_batch = nullptr;
   size_t batch_cap = 0;
   double* sum64 = nullptr;
@@ -272,20 +277,75 @@ adpsgd_status ensure_gslots(adpsgd_ctx* c, int count) {
   return ADPSGD_OK;
 }
 
-adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c) {
-  const size_t need = mlp_scratch_floats(c->mlp, c->M);
-  if (c->mlp_scratch_n >= need) return ADPSGD_OK;
+// one MLP scratch (gathered batch, W1 split, partial planes, tensor maps) per stream lane
+adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c, int lanes = 1) {
+  const size_t per = (mlp_scratch_floats(c->mlp, c->M) + 255) / 256 * 256;
+  if ((int)c->mlp_work.size() >= lanes) return ADPSGD_OK;
+  CU(cudaDeviceSynchronize());
   if (c->mlp_scratch) cudaFree(c->mlp_scratch);
   c->mlp_scratch = nullptr;
-  CU(cudaMalloc(&c->mlp_scratch, sizeof(float) * need));
-  c->mlp_scratch_n = need;
-  CU(mlp_plan(c->mlp_work, c->mlp, c->M, c->mlp_scratch));   // tensor maps over the scratch planes
+  CU(cudaMalloc(&c->mlp_scratch, sizeof(float) * per * lanes));
+  c->mlp_scratch_n = per * lanes;
+  c->mlp_work.assign(lanes, MlpWork{});
+  for (int l = 0; l < lanes; ++l)                                 // tensor maps over each lane's planes
+    CU(mlp_plan(c->mlp_work[l], c->mlp, c->M, c->mlp_scratch + per * l));
+  return ADPSGD_OK;
+}
+
+// ------------------------------------------------------ replay stream DAG --
+adpsgd_status ensure_pool(adpsgd_ctx* c, int ns) {
+  while ((int)c->pool.size() < ns) {
+    cudaStream_t st;
+    CU(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+    c->pool.push_back(st);
+  }
+  if (ns > 1 && c->evring.empty()) {
+    c->evring.assign(kEventRing, nullptr);
+    for (auto& e : c->evring) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  return ADPSGD_OK;
+}
+
+struct DagState {
+  std::vector<cudaEvent_t> w_evt;                 // last op that wrote worker w's row
+  std::vector<std::vector<cudaEvent_t>> r_evts;   // gradient reads of the row since that write
+  std::vector<cudaEvent_t> g_evt, gready;         // slot consumer / slot producer
+  DagState(int n, int slots) : w_evt(n, nullptr), r_evts(n), g_evt(slots, nullptr), gready(slots, nullptr) {}
+};
+
+adpsgd_status dag_wait(cudaStream_t st, cudaEvent_t e) {
+  if (e) CU(cudaStreamWaitEvent(st, e, 0));
+  return ADPSGD_OK;
+}
+
+// events are recycled from a ring: a recycled event stands for a LATER op
+// enqueued earlier in host order, so a wait on it is conservative, never cyclic
+adpsgd_status dag_record(adpsgd_ctx* c, cudaStream_t st, cudaEvent_t* out) {
+  cudaEvent_t e = c->evring[c->evnext++ % c->evring.size()];
+  CU(cudaEventRecord(e, st));
+  *out = e;
+  return ADPSGD_OK;
+}
+
+adpsgd_status dag_fork(adpsgd_ctx* c, cudaStream_t s, int ns) {
+  cudaEvent_t e;
+  ST(dag_record(c, s, &e));
+  for (int l = 0; l < ns; ++l) CU(cudaStreamWaitEvent(c->pool[l], e, 0));
+  return ADPSGD_OK;
+}
+
+adpsgd_status dag_join(adpsgd_ctx* c, cudaStream_t s, int ns) {
+  for (int l = 0; l < ns; ++l) {
+    cudaEvent_t e;
+    ST(dag_record(c, c->pool[l], &e));
+    CU(cudaStreamWaitEvent(s, e, 0));
+  }
   return ADPSGD_OK;
 }
 
 // gradient of the built-in model at xhat into g (minibatch of event k)
 adpsgd_status model_grad(adpsgd_ctx* c, const float* xhat, float* g, unsigned long long k,
-                         const int* idx_dev, cudaStream_t s) {
+                         const int* idx_dev, cudaStream_t s, int lane = 0) {
   switch (c->model) {
     case ADPSGD_MODEL_QUADRATIC:
       CU(launch_quad_grad(xhat, g, c->d, c->n4, c->q, k, s));
@@ -296,8 +356,8 @@ adpsgd_status model_grad(adpsgd_ctx* c, const float* xhat, float* g, unsigned lo
                             c->d, s));
       break;
     case ADPSGD_MODEL_MLP:
-      ST(ensure_mlp_scratch(c));
-      CU(launch_mlp_grad(c->mlp_work, c->dA, c->dy, c->S, idx_dev, c->seed2(), k, xhat, g, s));
+      ST(ensure_mlp_scratch(c, lane + 1));
+      CU(launch_mlp_grad(c->mlp_work[lane], c->dA, c->dy, c->S, idx_dev, c->seed2(), k, xhat, g, s));
       break;
     default:
       return fail(ADPSGD_E_UNSUPPORTED, "model has no built-in gradient");
@@ -364,26 +424,67 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
       if (bidx[t] < 0 || bidx[t] >= c->S) return fail(ADPSGD_E_INVALID, "batch index out of range");
     CU(cudaMemcpyAsync(c->d_batch, bidx, sizeof(int) * need, cudaMemcpyHostToDevice, s));
   }
+  // Events on disjoint workers commute (every coordinate sees the same op
+  // sequence), so large-d / heavy-gradient replays run as a DAG over a pool of
+  // streams: each op waits (cudaEvent) only for the last writer of the rows it
+  // reads, the readers of the rows it writes, and its gradient slot.  The
+  // result is bitwise the serial one.
+  const int ns = (c->model == ADPSGD_MODEL_MLP || c->d >= (1 << 16)) ? std::min(kPoolStreams, c->n) : 1;
+  ST(ensure_pool(c, ns));
+  if (c->model == ADPSGD_MODEL_MLP && need_slots) ST(ensure_mlp_scratch(c, ns));
+  DagState dag(c->n, slots);
+  if (ns > 1) ST(dag_fork(c, s, ns));
   for (int64_t e = 0; e < K; ++e) {
     for (int64_t kp : reads[e]) {     // stale reads that happen before event e
-      float* slot = c->gslots + (kp % slots) * c->d_pad;
+      const int i = ev[kp].i;
+      const int lane = ns > 1 ? i % ns : 0;
+      cudaStream_t st = ns > 1 ? c->pool[lane] : s;
+      const int sl = (int)(kp % slots);
+      if (ns > 1) { ST(dag_wait(st, dag.w_evt[i])); ST(dag_wait(st, dag.g_evt[sl])); }
+      float* slot = c->gslots + (long long)sl * c->d_pad;
       const int* idx = (sampled && bidx) ? c->d_batch + kp * c->M : nullptr;
-      ST(model_grad(c, c->row(ev[kp].i), slot, k0 + kp, idx, s));
+      ST(model_grad(c, c->row(i), slot, k0 + kp, idx, st, lane));
+      if (ns > 1) {
+        cudaEvent_t done;
+        ST(dag_record(c, st, &done));
+        dag.r_evts[i].push_back(done);
+        dag.gready[sl] = done;
+      }
     }
     const int i = ev[e].i, j = ev[e].j;
     const bool grad = has_model && !(ev[e].flags & ADPSGD_EV_NO_GRAD);
     int mode = kGradNone;
     const float* g = nullptr;
+    const int sl = (int)(e % slots);
     if (grad) {
       if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0) mode = kGradQuadInline;
-      else { mode = kGradExternal; g = c->gslots + (e % slots) * c->d_pad; }
+      else { mode = kGradExternal; g = c->gslots + (long long)sl * c->d_pad; }
     }
     if (j >= 0 || mode != kGradNone) {
+      cudaStream_t st = ns > 1 ? c->pool[i % ns] : s;
+      if (ns > 1) {
+        ST(dag_wait(st, dag.w_evt[i]));
+        for (cudaEvent_t r : dag.r_evts[i]) ST(dag_wait(st, r));
+        if (j >= 0) {
+          ST(dag_wait(st, dag.w_evt[j]));
+          for (cudaEvent_t r : dag.r_evts[j]) ST(dag_wait(st, r));
+        }
+        if (mode == kGradExternal) ST(dag_wait(st, dag.gready[sl]));
+      }
       CU(launch_event(c->row(i), j >= 0 ? c->row(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma,
-                      c->q, k0 + e, mode, s));
+                      c->q, k0 + e, mode, st));
       ++c->launches;
+      if (ns > 1) {
+        cudaEvent_t done;
+        ST(dag_record(c, st, &done));
+        dag.w_evt[i] = done;
+        dag.r_evts[i].clear();
+        if (j >= 0) { dag.w_evt[j] = done; dag.r_evts[j].clear(); }
+        if (mode == kGradExternal) dag.g_evt[sl] = done;
+      }
     }
   }
+  if (ns > 1) ST(dag_join(c, s, ns));
   c->host_k = k0 + K;
   CU(launch_set_u64(&c->gctl0->ticket, c->host_k, s));
   CU(launch_set_u64(&c->gctl0->committed, c->host_k, s));
@@ -544,6 +645,8 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
     if (r < c->peer_land.size() && c->peer_land[r]) cudaIpcCloseMemHandle(c->peer_land[r]);
   }
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
+  for (auto e : c->evring) if (e) cudaEventDestroy(e);
+  for (auto st : c->pool) if (st) cudaStreamDestroy(st);
   void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids, c->d_slots,
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
