@@ -14,7 +14,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libadpsgd.so")
+LIB_PATH = os.environ.get("ADPSGD_LIB", os.path.join(_HERE, "libadpsgd.so"))   # override: A/B builds
 _lib = None
 
 OK = 0

@@ -179,6 +179,7 @@ __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext,
   const float gv[4] = {gext.x, gext.y, gext.z, gext.w};
   const float hv[4] = {xh.x, xh.y, xh.z, xh.w};
   float out[4], mv[4];
+  const bool tail = (long long)c0 + 4 > d;       // only the last float4s of a row hold padding
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const float xhat = (kGrad == kGradQuadInline) ? av[e] : hv[e];   // tau = 0: pre-average x_i
@@ -190,7 +191,7 @@ __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext,
       float g;
       if (kGrad == kGradExternal) g = gv[e];
       else g = quad_grad(xhat, c0 + e, q.data_key, kk, q.Mf, q.s);
-      if ((long long)(c0 + e) >= d) g = 0.0f;                          // padding stays 0
+      if (tail && (long long)(c0 + e) >= d) g = 0.0f;                  // padding stays 0
       res = __fsub_rn(m, __fmul_rn(gamma, g));
     }
     out[e] = res;

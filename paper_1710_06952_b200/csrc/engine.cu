@@ -221,8 +221,16 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
 }
 
-constexpr int kTile4 = 512;              // float4 per stream per stage (8 KB)
-constexpr int kStages = 4;
+// tile x stages, fixed-mix A/B (tools/ab_engine.py, mixed / local-only GB/s):
+// 512x4 5356/4774, 1024x3 5488/5129, 1536x2 5589/5109, 2048x2 5491/5010
+#ifndef ADPSGD_TILE4
+#define ADPSGD_TILE4 1024
+#endif
+#ifndef ADPSGD_STAGES
+#define ADPSGD_STAGES 3
+#endif
+constexpr int kTile4 = ADPSGD_TILE4;     // float4 per stream per stage (16 KB)
+constexpr int kStages = ADPSGD_STAGES;
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * kStages * sizeof(uint64_t);
 
 // engine variants: 0 = bulk-copy staged, CTA barrier per tile (default);
