@@ -410,6 +410,73 @@ def main():
             "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
             "allreduce_updates_per_s": R5 * n5 / sec5ar,
             "adpsgd_vs_allreduce_updates_ratio": up5 / (R5 * n5 / sec5ar)}
+        # Table 4's shape: one worker slowed 1x / 2x / 10x / 100x; updates/s of
+        # AD-PSGD vs the two synchronous baselines (same emulated compute t_c per gradient)
+        t4 = {}
+        for slow in (1.0, 2.0, 10.0, 100.0):
+            stv = synth.stragglers(n, slow_worker=0, slow=slow)
+            c4 = make_ctx(stv)
+            c4.run(U, stream)
+            torch.cuda.synchronize()
+            c4.sync()
+            barrier()
+            s0 = c4.stats()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta.record(stream)
+            for _ in range(3):
+                c4.run(U, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            c4.sync()
+            barrier()
+            sec = maxr(ta.elapsed_time(tb)) / 1e3
+            row = {"adpsgd": sumr(c4.stats()["local_events"] - s0["local_events"]) / sec}
+            Rb = 4 if slow < 50 else 2
+            for kind in ("allreduce", "dpsgd"):
+                run = c4.allreduce_sgd if kind == "allreduce" else c4.dpsgd
+                (c4.allreduce_reset if kind == "allreduce" else c4.dpsgd_reset)()
+                run(1, stream)
+                torch.cuda.synchronize()
+                barrier()
+                ta.record(stream)
+                run(Rb, stream)
+                tb.record(stream)
+                torch.cuda.synchronize()
+                row[kind] = Rb * n / (maxr(ta.elapsed_time(tb)) / 1e3)
+                barrier()
+            c4.destroy()
+            barrier()
+            t4[f"x{slow:g}"] = row
+        extras["table4_updates_per_s"] = t4
+        if world > 1:
+            # NVLink stress: pure gossip, interleave placement -> every pair event crosses GPUs
+            cn = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+                           engine_variant=a.engine_variant, log_capacity=1 << 16)
+            cn.run(4 * n, stream)
+            torch.cuda.synchronize()
+            cn.sync()
+            barrier()
+            s0 = cn.stats()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta.record(stream)
+            for _ in range(3):
+                cn.run(16 * n, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            cn.sync()
+            barrier()
+            secn = maxr(ta.elapsed_time(tb)) / 1e3
+            s1 = cn.stats()
+            nvb = sumr(s1["local_nvlink_bytes"] - s0["local_nvlink_bytes"])
+            npair = sumr(s1["local_pair_events"] - s0["local_pair_events"])
+            cn.destroy()
+            barrier()
+            extras["nvlink_stress"] = {
+                "workload": f"pure gossip, n={n} ring, interleave placement (every pair crosses GPUs), d={d}",
+                "gossip_steps_per_s": npair / secn,
+                "per_gpu_per_direction_gbs": nvb / secn / world / 1e9,
+                "frac_of_900": nvb / secn / world / 900e9,
+                "frac_of_measured_peer_copy_770": nvb / secn / world / 770e9}
         if world == 1:
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
 
