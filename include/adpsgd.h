@@ -1,6 +1,6 @@
 /*
  * adpsgd.h -- C ABI of the B200-native AD-PSGD hot path (arXiv 1710.06952).
- * ABI version 1.  Implemented by paper_1710_06952_b200/libadpsgd.so (sm_100a).
+ * ABI version 2.  Implemented by paper_1710_06952_b200/libadpsgd.so (sm_100a).
  *
  * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
  *
@@ -45,7 +45,7 @@
 extern "C" {
 #endif
 
-#define ADPSGD_ABI_VERSION 1
+#define ADPSGD_ABI_VERSION 2
 
 typedef struct adpsgd_ctx adpsgd_ctx;
 typedef void* adpsgd_stream;
@@ -119,6 +119,14 @@ typedef struct {
                               /* 1 = register slices; 2 = bulk-copy, per-warp empty barriers; */
                               /* 3 = variant 0 + two-sided push protocol for cross-GPU pairs  */
   int64_t log_capacity;       /* event-log ring entries on rank 0; 0 = default (1<<20)        */
+  int32_t wait_free;          /* adpsgd_run loop: 0 = Alg. 1 (gradient fused into the event); */
+                              /* 1 = App. A wait-free runtime: a worker pulls   */
+                              /* its model, computes g into a buffer during s_w*t_c, and its  */
+                              /* communication loop flushes it (FLUSH_FIRST events) while     */
+                              /* actives keep averaging (NO_GRAD events) in between;          */
+                              /* 2 = as 1 plus local-update compensation (COMPENSATE).        */
+                              /* QUADRATIC model only; one-sided NVLink access.               */
+  int32_t reserved0;
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its
@@ -126,6 +134,20 @@ typedef struct {
  * tau is the staleness of the read, Xhat = X_{k - tau}.                         */
 typedef struct { int32_t i, j, tau; uint32_t flags; } adpsgd_event;
 #define ADPSGD_EV_NO_GRAD 1u   /* pure averaging: W_k only, no gradient update (k still advances) */
+/* App. A, the wait-free runtime, reading R20:
+ * FLUSH_FIRST  the communication thread flushes g into x_i BEFORE averaging
+ *              (Alg. 2 order): x_i <- fl(x_i - fl(gamma g));
+ *              m = fl(fl(x_i + x_j) * 0.5); x_i = x_j = m.  The gradient exists
+ *              before its flush event, so its random draws (noise, Philox batch)
+ *              are keyed by the read point: key = 2^62 | (k - tau) << 20 | i.
+ * COMPENSATE   local-update compensation (footnote at P:1265-1268): if worker
+ *              i's previous gradient event k_p (same schedule) has k_p >= k - tau,
+ *              i.e. it was still in the buffer when the model was pulled, the
+ *              gradient is evaluated at fl(xhat - fl(gamma g_p)).  Requires
+ *              k_p - tau_p <= k - tau (one gradient at a time per worker), else
+ *              ADPSGD_E_STALENESS.                                              */
+#define ADPSGD_EV_FLUSH_FIRST 2u
+#define ADPSGD_EV_COMPENSATE 4u
 
 /* Committed-event record written by the device (event log ring on rank 0).   */
 typedef struct {

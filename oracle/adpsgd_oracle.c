@@ -381,8 +381,28 @@ double oracle_full_loss(const oracle_problem* p, int64_t d, const float* x) {
  *   x_i <- fl(x_i - fl(gamma * g))                       (step 6)
  * X is row-major n x d (worker-major: the transpose of the paper's N x n).
  * mk_trace (nullable, K+1 entries): M_k with p_i = 1/n after each event
- * (P:1389-1391).  loss_trace unused (NULL).                                  */
+ * (P:1389-1391).  loss_trace unused (NULL).
+ *
+ * App. A events (the wait-free runtime; reading R20):
+ *   flags bit1 FLUSH_FIRST: Alg. 2's order -- "if g != 0:
+ *     x^i <- x^i - gamma g", then "x^i <- (x^i + x^j)/2" (the passive takes the
+ *     same average, Alg. 3):  x_i <- fl(x_i - fl(gamma g)); m = fl(fl(x_i + x_j)
+ *     * 0.5f); x_i = x_j = m.  The gradient's random draws are keyed by its read
+ *     point, key = 2^62 | (k0 + k - tau) << 20 | i, since it exists before its
+ *     flush event.
+ *   flags bit2 COMPENSATE: Alg. 1's footnote -- the computation
+ *     thread pulls x^i and applies "x^i <- x^i - gamma g" with the gradient g
+ *     still in the buffer, i.e. worker i's previous gradient event k_p when
+ *     k_p >= k - tau (not yet part of X_{k-tau}):  xhat <- fl(xhat - fl(gamma
+ *     g_p)).  One gradient at a time per worker (Alg. 1 blocks until g = 0):
+ *     k_p - tau_p > k - tau is ORC_E_STALENESS.                                */
 #define ORC_EV_NO_GRAD 1u
+#define ORC_EV_FLUSH_FIRST 2u
+#define ORC_EV_COMPENSATE 4u
+
+uint64_t oracle_read_key(uint64_t t_read, int32_t i) {
+  return (1ull << 62) | (t_read << 20) | (uint64_t)(uint32_t)i;
+}
 
 int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
                   int32_t n_edges, const int32_t* edges, const int8_t* role,
@@ -399,7 +419,17 @@ int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
   float* hist = (float*)malloc(sizeof(float) * (size_t)(nd * (T + 1)));
   float* xhat = (float*)malloc(sizeof(float) * (size_t)d);
   float* g = (float*)malloc(sizeof(float) * (size_t)d);
-  if (!hist || !xhat || !g) { free(r); free(hist); free(xhat); free(g); return ORC_E_OOM; }
+  /* App. A state: each worker's previous gradient event, its read point and value */
+  int64_t* kp = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int64_t* rp = (int64_t*)malloc(sizeof(int64_t) * (size_t)n);
+  int any_comp = 0;
+  for (int64_t k = 0; k < K; ++k) any_comp |= (events[4 * k + 3] & (int32_t)ORC_EV_COMPENSATE) != 0;
+  float* gp = any_comp ? (float*)malloc(sizeof(float) * (size_t)nd) : NULL;
+  if (!hist || !xhat || !g || !kp || !rp || (any_comp && !gp)) {
+    free(r); free(hist); free(xhat); free(g); free(kp); free(rp); free(gp);
+    return ORC_E_OOM;
+  }
+  for (int32_t w = 0; w < n; ++w) kp[w] = -1, rp[w] = -1;
   memcpy(hist, X, sizeof(float) * (size_t)nd);      /* X_0 at slot 0 */
   if (mk_trace) {
     double dummy;
@@ -424,15 +454,38 @@ int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
     const float* Xs = hist + nd * ((k - tau) % (T + 1));
     memcpy(xhat, Xs + (int64_t)i * d, sizeof(float) * (size_t)d);
     int do_grad = !(flags & ORC_EV_NO_GRAD) && p->kind != ORC_MODEL_NONE;
+    const int flush_first = (flags & ORC_EV_FLUSH_FIRST) != 0;
     if (do_grad) {
       const int32_t* idx = batch_idx ? batch_idx + k * p->M : NULL;
-      st = oracle_gradient(p, d, xhat, k0 + (uint64_t)k, idx, g, NULL);
+      uint64_t key = k0 + (uint64_t)k;
+      if (flush_first) key = oracle_read_key(k0 + (uint64_t)(k - tau), i);
+      if ((flags & ORC_EV_COMPENSATE) && kp[i] >= k - tau) {
+        /* pulled while g_p was still in the buffer: local update */
+        if (rp[i] > k - tau) { st = ORC_E_STALENESS; break; }
+        const float* gpi = gp + (int64_t)i * d;
+        for (int64_t c = 0; c < d; ++c) {
+          float step = p->gamma * gpi[c];
+          xhat[c] = xhat[c] - step;
+        }
+      }
+      st = oracle_gradient(p, d, xhat, key, idx, g, NULL);
       if (st != ORC_OK) break;
+      kp[i] = k; rp[i] = k - tau;
+      if (gp) memcpy(gp + (int64_t)i * d, g, sizeof(float) * (size_t)d);
     }
     /* X_{k+1} starts as a copy of X_k in the next history slot */
     float* Xn = hist + nd * ((k + 1) % (T + 1));
     if (Xn != Xk) memcpy(Xn, Xk, sizeof(float) * (size_t)nd);
     float* xi = Xn + (int64_t)i * d;
+    if (do_grad && flush_first) {       /* Alg. 2: flush g first */
+      for (int64_t c = 0; c < d; ++c) {
+        float step = p->gamma * g[c];
+        xi[c] = xi[c] - step;
+        if (!isfinite(xi[c])) st = ORC_E_DIVERGED;
+      }
+      if (st != ORC_OK) break;
+      do_grad = 0;
+    }
     if (j >= 0) {                       /* X_{k+1/2} = X_k W_k */
       float* xj = Xn + (int64_t)j * d;
       for (int64_t c = 0; c < d; ++c) {
@@ -455,7 +508,7 @@ int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
     }
   }
   if (st == ORC_OK) memcpy(X, hist + nd * (K % (T + 1)), sizeof(float) * (size_t)nd);
-  free(r); free(hist); free(xhat); free(g);
+  free(r); free(hist); free(xhat); free(g); free(kp); free(rp); free(gp);
   return st;
 }
 

@@ -20,6 +20,7 @@ _lock = threading.Lock()
 _lib = None
 
 MODEL_NONE, MODEL_QUADRATIC, MODEL_LSQ, MODEL_LOGREG, MODEL_MLP = 0, 2, 3, 4, 5
+EV_NO_GRAD, EV_FLUSH_FIRST, EV_COMPENSATE = 1, 2, 4     # App. A flags (reading R20)
 STATUS = {0: "OK", 1: "INVALID", 2: "NOT_BIPARTITE", 3: "DISCONNECTED", 4: "NOT_NEIGHBOURS",
           5: "STALENESS", 6: "DIVERGED", 10: "OOM"}
 
@@ -70,6 +71,8 @@ def lib():
             L.oracle_allreduce_update.argtypes = [C.c_int32, C.c_int64, C.c_float, P, P]
             L.oracle_mlp_dim.argtypes = [C.c_int32, C.c_int32, C.c_int32]
             L.oracle_mlp_dim.restype = C.c_int64
+            L.oracle_read_key.argtypes = [C.c_uint64, C.c_int32]
+            L.oracle_read_key.restype = C.c_uint64
             _lib = L
     return _lib
 
@@ -90,6 +93,11 @@ def philox(ctr, key):
     out = np.zeros(4, np.uint32)
     lib().oracle_philox4x32_10(_p(c), _p(k), _p(out))
     return out
+
+
+def read_key(t_read: int, i: int) -> int:
+    """Random-draw key of an App. A gradient read at X_{t_read} by worker i (R20)."""
+    return int(lib().oracle_read_key(t_read, i))
 
 
 def lowbias32(x: int) -> int:

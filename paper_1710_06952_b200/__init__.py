@@ -21,6 +21,7 @@ OK = 0
 STATUS = {0: "OK", 1: "E_INVALID", 2: "E_NOT_BIPARTITE", 3: "E_DISCONNECTED", 4: "E_NOT_NEIGHBOURS",
           5: "E_STALENESS", 6: "E_DIVERGED", 7: "E_TIMEOUT", 8: "E_CUDA", 9: "E_NCCL", 10: "E_OOM",
           11: "E_STATE", 12: "E_UNSUPPORTED"}
+EV_FLUSH_FIRST, EV_COMPENSATE = 2, 4   # App. A event flags (include/adpsgd.h, reading R20)
 MODEL_NONE, MODEL_EXTERNAL, MODEL_QUADRATIC, MODEL_LSQ, MODEL_LOGREG, MODEL_MLP = range(6)
 EV_NO_GRAD = 1
 REPLAY_HOST, REPLAY_ENGINE = 1, 2
@@ -56,7 +57,8 @@ class Config(C.Structure):
                 ("data_y", C.c_void_p), ("mlp_in", C.c_int32), ("mlp_hid", C.c_int32),
                 ("mlp_out", C.c_int32), ("x0", C.c_void_p), ("x0_per_worker", C.c_void_p),
                 ("straggler", C.c_void_p), ("compute_ns", C.c_int64), ("engine_ctas_per_sm", C.c_int32),
-                ("engine_variant", C.c_int32), ("log_capacity", C.c_int64)]
+                ("engine_variant", C.c_int32), ("log_capacity", C.c_int64),
+                ("wait_free", C.c_int32), ("reserved0", C.c_int32)]
 
 
 class Event(C.Structure):
@@ -179,7 +181,7 @@ class Context:
                  worker_rank=None, gamma=0.0, batch_M=1, T=0, seed=0, model=MODEL_NONE,
                  quad_keys=(0, 0), quad_noise_s=0.0, data_A=None, data_b=None, data_y=None,
                  mlp_dims=(0, 0, 0), x0=None, x0_per_worker=None, straggler=None, compute_ns=0,
-                 engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, connect=True, pg=None):
+                 engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, wait_free=0, connect=True, pg=None):
         self.n, self.d, self.rank, self.world = int(n), int(d), int(rank), int(world_size)
         e = _arr(np.asarray(edges).reshape(-1, 2), np.int32)
         r = _arr(role, np.int8)
@@ -203,6 +205,7 @@ class Context:
         cfg.x0, cfg.x0_per_worker, cfg.straggler = _ptr(x0a), _ptr(x0w), _ptr(st)
         cfg.compute_ns, cfg.engine_ctas_per_sm, cfg.engine_variant = int(compute_ns), engine_ctas_per_sm, engine_variant
         cfg.log_capacity = log_capacity
+        cfg.wait_free = int(wait_free)
         h = C.c_void_p()
         _chk(lib().adpsgd_init(C.byref(g), self.n, self.d, C.byref(cfg), C.byref(h)), "adpsgd_init")
         self._h = h

@@ -28,7 +28,17 @@ struct alignas(128) WorkerCtl {
   unsigned int req_tag;            // (request seq << 2) | state, written remotely (release.sys)
   int req_consumer;                // worker whose landing buffer receives the row
   unsigned int req_tag16;          // consumer's event seq (low 16 bits) for the counters
-  unsigned int pad[23];
+  // App. A wait-free runtime (home GPU only; persists across adpsgd_run calls):
+  // the computation thread's state and the shared gradient buffer g
+  unsigned int wf_state;           // 0 = pull next, 1 = computing (until wf_ready_ns)
+  unsigned long long wf_tread_cur; // read point t of the gradient being computed
+  unsigned long long wf_tread_pub; // read point of the gradient in the buffer
+  unsigned long long wf_ready_ns;  // compute phase of the current gradient ends
+  unsigned int wf_pub;             // buffer holds a gradient (g != 0)
+  unsigned int wf_buf;             // which of the worker's two gradient rows is the buffer
+  unsigned int wf_comp_cur;        // current gradient was compensated
+  unsigned int wf_comp_pub;        // buffered gradient was compensated
+  unsigned int pad[12];
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
 
@@ -67,6 +77,7 @@ struct WorkerDesc {
   int nb_off, nb_cnt;              // CSR neighbour range
   float straggle;                  // slowdown factor s_w >= 1
   int local;                       // index among this rank's workers, -1 if remote
+  float* gb;                       // App. A: two gradient rows (2 * d_pad), local workers only
 };
 
 // --------------------------------------------------------------- hashing ----
@@ -169,8 +180,17 @@ __device__ __forceinline__ unsigned long long globaltimer() {
 //   x_j <- m
 //   x_i <- fl(m - fl(gamma * g))  (g from the quadratic at xhat, or external)
 enum GradMode { kGradNone = 0, kGradExternal = 1, kGradQuadInline = 2, kGradQuadSnapshot = 3 };
+constexpr int kModeFlushFirst = 0x10;   // launch_event: grad_mode | kModeFlushFirst (App. A order)
 
-template <bool kPair, int kGrad>
+// Random-draw key of a gradient read at X_t by worker i in the App. A runtime
+// (reading R20): the gradient exists before its flush event k is known.
+__host__ __device__ __forceinline__ unsigned long long read_key(unsigned long long t, int i) {
+  return (1ull << 62) | (t << 20) | (unsigned long long)(uint32_t)i;
+}
+
+// kFF = App. A order (Alg. 2): x_i <- fl(x_i - fl(gamma g)) first,
+// then m = fl(fl(x_i + x_j) * 0.5) to both endpoints.
+template <bool kPair, int kGrad, bool kFF = false>
 __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext, const float4 xh,
                                         uint32_t c0, long long d, float gamma,
                                         const QuadParams& q, uint32_t kk) {
@@ -183,21 +203,41 @@ __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext,
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const float xhat = (kGrad == kGradQuadInline) ? av[e] : hv[e];   // tau = 0: pre-average x_i
-    float m = av[e];
-    if (kPair) m = __fmul_rn(__fadd_rn(av[e], bv[e]), 0.5f);
-    mv[e] = m;
-    float res = m;
+    float g = 0.0f;
     if (kGrad != kGradNone) {
-      float g;
       if (kGrad == kGradExternal) g = gv[e];
       else g = quad_grad(xhat, c0 + e, q.data_key, kk, q.Mf, q.s);
       if (tail && (long long)(c0 + e) >= d) g = 0.0f;                  // padding stays 0
-      res = __fsub_rn(m, __fmul_rn(gamma, g));
     }
-    out[e] = res;
+    if (kFF && kGrad != kGradNone) {
+      const float xi = __fsub_rn(av[e], __fmul_rn(gamma, g));
+      const float m = kPair ? __fmul_rn(__fadd_rn(xi, bv[e]), 0.5f) : xi;
+      mv[e] = m;
+      out[e] = m;
+    } else {
+      float m = av[e];
+      if (kPair) m = __fmul_rn(__fadd_rn(av[e], bv[e]), 0.5f);
+      mv[e] = m;
+      out[e] = kGrad != kGradNone ? __fsub_rn(m, __fmul_rn(gamma, g)) : m;
+    }
   }
   a = make_float4(out[0], out[1], out[2], out[3]);
   if (kPair) b = make_float4(mv[0], mv[1], mv[2], mv[3]);
+}
+
+// App. A computation thread: gradient of the pulled model, with
+// the local-update compensation xhat = fl(x - fl(gamma g_p)) when comp.
+__device__ __forceinline__ float4 pull4(const float4 x, const float4 gp, bool comp, uint32_t c0, long long d,
+                                        float gamma, const QuadParams& q, uint32_t kk) {
+  const float xv[4] = {x.x, x.y, x.z, x.w};
+  const float pv[4] = {gp.x, gp.y, gp.z, gp.w};
+  float out[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const float xh = comp ? __fsub_rn(xv[e], __fmul_rn(gamma, pv[e])) : xv[e];
+    out[e] = (long long)(c0 + e) < d ? quad_grad(xh, c0 + e, q.data_key, kk, q.Mf, q.s) : 0.0f;
+  }
+  return make_float4(out[0], out[1], out[2], out[3]);
 }
 
 // ------------------------------------------------- bulk-copy (TMA) staging ---
@@ -276,20 +316,24 @@ struct Stager {
     return tot > first ? (tot - first + step - 1) / step : 0;
   }
 
-  template <bool kPair, int kGrad>
+  template <bool kPair, int kGrad, bool kFF = false>
   __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long first, long long step,
                                       long long hi, long long d, float gamma, const QuadParams& q,
-                                      uint32_t kk) {
-    run_range<kPair, kGrad>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma, q, kk);
+                                      uint32_t kk, const float4* g4 = nullptr) {
+    run_range<kPair, kGrad, kFF>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma, q, kk,
+                                 g4);
   }
 
   // Tiles [t0, t1) of this CTA's list; the partner row is read from xj_src and
   // the average written to xj_dst (equal for an in-place pair; for a cross-GPU
   // event xj_src is the local landing row and xj_dst the peer's model row).
-  template <bool kPair, int kGrad>
+  // kGradExternal reads the gradient row g4 directly (L2), issued before the
+  // stage wait so it overlaps the bulk copies.
+  template <bool kPair, int kGrad, bool kFF = false>
   __device__ __forceinline__ void run_range(float4* xi4, const float4* xj_src, float4* xj_dst, long long first,
                                             long long step, long long hi, long long t0, long long t1,
-                                            long long d, float gamma, const QuadParams& q, uint32_t kk) {
+                                            long long d, float gamma, const QuadParams& q, uint32_t kk,
+                                            const float4* g4 = nullptr) {
     const long long n_t = t1 - t0;
     if (n_t <= 0) return;
     if (threadIdx.x == 0) {
@@ -300,11 +344,20 @@ struct Stager {
     for (long long t = 0; t < n_t; ++t) {
       const uint32_t g = consumed + (uint32_t)t;
       const uint32_t s = g % kStages;
+      const long long base = (first + (t0 + t) * step) * kTile4;
+      constexpr int kPer = kTile4 / 512;
+      float4 gx[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        gx[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+        if (kGrad == kGradExternal) {
+          const long long idx = base + u * 512 + (int)threadIdx.x;
+          if (idx < hi) gx[u] = ld_cg4(g4 + idx);
+        }
+      }
       mbar_wait(bar + s, (g / kStages) & 1u);
       const float4* sa = buf + (size_t)s * 2 * kTile4;
       const float4* sb = sa + kTile4;
-      const long long base = (first + (t0 + t) * step) * kTile4;
-      constexpr int kPer = kTile4 / 512;
       float4 a[kPer], b[kPer];
 #pragma unroll
       for (int u = 0; u < kPer; ++u) {
@@ -322,14 +375,60 @@ struct Stager {
       for (int u = 0; u < kPer; ++u) {
         const long long idx = base + u * 512 + (int)threadIdx.x;
         if (idx < hi) {
-          update4<kPair, kGrad>(a[u], b[u], make_float4(0.f, 0.f, 0.f, 0.f),
-                                make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d, gamma, q, kk);
+          update4<kPair, kGrad, kFF>(a[u], b[u], gx[u], make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d,
+                                     gamma, q, kk);
           if (kPair) st_cg4(xj_dst + idx, b[u]);
           st_cg4(xi4 + idx, a[u]);
         }
       }
       if (threadIdx.x == 0 && t + kStages < n_t)
         issue(g + kStages, xi4, kPair ? xj_src : nullptr, (first + (t0 + t + kStages) * step) * kTile4, hi);
+    }
+    consumed += (uint32_t)n_t;
+  }
+
+  // App. A pull (computation thread): gout = gradient at the
+  // pulled model x, compensated by the buffered gradient gp when gp != null.
+  // x and gp are staged like x_i / x_j of a pair event; x is not written.
+  __device__ __forceinline__ void pull(const float4* x4, const float4* gp4, float4* gout, long long first,
+                                       long long step, long long hi, long long d, float gamma, const QuadParams& q,
+                                       uint32_t kk) {
+    const long long n_t = tiles_of(first, step, hi);
+    if (n_t <= 0) return;
+    const bool comp = gp4 != nullptr;
+    if (threadIdx.x == 0) {
+      fence_proxy_async();
+      for (long long t = 0; t < n_t && t < kStages; ++t)
+        issue(consumed + (uint32_t)t, x4, gp4, (first + t * step) * kTile4, hi);
+    }
+    for (long long t = 0; t < n_t; ++t) {
+      const uint32_t g = consumed + (uint32_t)t;
+      const uint32_t s = g % kStages;
+      mbar_wait(bar + s, (g / kStages) & 1u);
+      const float4* sa = buf + (size_t)s * 2 * kTile4;
+      const float4* sb = sa + kTile4;
+      const long long base = (first + t * step) * kTile4;
+      constexpr int kPer = kTile4 / 512;
+      float4 a[kPer], b[kPer];
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const int off = u * 512 + (int)threadIdx.x;
+        a[u] = sa[off];
+        b[u] = comp ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      if (kWarpEmpty) {
+        __syncwarp();
+        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
+      } else {
+        __syncthreads();
+      }
+#pragma unroll
+      for (int u = 0; u < kPer; ++u) {
+        const long long idx = base + u * 512 + (int)threadIdx.x;
+        if (idx < hi) st_cg4(gout + idx, pull4(a[u], b[u], comp, (uint32_t)(idx * 4), d, gamma, q, kk));
+      }
+      if (threadIdx.x == 0 && t + kStages < n_t)
+        issue(g + kStages, x4, gp4, (first + (t + kStages) * step) * kTile4, hi);
     }
     consumed += (uint32_t)n_t;
   }
@@ -384,7 +483,7 @@ struct Stager {
 // Process float4 range [lo, hi) of one event with `nthreads` threads of a CTA.
 // Loads of the (possibly remote) partner row are issued first, U-deep, so that
 // NVLink latency overlaps the local HBM loads (SURVEY 8(a) sketch).
-template <bool kPair, int kGrad, int U>
+template <bool kPair, int kGrad, int U, bool kFF = false>
 __device__ __forceinline__ void event_range(float4* __restrict__ xi4, float4* __restrict__ xj4,
                                             const float4* __restrict__ g4,
                                             const float4* __restrict__ xh4, long long lo,
@@ -412,7 +511,7 @@ __device__ __forceinline__ void event_range(float4* __restrict__ xi4, float4* __
     for (int u = 0; u < U; ++u) {
       const long long idx = base + (long long)u * nthreads;
       if (idx < hi) {
-        update4<kPair, kGrad>(a[u], b[u], gg[u], hh[u], (uint32_t)(idx * 4), d, gamma, q, kk);
+        update4<kPair, kGrad, kFF>(a[u], b[u], gg[u], hh[u], (uint32_t)(idx * 4), d, gamma, q, kk);
         if (kPair) st_cg4(xj4 + idx, b[u]);
         st_cg4(xi4 + idx, a[u]);
       }

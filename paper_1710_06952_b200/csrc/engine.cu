@@ -56,6 +56,12 @@ struct SmemSlot {                  // tid 0 copies the running event here for th
   float* dst;
   unsigned int* cnt;
   unsigned int tag16;
+  // App. A: flush-first order, pulls, buffered gradients
+  int ff;
+  int kind;
+  unsigned long long key;
+  const float* g;
+  float* gout;
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -95,6 +101,97 @@ __device__ void post_push_request(const EngineParams& p, Slot* sl, int w, int j,
   st_release_sys(&cj->req_tag, ((rq + 1u) << 2) | kStateRunning);
 }
 
+// App. A wait-free runtime, reading R20.  A worker runs two
+// threads that share the gradient buffer g (one of its two gradient rows):
+//  * computation thread (App. A Alg. 1): pull x^w -- a consistent copy, so a
+//    passive holds its own lock; the read point t is the ticket counter at that
+//    moment -- and compute g' at x^w (compensated by the buffered g when
+//    wait_free == 2) into the other row; after s_w * t_c, when the buffer is
+//    empty, g' becomes the buffer;
+//  * communication thread (Alg. 2 / Alg. 3): an active flushes the buffer (if
+//    any) and averages with a random neighbour, continuously (NO_GRAD events
+//    when the buffer is empty); a passive flushes its buffer when it fills and
+//    otherwise only serves the actives' averages.
+// Both run as events of the worker's slot, so the pull is serialised with the
+// worker's own averages.  Pulls take no ticket (X does not change); flushes log
+// tau = k - t and the flags FLUSH_FIRST | COMPENSATE, which is all the oracle
+// needs to replay the run.
+__device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, unsigned int tag, int w,
+                                             unsigned long long now) {
+  const unsigned int seq = tag >> 2;
+  const WorkerDesc dw = p.workers[w];
+  volatile WorkerCtl* cw = dw.ctl;                     // home GPU control word
+  const bool active = dw.role == 0 && dw.nb_cnt > 0;
+  const long long dpad = p.n4 * 4;
+  if (cw->wf_state == 1u && now >= cw->wf_ready_ns && cw->wf_pub == 0u) {   // g' -> buffer
+    cw->wf_buf ^= 1u;
+    cw->wf_tread_pub = cw->wf_tread_cur;
+    cw->wf_comp_pub = cw->wf_comp_cur;
+    cw->wf_pub = 1u;
+    cw->wf_state = 0u;
+  }
+  if (cw->wf_state == 0u) {                            // computation thread: pull
+    unsigned int* lock = nullptr;
+    if (!active) {
+      lock = &dw.ctl->lock;
+      if (atomicCAS_system(lock, 0u, 1u) != 0u) { st_release_gpu(&sl->tag, tag); return false; }
+      __threadfence_system();
+    }
+    const unsigned long long t = ld_relaxed_sys64(&p.gctl0->ticket);
+    const bool comp = p.wait_free == 2 && cw->wf_pub != 0u;
+    cw->wf_tread_cur = t;
+    cw->wf_comp_cur = comp ? 1u : 0u;
+    sl->kind = kKindPull;
+    sl->i = w; sl->j = -1; sl->tau = 0; sl->flags = 0u; sl->k = -1;
+    sl->key = read_key(t, w);
+    sl->xi = dw.x; sl->xj = nullptr;
+    sl->g = comp ? dw.gb + (long long)cw->wf_buf * dpad : nullptr;
+    sl->gout = dw.gb + (long long)(cw->wf_buf ^ 1u) * dpad;
+    sl->ctl_i = dw.ctl; sl->ctl_j = nullptr; sl->lock = lock; sl->cross = 0;
+    sl->t0 = now;
+    sl->done = 0;
+    publish_running(sl, seq);
+    return true;
+  }
+  const bool flush = cw->wf_pub != 0u;                 // communication thread
+  int j = -1;
+  unsigned int* lock;
+  if (active) {
+    j = sl->pending_j;
+    if (j < -1) {
+      const uint4 r = philox4x32_10(make_uint4((uint32_t)w, sl->nb_ctr, 0x4E424F52u, 0u), p.seed);
+      j = p.nbrs[dw.nb_off + (int)(((unsigned long long)r.x * (unsigned)dw.nb_cnt) >> 32)];
+      sl->pending_j = j;
+    }
+    lock = &p.workers[j].ctl->lock;
+  } else {
+    if (!flush) { st_release_gpu(&sl->tag, tag); return false; }
+    lock = &dw.ctl->lock;
+  }
+  if (atomicCAS_system(lock, 0u, 1u) != 0u) { st_release_gpu(&sl->tag, tag); return false; }
+  __threadfence_system();
+  unsigned long long k;
+  if (!take_ticket(p, &k)) {
+    __threadfence_system();
+    atomicExch_system(lock, 0u);
+    st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
+    return true;
+  }
+  sl->kind = kKindEvent;
+  sl->i = w; sl->j = j; sl->k = (long long)k; sl->key = k;
+  sl->tau = flush ? (int)(k - cw->wf_tread_pub) : 0;
+  sl->flags = flush ? (2u | (cw->wf_comp_pub ? 4u : 0u)) : 1u;
+  sl->g = flush ? dw.gb + (long long)cw->wf_buf * dpad : nullptr;
+  sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
+  sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
+  sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
+  if (j >= 0) { sl->pending_j = -2; sl->nb_ctr += 1; }
+  sl->t0 = now;
+  sl->done = 0;
+  publish_running(sl, seq);
+  return true;
+}
+
 // Called by tid 0 of some CTA that found no slice to do.  Returns true if it
 // started or finished a worker (progress).
 __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned int tag, unsigned long long now) {
@@ -131,6 +228,8 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     }
     __threadfence_system();                                 // acquire their data
     sl->i = w; sl->j = e.j; sl->tau = 0; sl->flags = e.flags; sl->k = e.k;
+    sl->kind = kKindEvent; sl->g = nullptr;
+    sl->key = (e.flags & 2u) ? read_key((unsigned long long)e.k, w) : (unsigned long long)e.k;   // R20
     sl->xi = dw.x; sl->xj = e.j >= 0 ? p.workers[e.j].x : nullptr;
     sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
     sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
@@ -142,6 +241,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     return true;
   }
   // ------------------------------------------------------- free-running ----
+  if (p.wait_free) return start_wait_free(p, sl, tag, w, now);
   int j = -1;
   unsigned int* lock;
   if (dw.role == 0 && dw.nb_cnt > 0) {
@@ -172,6 +272,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     return true;
   }
   sl->i = w; sl->j = j; sl->tau = 0; sl->flags = p.model == 0 ? 1u : 0u; sl->k = (long long)k;
+  sl->kind = kKindEvent; sl->key = k; sl->g = nullptr;
   sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
   sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
   sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
@@ -189,22 +290,35 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   Slot* sl = p.slots + s;
   __threadfence_system();                 // every slice's stores (fenced by their CTAs) first
   const unsigned long long now = globaltimer();
+  const double d4 = 4.0 * (double)p.d;
+  if (sl->kind == kKindPull) {            // App. A: g' computed; its compute phase starts now
+    volatile WorkerCtl* cw = sl->ctl_i;
+    cw->wf_ready_ns = now + (unsigned long long)((double)p.workers[sl->i].straggle * (double)p.compute_ns);
+    cw->wf_state = 1u;
+    atomicAdd(&p.gctl->st_bytes, (sl->g ? 3.0 : 2.0) * d4);
+    atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
+    if (sl->lock) { __threadfence_system(); atomicExch_system(sl->lock, 0u); }
+    const unsigned int seq = sl->tag >> 2;
+    st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
+    return;
+  }
   const int i = sl->i, j = sl->j;
   const unsigned int flags = sl->flags;
   const long long k = sl->k;
   const bool grad = !(flags & 1u) && p.model != 0;
+  if (p.wait_free && grad) ((volatile WorkerCtl*)sl->ctl_i)->wf_pub = 0u;   // buffer flushed (g <- 0)
   if (grad) atomicAdd(&sl->ctl_i->updates, 1ull);
   if (j >= 0) atomicAdd(&sl->ctl_i->gossips, 1ull);
   // event log (rank 0's ring; a P2P store when this rank is not 0)
   LogEntry* le = p.log + (k % p.log_cap);
   le->k = k; le->i = i; le->j = j; le->tau = sl->tau; le->flags = flags;
   le->t0 = sl->t0; le->t1 = now;
-  // stats: algorithmic bytes: pair 16d, local 8d; NVLink 8d per cross pair
-  const double d4 = 4.0 * (double)p.d;
+  // stats: algorithmic bytes: pair 16d, local 8d; NVLink 8d per cross
+  // pair; a flushed App. A buffer adds its 4d read
   atomicAdd(&p.gctl->st_events, 1ull);
   if (j >= 0) atomicAdd(&p.gctl->st_pair, 1ull);
   if (sl->cross) { atomicAdd(&p.gctl->st_cross, 1ull); atomicAdd(&p.gctl->st_nvl_bytes, 2.0 * d4); }
-  atomicAdd(&p.gctl->st_bytes, (j >= 0 ? 4.0 : (grad ? 2.0 : 0.0)) * d4);
+  atomicAdd(&p.gctl->st_bytes, ((j >= 0 ? 4.0 : (grad ? 2.0 : 0.0)) + (sl->g && grad ? 1.0 : 0.0)) * d4);
   atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
   __threadfence_system();                 // log + data before the release below
   if (p.mode == 1) {
@@ -214,7 +328,9 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   } else {
     atomicExch_system(sl->lock, 0u);
     const float sw = p.workers[i].straggle;
-    sl->ready_ns = now + (unsigned long long)((double)sw * (double)p.compute_ns);
+    // Alg. 1 loop: the next gradient is computed before the next event; in the
+    // App. A runtime the communication thread never waits for it
+    sl->ready_ns = p.wait_free ? 0ull : now + (unsigned long long)((double)sw * (double)p.compute_ns);
   }
   atomicAdd_system(&p.gctl0->committed, 1ull);
   const unsigned int seq = sl->tag >> 2;
@@ -240,23 +356,24 @@ constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * 
 template <int kVar>
 using EngineStager = Stager<kTile4, kStages, kVar == 2>;
 
-template <int kVar, bool kPair, int kGrad>
+template <int kVar, bool kPair, int kGrad, bool kFF = false>
 __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, EngineStager<kVar>& stg) {
-  const uint32_t kk = quad_event_key_h(p.q.noise_key, (unsigned long long)e.k);
+  const uint32_t kk = quad_event_key_h(p.q.noise_key, e.key);
   float4* xi4 = reinterpret_cast<float4*>(e.xi);
   float4* xj4 = reinterpret_cast<float4*>(e.xj);
+  const float4* g4 = reinterpret_cast<const float4*>(e.g);
   if (kVar != 1) {
     if (e.cross && p.two_sided)             // consume landed tiles [t0, t1); average back to x_j
-      stg.template run_range<kPair, kGrad>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
-                                           gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk);
+      stg.template run_range<kPair, kGrad, kFF>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
+                                                gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk, g4);
     else
-      stg.template run<kPair, kGrad>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk);
+      stg.template run<kPair, kGrad, kFF>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk, g4);
   } else {
     const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)blockIdx.x * per;
     const long long hi = lo + per < p.n4 ? lo + per : p.n4;
-    event_range<kPair, kGrad, kEngineUnroll>(xi4, xj4, nullptr, nullptr, lo, hi, threadIdx.x, blockDim.x, p.d,
-                                             p.gamma, p.q, kk);
+    event_range<kPair, kGrad, kEngineUnroll, kFF>(xi4, xj4, g4, nullptr, lo, hi, threadIdx.x, blockDim.x, p.d,
+                                                  p.gamma, p.q, kk);
   }
 }
 
@@ -344,6 +461,11 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.k = *(volatile long long*)&sl->k;
         const unsigned int fl = *(volatile unsigned int*)&sl->flags;
         s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+        s_ev.ff = (fl & 2u) ? 1 : 0;
+        s_ev.kind = *(volatile int*)&sl->kind;
+        s_ev.key = *(volatile unsigned long long*)&sl->key;
+        s_ev.g = *(float* volatile*)&sl->g;
+        s_ev.gout = *(float* volatile*)&sl->gout;
         s_ev.pair = s_ev.xj != nullptr;
         s_ev.cross = cross;
         s_ev.t0 = t0;
@@ -375,17 +497,29 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     const int pick = s_pick;
     if (pick == kExit) break;
     if (pick >= kPickPush) {
-      const SmemSlot e = s_ev;
+      const SmemSlot& e = s_ev;      // stable until the trailing barrier
       if (kVar != 1)
         stg.push(reinterpret_cast<const float4*>(e.src), reinterpret_cast<float4*>(e.dst), e.cnt, e.tag16,
                  blockIdx.x, gridDim.x, p.n4);
       __syncthreads();
       if (threadIdx.x == 0) push_seq[pick - kPickPush] = s_seq;
     } else if (pick >= 0) {
-      const SmemSlot e = s_ev;
-      if (e.pair) {
-        if (e.grad) slice<kVar, true, kGradQuadInline>(p, e, stg);
-        else slice<kVar, true, kGradNone>(p, e, stg);
+      const SmemSlot& e = s_ev;      // stable until the trailing barrier
+      if (e.kind == kKindPull) {
+        if (kVar != 1)
+          stg.pull(reinterpret_cast<const float4*>(e.xi), reinterpret_cast<const float4*>(e.g),
+                   reinterpret_cast<float4*>(e.gout), blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q,
+                   quad_event_key_h(p.q.noise_key, e.key));
+      } else if (kVar != 1 && e.g) {        // App. A flush of the buffered gradient (staged variants)
+        if (e.pair) slice<kVar, true, kGradExternal, true>(p, e, stg);
+        else slice<kVar, false, kGradExternal>(p, e, stg);
+      } else if (e.pair) {
+        if (e.grad) {
+          if (kVar != 1 && e.ff) slice<kVar, true, kGradQuadInline, true>(p, e, stg);
+          else slice<kVar, true, kGradQuadInline>(p, e, stg);
+        } else {
+          slice<kVar, true, kGradNone>(p, e, stg);
+        }
       } else if (e.grad) {
         slice<kVar, false, kGradQuadInline>(p, e, stg);
       }

@@ -31,7 +31,13 @@ struct Slot {                      // per local worker, in local device memory
   unsigned int tag16;              // push-counter tag of this event (cross, two-sided)
   float* land;                     // local landing row the partner pushes x_j into (cross)
   unsigned int* pcnt;              // per-CTA push counters of that landing row (cross)
+  // App. A (wait_free) and flush-first replay events
+  int kind;                        // 0 = event (ticketed), 1 = pull (computation thread, no ticket)
+  unsigned long long key;          // random-draw key of an inline / pulled gradient
+  float* g;                        // event: buffered gradient to flush; pull: g_p to compensate with
+  float* gout;                     // pull: gradient row written
 };
+constexpr int kKindEvent = 0, kKindPull = 1;
 
 struct ReplayEv {                  // one schedule event owned by this rank (i local)
   long long k;
@@ -66,6 +72,7 @@ struct EngineParams {
   int variant;                     // 0 = bulk-copy (TMA) staged slices, 1 = register slices
   int two_sided;                   // cross-GPU events via partner push (write-only NVLink)
   unsigned int* served;            // [n_local][kMaxGrid] last push request served per CTA (persistent)
+  int wait_free;                   // free-running loop: 0 Alg. 1, 1 App. A, 2 App. A + compensation
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);
@@ -83,6 +90,8 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
                                int M, uint2 batch_key, unsigned long long k, const float* xhat,
                                float* g, long long d, cudaStream_t s);
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s);
+// App. A local-update compensation of a pulled model: out = fl(x - fl(gamma gp))
+cudaError_t launch_comp_row(const float* x, const float* gp, float gamma, float* out, long long n4, cudaStream_t s);
 cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,
                                  double* sum, cudaStream_t s);
 cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out,

@@ -36,14 +36,14 @@ int stream_grid(long long n4) {
 
 // ----------------------------------------------------------- event pass ----
 // Each CTA takes a contiguous slice of the float4 range (DRAM-page friendly).
-template <bool kPair, int kGrad>
+template <bool kPair, int kGrad, bool kFF = false>
 __global__ void __launch_bounds__(kThreads, 2) k_event(float* xi, float* xj, const float* g,
                                                     const float* xhat, long long d, long long n4,
                                                     float gamma, QuadParams q, uint32_t kk) {
   const long long per = (n4 + gridDim.x - 1) / gridDim.x;
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = lo + per < n4 ? lo + per : n4;
-  event_range<kPair, kGrad, kUnroll>(reinterpret_cast<float4*>(xi), reinterpret_cast<float4*>(xj),
+  event_range<kPair, kGrad, kUnroll, kFF>(reinterpret_cast<float4*>(xi), reinterpret_cast<float4*>(xj),
                                      reinterpret_cast<const float4*>(g),
                                      reinterpret_cast<const float4*>(xhat), lo, hi,
                                      threadIdx.x, blockDim.x, d, gamma, q, kk);
@@ -119,6 +119,17 @@ __global__ void k_copy(float4* __restrict__ dst, const float4* __restrict__ src,
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x)
     st_cg4(dst + i, ld_cg4(src + i));
+}
+
+// App. A compensation (footnote at P:1265-1268): out = fl(x - fl(gamma gp))
+__global__ void k_comp_row(const float4* __restrict__ x, const float4* __restrict__ gp, float gamma,
+                           float4* __restrict__ out, long long n4) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
+       i += (long long)gridDim.x * blockDim.x) {
+    const float4 a = ld_cg4(x + i), g = ld_cg4(gp + i);
+    st_cg4(out + i, make_float4(__fsub_rn(a.x, __fmul_rn(gamma, g.x)), __fsub_rn(a.y, __fmul_rn(gamma, g.y)),
+                                __fsub_rn(a.z, __fmul_rn(gamma, g.z)), __fsub_rn(a.w, __fmul_rn(gamma, g.w))));
+  }
 }
 
 // ------------------------------------------------------ consensus output ---
@@ -288,14 +299,30 @@ cudaError_t ev(float* xi, float* xj, const float* g, const float* xh, long long 
   return cudaGetLastError();
 }
 
+template <int G>
+cudaError_t ev_ff(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
+                  float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s) {
+  k_event<true, G, true><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk);
+  return cudaGetLastError();
+}
+
 }  // namespace
 
+// k: random-draw key of the gradient (the event's k, or read_key for App. A events)
 cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat, long long d,
                          long long n4, float gamma, const QuadParams& q, unsigned long long k,
                          int grad_mode, cudaStream_t s) {
   const uint32_t kk = quad_event_key_h(q.noise_key, k);
   const bool pair = xj != nullptr;
-  switch (grad_mode) {
+  if ((grad_mode & kModeFlushFirst) && pair) {     // App. A order; a local flush is Alg. 1's local step
+    switch (grad_mode & 0xf) {
+      case kGradNone: return ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      case kGradExternal: return ev_ff<kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      case kGradQuadInline: return ev_ff<kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  switch (grad_mode & 0xf) {
     case kGradNone:
       return pair ? ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
                   : cudaSuccess;
@@ -329,6 +356,13 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s) {
   k_copy<<<stream_grid(n4), kThreads, 0, s>>>(reinterpret_cast<float4*>(dst),
                                               reinterpret_cast<const float4*>(src), n4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_comp_row(const float* x, const float* gp, float gamma, float* out, long long n4, cudaStream_t s) {
+  k_comp_row<<<stream_grid(n4), kThreads, 0, s>>>(reinterpret_cast<const float4*>(x),
+                                                  reinterpret_cast<const float4*>(gp), gamma,
+                                                  reinterpret_cast<float4*>(out), n4);
   return cudaGetLastError();
 }
 

@@ -83,6 +83,7 @@ struct adpsgd_ctx {
   QuadParams q{};
   long long compute_ns = 0;
   int engine_cps = 0, engine_threads = 512, engine_variant = 0;
+  int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
   long long log_cap = 1 << 20;
   std::vector<int32_t> edges;
   std::vector<int8_t> role;
@@ -124,6 +125,8 @@ struct adpsgd_ctx {
   float* gslots = nullptr;
   int gslot_n = 0;
   float* gstep = nullptr;            // per-local-worker gradient buffers (adpsgd_step)
+  float* wf_g = nullptr;             // App. A: [n_local][2][d_pad] gradient rows (wait_free)
+  float* comp_row = nullptr;         // host replay: compensated pulled model (COMPENSATE events)
   float* mlp_scratch = nullptr;
   size_t mlp_scratch_n = 0;
   std::vector<MlpWork> mlp_work;     // one per replay stream lane
@@ -247,6 +250,7 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
     x.nb_cnt = c->nb_off[w + 1] - c->nb_off[w];
     x.straggle = c->straggle[w];
     x.local = r == c->rank ? c->worker_local[w] : -1;
+    x.gb = (r == c->rank && c->wf_g) ? c->wf_g + l * 2 * c->d_pad : nullptr;
   }
   CU(cudaMemcpy(c->d_workers, wd.data(), sizeof(WorkerDesc) * c->n, cudaMemcpyHostToDevice));
   CU(cudaDeviceSynchronize());   // pageable H2D may still be in flight; kernels use non-blocking streams
@@ -400,16 +404,43 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   unsigned long long k0;
   ST(host_ticket(c, &k0));
   const int slots = c->T + 1;
+  // App. A compensation (reading R20): comp_src[e] = worker i's previous
+  // gradient event when it was still buffered at e's read point.  Its gradient
+  // is in slot comp_src mod (T+1) at that point: it was computed at its own
+  // read point (<= e's, checked) and that slot is reused only by the read of
+  // event comp_src + T + 1, which comes later.
+  std::vector<int64_t> comp_src(K, -1);
+  bool any_comp = false;
+  {
+    std::vector<int64_t> last(c->n, -1);
+    for (int64_t e = 0; e < K; ++e) {
+      if (!has_model || (ev[e].flags & ADPSGD_EV_NO_GRAD)) continue;
+      const int i = ev[e].i;
+      const int64_t t = e - ev[e].tau;
+      if ((ev[e].flags & ADPSGD_EV_COMPENSATE) && last[i] >= t) {
+        if (last[i] - ev[last[i]].tau > t) {
+          char buf[160];
+          snprintf(buf, sizeof buf, "event %lld: compensated read precedes the previous gradient's read (App. A)",
+                   (long long)e);
+          return fail(ADPSGD_E_STALENESS, buf);
+        }
+        comp_src[e] = last[i];
+        any_comp = true;
+      }
+      last[i] = e;
+    }
+  }
   bool need_slots = false;
   std::vector<std::vector<int64_t>> reads(K);
   for (int64_t e = 0; e < K; ++e) {
     const bool grad = has_model && !(ev[e].flags & ADPSGD_EV_NO_GRAD);
     if (!grad) continue;
-    if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0) continue;   // fused inline
+    if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0 && !any_comp) continue;   // fused inline
     need_slots = true;
     reads[e - ev[e].tau].push_back(e);   // gradient at X_{e - tau}
   }
   if (need_slots) ST(ensure_gslots(c, slots));
+  if (any_comp && !c->comp_row) CU(cudaMalloc(&c->comp_row, sizeof(float) * c->d_pad));
   const bool sampled = c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG ||
                        c->model == ADPSGD_MODEL_MLP;
   if (sampled && bidx) {
@@ -429,7 +460,8 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   // streams: each op waits (cudaEvent) only for the last writer of the rows it
   // reads, the readers of the rows it writes, and its gradient slot.  The
   // result is bitwise the serial one.
-  const int ns = (c->model == ADPSGD_MODEL_MLP || c->d >= (1 << 16)) ? std::min(kPoolStreams, c->n) : 1;
+  const int ns =
+      (!any_comp && (c->model == ADPSGD_MODEL_MLP || c->d >= (1 << 16))) ? std::min(kPoolStreams, c->n) : 1;
   ST(ensure_pool(c, ns));
   if (c->model == ADPSGD_MODEL_MLP && need_slots) ST(ensure_mlp_scratch(c, ns));
   DagState dag(c->n, slots);
@@ -443,7 +475,16 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
       if (ns > 1) { ST(dag_wait(st, dag.w_evt[i])); ST(dag_wait(st, dag.g_evt[sl])); }
       float* slot = c->gslots + (long long)sl * c->d_pad;
       const int* idx = (sampled && bidx) ? c->d_batch + kp * c->M : nullptr;
-      ST(model_grad(c, c->row(i), slot, k0 + kp, idx, st, lane));
+      const unsigned long long key =
+          (ev[kp].flags & ADPSGD_EV_FLUSH_FIRST) ? read_key(k0 + kp - ev[kp].tau, i) : k0 + kp;
+      const float* src = c->row(i);
+      if (comp_src[kp] >= 0) {            // pulled while g_p was buffered: x - gamma g_p
+        CU(launch_comp_row(src, c->gslots + (long long)(comp_src[kp] % slots) * c->d_pad, c->gamma, c->comp_row,
+                           c->n4, st));
+        ++c->launches;
+        src = c->comp_row;
+      }
+      ST(model_grad(c, src, slot, key, idx, st, lane));
       if (ns > 1) {
         cudaEvent_t done;
         ST(dag_record(c, st, &done));
@@ -456,9 +497,14 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
     int mode = kGradNone;
     const float* g = nullptr;
     const int sl = (int)(e % slots);
+    unsigned long long key = k0 + e;
     if (grad) {
-      if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0) mode = kGradQuadInline;
+      if (c->model == ADPSGD_MODEL_QUADRATIC && ev[e].tau == 0 && !any_comp) mode = kGradQuadInline;
       else { mode = kGradExternal; g = c->gslots + (long long)sl * c->d_pad; }
+      if (ev[e].flags & ADPSGD_EV_FLUSH_FIRST) {
+        key = read_key(k0 + e, i);           // tau = 0 here when inline
+        mode |= kModeFlushFirst;
+      }
     }
     if (j >= 0 || mode != kGradNone) {
       cudaStream_t st = ns > 1 ? c->pool[i % ns] : s;
@@ -469,10 +515,10 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
           ST(dag_wait(st, dag.w_evt[j]));
           for (cudaEvent_t r : dag.r_evts[j]) ST(dag_wait(st, r));
         }
-        if (mode == kGradExternal) ST(dag_wait(st, dag.gready[sl]));
+        if ((mode & 0xf) == kGradExternal) ST(dag_wait(st, dag.gready[sl]));
       }
       CU(launch_event(c->row(i), j >= 0 ? c->row(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma,
-                      c->q, k0 + e, mode, st));
+                      c->q, key, mode, st));
       ++c->launches;
       if (ns > 1) {
         cudaEvent_t done;
@@ -480,7 +526,7 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
         dag.w_evt[i] = done;
         dag.r_evts[i].clear();
         if (j >= 0) { dag.w_evt[j] = done; dag.r_evts[j].clear(); }
-        if (mode == kGradExternal) dag.g_evt[sl] = done;
+        if ((mode & 0xf) == kGradExternal) dag.g_evt[sl] = done;
       }
     }
   }
@@ -527,6 +573,7 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.two_sided = (c->world > 1 && p.variant == 3 && c->land) ? 1 : 0;
   if (p.variant == 3) p.variant = 0;
   p.served = c->served;
+  p.wait_free = mode == 0 ? c->wait_free : 0;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
@@ -603,8 +650,11 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   if (c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_QUADRATIC)
     return fail(ADPSGD_E_UNSUPPORTED, "engine replay supports models NONE and QUADRATIC");
   ST(validate_events(c, ev, K, false));
-  for (int64_t e = 0; e < K; ++e)
+  for (int64_t e = 0; e < K; ++e) {
     if (ev[e].tau != 0) return fail(ADPSGD_E_UNSUPPORTED, "engine replay needs tau = 0 (use HOST)");
+    if ((ev[e].flags & ADPSGD_EV_FLUSH_FIRST) && c->engine_variant == 1)
+      return fail(ADPSGD_E_UNSUPPORTED, "FLUSH_FIRST events need a staged engine variant (0, 2, 3)");
+  }
   // k and the epochs are tracked identically on every rank (they only change
   // through collective calls whose effect is known: a replay advances k by K
   // and the epochs by the schedule, a run ends at exactly its target), so no
@@ -651,7 +701,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
-                  c->d_dp_wself};
+                  c->d_dp_wself, c->wf_g, c->comp_row};
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -690,6 +740,12 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   if (c->engine_variant < 0 || c->engine_variant > 3) return fail(ADPSGD_E_INVALID, "engine_variant");
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
+  c->wait_free = cfg->wait_free;
+  if (c->wait_free < 0 || c->wait_free > 2) return fail(ADPSGD_E_INVALID, "wait_free must be 0, 1 or 2");
+  if (c->wait_free && c->model != ADPSGD_MODEL_QUADRATIC)
+    return fail(ADPSGD_E_UNSUPPORTED, "the wait-free (App. A) engine loop supports the QUADRATIC model");
+  if (c->wait_free && (c->engine_variant == 1 || c->engine_variant == 3))
+    return fail(ADPSGD_E_UNSUPPORTED, "the wait-free engine loop needs engine_variant 0 or 2");
   ST(check_graph(c.get(), g));
   // placement
   ST(compute_placement(c->n, c->world, cfg->placement, cfg->worker_rank, c->worker_rank, c->worker_local));
@@ -776,6 +832,10 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     CU(cudaMemcpy(c->d_local_ids, c->local_ids.data(), sizeof(int) * c->n_local, cudaMemcpyHostToDevice));
   CU(cudaMalloc(&c->d_slots, sizeof(Slot) * std::max(1, c->n_local)));
   CU(cudaMemset(c->d_slots, 0, sizeof(Slot) * std::max(1, c->n_local)));
+  if (c->wait_free && c->n_local) {          // App. A gradient rows: buffer + computing gradient
+    CU(cudaMalloc(&c->wf_g, sizeof(float) * 2 * c->d_pad * c->n_local));
+    CU(cudaMemset(c->wf_g, 0, sizeof(float) * 2 * c->d_pad * c->n_local));
+  }
   CU(cudaMalloc(&c->sum64, sizeof(double) * c->d_pad));
   CU(cudaMalloc(&c->mk_acc, sizeof(double)));
   c->peer_models.assign(c->world, nullptr);

@@ -86,6 +86,37 @@ def schedule_iid(n, edges, K, T=0, seed=0, M=0, S=0, no_grad=False, tau=None,
     return ev, bidx
 
 
+EV_FLUSH_FIRST, EV_COMPENSATE = 2, 4
+
+
+def schedule_appa(n, edges, role, K, T, seed=0, compensate=True, p_gossip=0.3):
+    """A valid App. A (wait-free runtime) schedule, reading R20: actives either
+    average with no gradient (probability p_gossip) or flush a buffered
+    gradient and average; passives flush with no partner.  A gradient's read
+    point t (tau = k - t) is drawn so that each worker reads in order and has
+    at most one gradient in the buffer when it pulls:
+    t in [max(k - T, previous read, flush before the previous + 1), k]."""
+    rng = np.random.default_rng(seed)
+    nb = neighbours(n, edges)
+    last_k = [-1] * n
+    last_r = [0] * n
+    prev_k = [-1] * n
+    flags = EV_FLUSH_FIRST | (EV_COMPENSATE if compensate else 0)
+    ev = np.zeros((K, 4), np.int32)
+    for k in range(K):
+        i = int(rng.integers(n))
+        active = role[i] == 0 and len(nb[i]) > 0
+        j = nb[i][int(rng.integers(len(nb[i])))] if active else -1
+        if active and rng.random() < p_gossip:
+            ev[k] = (i, j, 0, EV_NO_GRAD)
+            continue
+        lo = max(0, k - T, last_r[i], prev_k[i] + 1)
+        t = int(rng.integers(lo, k + 1))
+        ev[k] = (i, j, k - t, flags)
+        prev_k[i], last_k[i], last_r[i] = last_k[i], k, t
+    return ev
+
+
 def x0_uniform(n: int, d: int, seed: int = 7) -> np.ndarray:
     """Per-worker initial models, values 2u-1 with u = m * 2^-24 exact in fp32
     (pure-gossip tests only, reading c7)."""

@@ -176,6 +176,92 @@ def test_n1_lsq_equals_serial_sgd():
     np.testing.assert_allclose(X[0], x, rtol=1e-5, atol=1e-6)
 
 
+FF, COMP = O.EV_FLUSH_FIRST, O.EV_COMPENSATE
+
+
+def test_appa_flush_first_hand_example():
+    """App. A, Alg. 2: flush g, then average -- both endpoints get
+    (x_i - gamma g + x_j)/2.  Alg. 1: average, then x_i -= gamma g.
+    f = x^2/2 (g = x), gamma = 0.5, x = (1, 3): App. A -> (1.75, 1.75);
+    Alg. 1 -> (1.5, 2).  All values are exact in fp32."""
+    p = quad([1.0], [0.0], gamma=0.5)
+    e = np.array([[0, 1]], np.int32)
+    X, _ = O.replay(p, [[1.0], [3.0]], e, [0, 1], [[0, 1, 0, FF]])
+    assert X[:, 0].tolist() == [1.75, 1.75]
+    X, _ = O.replay(p, [[1.0], [3.0]], e, [0, 1], [[0, 1, 0, 0]])
+    assert X[:, 0].tolist() == [1.5, 2.0]
+    # the passive flushes its own gradient with no partner (Alg. 3, P:1305-1306)
+    X, _ = O.replay(p, [[1.0], [3.0]], e, [0, 1], [[1, -1, 0, FF]])
+    assert X[:, 0].tolist() == [1.0, 1.5]
+
+
+def test_appa_compensation_reduces_to_gd_and_delayed_gd():
+    """Footnote at P:1265-1268: the computation thread pulls x while g is still
+    in the buffer and applies x -= gamma g locally.  n = 1, f = x^2/2, gamma =
+    0.5, x0 = 1, every read one event stale (tau = 1): with compensation the
+    pulled model equals the current one, so x_k = 0.5^k (plain GD, S:291);
+    without it, delayed GD x_{k+1} = x_k - 0.5 x_{k-1} (exact rationals)."""
+    from fractions import Fraction
+    p = quad([1.0], [0.0], gamma=0.5)
+    K = 40
+    none = np.zeros((0, 2), np.int32)
+    ev = [[0, -1, 0, FF | COMP]] + [[0, -1, 1, FF | COMP]] * (K - 1)
+    X, _ = O.replay(p, [[1.0]], none, None, ev, T=1)
+    assert X[0, 0] == np.float32(2.0 ** -K)
+    ev = [[0, -1, 0, FF]] + [[0, -1, 1, FF]] * (K - 1)
+    X, _ = O.replay(p, [[1.0]], none, None, ev, T=1)
+    xs = [Fraction(1), Fraction(1, 2)]
+    for _ in range(K - 1):
+        xs.append(xs[-1] - Fraction(1, 2) * xs[-2])
+    assert X[0, 0] == np.float32(float(xs[-1]))
+
+
+def test_appa_compensation_causality_and_lsq_serial_equivalence():
+    """(a) A worker computes one gradient at a time (Alg. 1 blocks until g = 0):
+    a compensated read older than the previous gradient's read is rejected.
+    (b) n = 1 least squares, every read one event stale with compensation ==
+    the serial minibatch-SGD loop, numpy fp64 BLAS, to fp32 rounding."""
+    p = quad([1.0], [0.0], gamma=0.5)
+    none = np.zeros((0, 2), np.int32)
+    with pytest.raises(O.OracleError) as ex:
+        O.replay(p, [[1.0]], none, None, [[0, -1, 0, 0], [0, -1, 0, COMP], [0, -1, 2, FF | COMP]], T=2)
+    assert ex.value.code == 5
+    A, b = synth.lsq_data(S=256, d=64, seed=5)
+    ev, bi = synth.schedule_iid(1, none, K=200, M=8, S=256, seed=3)
+    ev[:, 3] = FF | COMP
+    ev[1:, 2] = 1
+    pl = O.OracleProblem(O.MODEL_LSQ, M=8, gamma=0.05, A=A, b=b)
+    X, _ = O.replay(pl, np.zeros((1, 64), np.float32), none, None, ev, bi, T=1)
+    x = np.zeros(64, np.float32)
+    for k in range(200):
+        Ab = A[bi[k]].astype(np.float64)
+        g = (Ab.T @ (Ab @ x.astype(np.float64) - b[bi[k]])).astype(np.float32)
+        x = (x - np.float32(0.05) * g).astype(np.float32)
+    np.testing.assert_allclose(X[0], x, rtol=1e-5, atol=1e-6)
+
+
+def test_appa_pair_endpoints_equal_and_sum_moves_by_gradient():
+    """Invariants of a flush-first pair event (Alg. 2/3): both endpoints hold
+    the same bits afterwards, and the pair sum (hence sum_i x_i) moves by
+    -gamma g (S:297 analogue, fp64-tracked, tolerance of reading c10)."""
+    n, d = 8, 512
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(2)
+    p = O.OracleProblem(O.MODEL_QUADRATIC, M=8, gamma=0.01, data_key=dk, noise_key=nk, noise_s=0.3)
+    X = synth.x0_uniform(n, d, seed=6)
+    ev, _ = synth.schedule_iid(n, e, K=40, seed=7, local_prob=0.0)
+    ev[:, 3] = FF
+    for k in range(40):
+        i, j = int(ev[k, 0]), int(ev[k, 1])
+        Xn, _ = O.replay(p, X, e, r, ev[k:k + 1], k0=k)
+        assert np.array_equal(Xn[i].view(np.uint32), Xn[j].view(np.uint32))
+        g = O.gradient(p, X[i], k=O.read_key(k, i))        # tau = 0: read at X_k
+        pair0 = X[i].astype(np.float64) + X[j].astype(np.float64)
+        pair1 = 2.0 * Xn[i].astype(np.float64)
+        np.testing.assert_allclose(pair1 - pair0, -0.01 * g.astype(np.float64), atol=4e-7)
+        X = Xn
+
+
 def test_noiseless_quadratic_converges_to_closed_form_minimiser():
     """Shared noiseless quadratic f = 1/2 sum h (x - x*)^2 with gamma*M*h_max < 1:
     every worker converges to the closed-form minimiser x* (a fixed point of
