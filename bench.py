@@ -232,14 +232,14 @@ def main():
     strag = synth.stragglers(n, slow_worker=0, slow=a.straggler)
     cns = int(a.compute_us * 1000)
 
-    def make_ctx(st, nn=None, ee=None, rr=None):
+    def make_ctx(st, nn=None, ee=None, rr=None, wait_free=0):
         nn = n if nn is None else nn
         ee = e if ee is None else ee
         rr = r if rr is None else rr
         return P.Context(ee, nn, d, role=rr, rank=rank, world_size=world, device=local, placement=a.placement,
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                          quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
-                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm)
+                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free)
 
     stream = torch.cuda.Stream()
     out = torch.empty(d, dtype=torch.float32, device="cuda")
@@ -448,6 +448,35 @@ def main():
             barrier()
             t4[f"x{slow:g}"] = row
         extras["table4_updates_per_s"] = t4
+        # App. A wait-free runtime (reading R20) on the bench workload:
+        # gradients computed into a buffer, flushed before averaging; actives
+        # average continuously in between (no-gradient events)
+        wf = {}
+        for mode in (1, 2):
+            cw = make_ctx(strag, wait_free=mode)
+            cw.run(U, stream)
+            torch.cuda.synchronize()
+            cw.sync()
+            barrier()
+            s0, u0 = cw.stats(), sum(cw.update_counts().values())
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta.record(stream)
+            for _ in range(3):
+                cw.run(U, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            cw.sync()
+            barrier()
+            secw = maxr(ta.elapsed_time(tb)) / 1e3
+            s1, u1 = cw.stats(), sum(cw.update_counts().values())
+            wf["compensated" if mode == 2 else "plain"] = {
+                "updates_per_s": sumr(u1 - u0) / secw,
+                "gossip_steps_per_s": sumr(s1["local_pair_events"] - s0["local_pair_events"]) / secw,
+                "events_per_s": sumr(s1["local_events"] - s0["local_events"]) / secw}
+            cw.destroy()
+            barrier()
+        wf["workload"] = "config 4 workload and straggler, adpsgd_run with wait_free = 1 / 2"
+        extras["wait_free_appA"] = wf
         if world > 1:
             # NVLink stress: pure gossip, interleave placement -> every pair event crosses GPUs
             cn = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,

@@ -9,7 +9,9 @@ Checks (DESIGN.md 'Multi-GPU'):
   3. free-running engine, quadratic: the device event log replayed through the
      oracle reproduces every rank's models bitwise;
   4. consensus mean (NCCL fp64 all-reduce) within 1 ulp;
-  5. AllReduce-SGD baseline (NCCL fp32) within 1e-5 relative.
+  5. AllReduce-SGD baseline (NCCL fp32) within 1e-5 relative;
+  6. D-PSGD baseline (NCCL halo exchange) bitwise;
+  7. App. A wait-free engine loop across GPUs: log replay bitwise.
 """
 import math
 import os
@@ -144,6 +146,32 @@ def main():
             x = O.allreduce_update(x, G, 0.01)
         if not np.allclose(xa, x, rtol=1e-5, atol=1e-6):
             fails.append(f"allreduce baseline max err {np.abs(xa - x).max()}")
+    ctx.destroy()
+    dist.barrier()
+
+    # 7. App. A wait-free engine loop (reading R20), interleave placement: pulls,
+    #    buffered-gradient flushes and continuous averages across NVLink; the log
+    #    (tau = k - t_read, FLUSH_FIRST | COMPENSATE) replays bitwise
+    d = (1 << 14) + 20
+    X0w = synth.x0_uniform(n, d, seed=25)
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+                    model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
+                    x0_per_worker=X0w, straggler=synth.stragglers(n, slow=3.0), compute_ns=30_000, seed=11,
+                    wait_free=2)
+    ctx.run(2000)
+    ctx.sync()
+    dist.barrier()
+    Xw = gather_models(ctx)
+    if rank == 0:
+        log = ctx.read_log(0)
+        evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+        grad = (evs[:, 3] & 1) == 0
+        if len(log) != 2000 or grad.sum() == 0 or not (evs[grad, 3] & 4).any():
+            fails.append(f"wait-free log: {len(log)} entries, {int(grad.sum())} flushes")
+        else:
+            Xwo, _ = O.replay(prob_q, X0w, e, r, evs, T=int(evs[:, 2].max()))
+            if not np.array_equal(Xw.view(np.uint32), Xwo.view(np.uint32)):
+                fails.append("wait-free multi-GPU log replay not bit-exact")
     ctx.destroy()
     dist.barrier()
     if rank == 0:
