@@ -127,6 +127,14 @@ typedef struct {
                               /* 2 = as 1 plus local-update compensation (COMPENSATE).        */
                               /* QUADRATIC model only; one-sided NVLink access.               */
   int32_t reserved0;
+  /* --- heterogeneous communication (Fig. loss-link), reading R21 --- */
+  const float* link_slow;     /* n factors L_w >= 1: worker w's network link is L_w x slower;  */
+                              /* NULL = all 1.  Emulated: a model transfer over a link of     */
+                              /* factor L takes L * link_ns, so a pair event holds both        */
+                              /* workers (and the passive's lock) (max(L_i, L_j) - 1) * link_ns */
+                              /* after its pass; the synchronous baselines wait for their     */
+                              /* slowest link every round (adpsgd_allreduce_sgd, adpsgd_dpsgd)*/
+  int64_t link_ns;            /* nominal time of one model transfer over a 1x link            */
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its

@@ -78,6 +78,7 @@ struct WorkerDesc {
   float straggle;                  // slowdown factor s_w >= 1
   int local;                       // index among this rank's workers, -1 if remote
   float* gb;                       // App. A: two gradient rows (2 * d_pad), local workers only
+  float link;                      // link slowdown L_w >= 1 (emulated slow network, R21)
 };
 
 // --------------------------------------------------------------- hashing ----

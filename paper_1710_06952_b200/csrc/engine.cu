@@ -197,16 +197,30 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
 __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned int tag, unsigned long long now) {
   Slot* sl = p.slots + s;
   const unsigned int seq = tag >> 2;
+  bool done = false;
   if (p.mode == 0) {
-    // stop early if the system-wide budget is exhausted (straggler in compute)
-    if (ld_relaxed_sys64(&p.gctl0->ticket) >= p.target) {
-      if (atomicCAS(&sl->tag, tag, tag_of(seq, kStateClaimed)) != tag) return false;
+    // stop early if the system-wide budget is exhausted (straggler in compute),
+    // once a slow-link transfer still in progress has ended
+    done = ld_relaxed_sys64(&p.gctl0->ticket) >= p.target;
+    if (done) {
+      if (*(unsigned int* volatile*)&sl->held_lock && now < *(volatile unsigned long long*)&sl->unlock_at)
+        return false;
+    } else if (now < *(volatile unsigned long long*)&sl->ready_ns) {
+      return false;
+    }
+  }
+  if (atomicCAS(&sl->tag, tag, tag_of(seq, kStateClaimed)) != tag) return false;   // claim
+  if (p.mode == 0) {
+    if (sl->held_lock) {                    // release the partner held by the slow transfer (R21)
+      __threadfence_system();
+      atomicExch_system(sl->held_lock, 0u);
+      sl->held_lock = nullptr;
+    }
+    if (done) {
       st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
       return true;
     }
-    if (now < *(volatile unsigned long long*)&sl->ready_ns) return false;
   }
-  if (atomicCAS(&sl->tag, tag, tag_of(seq, kStateClaimed)) != tag) return false;   // claim
 
   const int w = p.local_ids[s];
   const WorkerDesc dw = p.workers[w];
@@ -326,11 +340,21 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     if (j >= 0) atomicAdd_system(&sl->ctl_j->epoch, 1u);
     atomicAdd_system(&p.gctl0->ticket, 1ull);
   } else {
-    atomicExch_system(sl->lock, 0u);
+    // slow link (R21): the transfer over the slower endpoint's link takes L x
+    // link_ns; both workers stay busy and the passive stays locked until then
+    float L = 1.0f;
+    if (j >= 0) L = fmaxf(p.workers[i].link, p.workers[j].link);
+    const unsigned long long hold = L > 1.0f ? (unsigned long long)((double)(L - 1.0f) * (double)p.link_ns) : 0ull;
+    if (hold) {
+      sl->held_lock = sl->lock;
+      sl->unlock_at = now + hold;
+    } else {
+      atomicExch_system(sl->lock, 0u);
+    }
     const float sw = p.workers[i].straggle;
     // Alg. 1 loop: the next gradient is computed before the next event; in the
     // App. A runtime the communication thread never waits for it
-    sl->ready_ns = p.wait_free ? 0ull : now + (unsigned long long)((double)sw * (double)p.compute_ns);
+    sl->ready_ns = now + hold + (p.wait_free ? 0ull : (unsigned long long)((double)sw * (double)p.compute_ns));
   }
   atomicAdd_system(&p.gctl0->committed, 1ull);
   const unsigned int seq = sl->tag >> 2;

@@ -36,6 +36,9 @@ struct Slot {                      // per local worker, in local device memory
   unsigned long long key;          // random-draw key of an inline / pulled gradient
   float* g;                        // event: buffered gradient to flush; pull: g_p to compensate with
   float* gout;                     // pull: gradient row written
+  // slow-link emulation (R21): the passive's lock is released at unlock_at
+  unsigned int* held_lock;
+  unsigned long long unlock_at;
 };
 constexpr int kKindEvent = 0, kKindPull = 1;
 
@@ -73,6 +76,7 @@ struct EngineParams {
   int two_sided;                   // cross-GPU events via partner push (write-only NVLink)
   unsigned int* served;            // [n_local][kMaxGrid] last push request served per CTA (persistent)
   int wait_free;                   // free-running loop: 0 Alg. 1, 1 App. A, 2 App. A + compensation
+  long long link_ns;               // nominal model-transfer time of a 1x link (R21)
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);

@@ -84,6 +84,9 @@ struct adpsgd_ctx {
   long long compute_ns = 0;
   int engine_cps = 0, engine_threads = 512, engine_variant = 0;
   int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
+  std::vector<float> link;           // link slowdown per worker (reading R21)
+  long long link_ns = 0;
+  float link_max() const { return link.empty() ? 1.0f : *std::max_element(link.begin(), link.end()); }
   long long log_cap = 1 << 20;
   std::vector<int32_t> edges;
   std::vector<int8_t> role;
@@ -251,6 +254,7 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
     x.straggle = c->straggle[w];
     x.local = r == c->rank ? c->worker_local[w] : -1;
     x.gb = (r == c->rank && c->wf_g) ? c->wf_g + l * 2 * c->d_pad : nullptr;
+    x.link = c->link[w];
   }
   CU(cudaMemcpy(c->d_workers, wd.data(), sizeof(WorkerDesc) * c->n, cudaMemcpyHostToDevice));
   CU(cudaDeviceSynchronize());   // pageable H2D may still be in flight; kernels use non-blocking streams
@@ -574,6 +578,7 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   if (p.variant == 3) p.variant = 0;
   p.served = c->served;
   p.wait_free = mode == 0 ? c->wait_free : 0;
+  p.link_ns = c->link_ns;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
@@ -758,6 +763,14 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     for (int w = 0; w < c->n; ++w) {
       if (!(cfg->straggler[w] >= 1.0f)) return fail(ADPSGD_E_INVALID, "straggler factors must be >= 1");
       c->straggle[w] = cfg->straggler[w];
+    }
+  c->link.assign(c->n, 1.0f);
+  c->link_ns = cfg->link_ns;
+  if (c->link_ns < 0) return fail(ADPSGD_E_INVALID, "link_ns < 0");
+  if (cfg->link_slow)
+    for (int w = 0; w < c->n; ++w) {
+      if (!(cfg->link_slow[w] >= 1.0f)) return fail(ADPSGD_E_INVALID, "link_slow factors must be >= 1");
+      c->link[w] = cfg->link_slow[w];
     }
   // model data
   if (c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG || c->model == ADPSGD_MODEL_MLP) {
@@ -1145,7 +1158,10 @@ adpsgd_status adpsgd_allreduce_sgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_strea
     cudaStream_t st = c->use(s);
     float smax = 1.0f;
     for (int w : c->local_ids) smax = std::max(smax, c->straggle[w]);
-    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns);
+    // slow link (R21): a ring all-reduce moves ~2 models over every link per
+    // round, so the round waits 2 (L_max - 1) link_ns for its slowest link
+    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns) +
+                                     (unsigned long long)(2.0 * ((double)c->link_max() - 1.0) * (double)c->link_ns);
     for (int64_t r = 0; r < n_rounds; ++r) {
       if (delay) { CU(launch_delay(delay, st)); ++c->launches; }
       CU(launch_ar_grad_sum(c->xr, c->gsum, c->d, c->n4, c->q, c->ar_k, c->n_local, c->d_local_ids, st));
@@ -1253,7 +1269,10 @@ adpsgd_status adpsgd_dpsgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_stream s) {
     cudaStream_t st = c->use(s);
     float smax = 1.0f;
     for (int w : c->local_ids) smax = std::max(smax, c->straggle[w]);
-    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns);
+    // slow link (R21): every worker exchanges one model with each neighbour per
+    // round (in parallel, full duplex), so the round waits (L_max - 1) link_ns
+    const unsigned long long delay = (unsigned long long)((double)smax * (double)c->compute_ns) +
+                                     (unsigned long long)(((double)c->link_max() - 1.0) * (double)c->link_ns);
     const int model = c->model == ADPSGD_MODEL_QUADRATIC ? 1 : 0;
     for (int64_t r = 0; r < n_rounds; ++r) {
       if (delay) { CU(launch_delay(delay, st)); ++c->launches; }     // the round waits for its slowest worker

@@ -408,3 +408,31 @@ def test_skip_ring_free_running_log_replay(P):
     Xo, _ = O.replay(prob, X0, e, r, log_events(log))
     assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
     ctx.destroy()
+
+
+def test_slow_link_locality_and_log_replay(P):
+    """Heterogeneous communication (reading R21): worker 1's link
+    is 10x slower.  Only the averages touching it wait; actives away from it
+    keep their pace; the event log still replays bitwise through the oracle."""
+    n, d, U = 8, (1 << 16) + 12, 3000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(17)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    X0 = synth.x0_uniform(n, d, seed=18)
+    link = np.ones(n, np.float32)
+    link[1] = 10.0
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s, compute_ns=20_000, link_slow=link, link_ns=100_000,
+                    seed=3)
+    ctx.run(U)
+    ctx.sync()
+    log = ctx.read_log(0)
+    ev = log_events(log)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, X0, e, r, ev)
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    served = {w: int((ev[:, 1] == w).sum()) for w in range(1, n, 2)}
+    assert served[1] < 0.5 * np.mean([served[w] for w in (3, 5, 7)])
+    cnt = ctx.update_counts()
+    assert min(cnt[4], cnt[6]) > max(cnt[0], cnt[2])            # actives not adjacent to worker 1
+    ctx.destroy()
