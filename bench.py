@@ -410,12 +410,8 @@ def main():
             "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
             "allreduce_updates_per_s": R5 * n5 / sec5ar,
             "adpsgd_vs_allreduce_updates_ratio": up5 / (R5 * n5 / sec5ar)}
-        # Table 4's shape (P:1149-1162): one worker slowed 1x / 2x / 10x / 100x; updates/s of
-        # AD-PSGD vs the two synchronous baselines (same emulated compute t_c per gradient)
-        t4 = {}
-        for slow in (1.0, 2.0, 10.0, 100.0):
-            stv = synth.stragglers(n, slow_worker=0, slow=slow)
-            c4 = make_ctx(stv)
+        def three_way(c4, Rb):
+            """updates/s of AD-PSGD (free-running), AllReduce-SGD and D-PSGD on one context"""
             c4.run(U, stream)
             torch.cuda.synchronize()
             c4.sync()
@@ -431,7 +427,6 @@ def main():
             barrier()
             sec = maxr(ta.elapsed_time(tb)) / 1e3
             row = {"adpsgd": sumr(c4.stats()["local_events"] - s0["local_events"]) / sec}
-            Rb = 4 if slow < 50 else 2
             for kind in ("allreduce", "dpsgd"):
                 run = c4.allreduce_sgd if kind == "allreduce" else c4.dpsgd
                 (c4.allreduce_reset if kind == "allreduce" else c4.dpsgd_reset)()
@@ -446,8 +441,30 @@ def main():
                 barrier()
             c4.destroy()
             barrier()
-            t4[f"x{slow:g}"] = row
+            return row
+
+        # Table 4's shape (P:1149-1162): one worker slowed 1x / 2x / 10x / 100x; updates/s of
+        # AD-PSGD vs the two synchronous baselines (same emulated compute t_c per gradient)
+        t4 = {}
+        for slow in (1.0, 2.0, 10.0, 100.0):
+            t4[f"x{slow:g}"] = three_way(make_ctx(synth.stragglers(n, slow_worker=0, slow=slow)),
+                                         4 if slow < 50 else 2)
         extras["table4_updates_per_s"] = t4
+        # heterogeneous communication (Fig. loss-link; reading R21): worker 1's
+        # link 10x slower, nominal model transfer 4d / 900 GB/s; no compute straggler
+        link_ns = int(4 * d / 900e9 * 1e9)
+        lk = {}
+        for L in (1.0, 10.0):
+            lv = np.ones(n, np.float32)
+            lv[1 % n] = L
+            cl = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=a.placement,
+                           model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
+                           quad_noise_s=s, straggler=synth.stragglers(n, slow_worker=None), compute_ns=cns,
+                           seed=1234, log_capacity=1 << 16, engine_variant=a.engine_variant,
+                           engine_ctas_per_sm=a.ctas_per_sm, link_slow=lv, link_ns=link_ns)
+            lk[f"link_x{L:g}"] = three_way(cl, 4)
+        lk["workload"] = f"config 4, no compute straggler, worker 1 link slowed, link_ns = {link_ns}"
+        extras["slow_link_updates_per_s"] = lk
         # App. A wait-free runtime (reading R20) on the bench workload:
         # gradients computed into a buffer, flushed before averaging; actives
         # average continuously in between (no-gradient events)
