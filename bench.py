@@ -50,6 +50,7 @@ def parse():
     ap.add_argument("--engine-variant", type=int, default=0, help="0 TMA-staged, 1 register slices")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--topology", default="ring", choices=["ring", "skip"])
+    ap.add_argument("--no-fuse", action="store_true", help="never fuse a due passive step into a pair pass")
     return ap.parse_args()
 
 
@@ -239,7 +240,8 @@ def main():
         return P.Context(ee, nn, d, role=rr, rank=rank, world_size=world, device=local, placement=a.placement,
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                          quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
-                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free)
+                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free,
+                         engine_fuse=not a.no_fuse)
 
     stream = torch.cuda.Stream()
     out = torch.empty(d, dtype=torch.float32, device="cuda")

@@ -135,6 +135,14 @@ typedef struct {
                               /* after its pass; the synchronous baselines wait for their     */
                               /* slowest link every round (adpsgd_allreduce_sgd, adpsgd_dpsgd)*/
   int64_t link_ns;            /* nominal time of one model transfer over a 1x link            */
+  int32_t engine_no_fuse;     /* 0 (default): when an active holds a passive's lock and the   */
+                              /* passive's own local step is due, run both events (tickets    */
+                              /* k, k+1) in one pass -- same result and log, 16d bytes instead */
+                              /* of 24d; 1: never fuse                                        */
+  int32_t reserved1;
+  int64_t engine_fuse_wait_ns;/* a due passive waits up to this long for an active to take    */
+                              /* its lock (and fuse its step) before stepping alone; 0 = never */
+                              /* waits.  Scheduling only: any interleaving is an AD-PSGD run.  */
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its

@@ -191,12 +191,21 @@ __host__ __device__ __forceinline__ unsigned long long read_key(unsigned long lo
 
 // kFF = App. A order (Alg. 2): x_i <- fl(x_i - fl(gamma g)) first,
 // then m = fl(fl(x_i + x_j) * 0.5) to both endpoints.
-template <bool kPair, int kGrad, bool kFF = false>
+// kPreJ = fused passive step (engine): event k-1 is x_j's own local update
+// x_j <- fl(x_j - fl(gamma g(x_j; kkj))), applied before event k's average.
+template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
 __device__ __forceinline__ void update4(float4& a, float4& b, const float4 gext, const float4 xh,
                                         uint32_t c0, long long d, float gamma,
-                                        const QuadParams& q, uint32_t kk) {
+                                        const QuadParams& q, uint32_t kk, uint32_t kkj = 0u) {
   float av[4] = {a.x, a.y, a.z, a.w};
-  const float bv[4] = {b.x, b.y, b.z, b.w};
+  float bv[4] = {b.x, b.y, b.z, b.w};
+  if (kPair && kPreJ) {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const float gj = (long long)(c0 + e) < d ? quad_grad(bv[e], c0 + e, q.data_key, kkj, q.Mf, q.s) : 0.0f;
+      bv[e] = __fsub_rn(bv[e], __fmul_rn(gamma, gj));
+    }
+  }
   const float gv[4] = {gext.x, gext.y, gext.z, gext.w};
   const float hv[4] = {xh.x, xh.y, xh.z, xh.w};
   float out[4], mv[4];
@@ -317,12 +326,12 @@ struct Stager {
     return tot > first ? (tot - first + step - 1) / step : 0;
   }
 
-  template <bool kPair, int kGrad, bool kFF = false>
+  template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
   __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long first, long long step,
                                       long long hi, long long d, float gamma, const QuadParams& q,
-                                      uint32_t kk, const float4* g4 = nullptr) {
-    run_range<kPair, kGrad, kFF>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma, q, kk,
-                                 g4);
+                                      uint32_t kk, const float4* g4 = nullptr, uint32_t kkj = 0u) {
+    run_range<kPair, kGrad, kFF, kPreJ>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma,
+                                        q, kk, g4, kkj);
   }
 
   // Tiles [t0, t1) of this CTA's list; the partner row is read from xj_src and
@@ -330,11 +339,11 @@ struct Stager {
   // event xj_src is the local landing row and xj_dst the peer's model row).
   // kGradExternal reads the gradient row g4 directly (L2), issued before the
   // stage wait so it overlaps the bulk copies.
-  template <bool kPair, int kGrad, bool kFF = false>
+  template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
   __device__ __forceinline__ void run_range(float4* xi4, const float4* xj_src, float4* xj_dst, long long first,
                                             long long step, long long hi, long long t0, long long t1,
                                             long long d, float gamma, const QuadParams& q, uint32_t kk,
-                                            const float4* g4 = nullptr) {
+                                            const float4* g4 = nullptr, uint32_t kkj = 0u) {
     const long long n_t = t1 - t0;
     if (n_t <= 0) return;
     if (threadIdx.x == 0) {
@@ -376,8 +385,8 @@ struct Stager {
       for (int u = 0; u < kPer; ++u) {
         const long long idx = base + u * 512 + (int)threadIdx.x;
         if (idx < hi) {
-          update4<kPair, kGrad, kFF>(a[u], b[u], gx[u], make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d,
-                                     gamma, q, kk);
+          update4<kPair, kGrad, kFF, kPreJ>(a[u], b[u], gx[u], make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4),
+                                            d, gamma, q, kk, kkj);
           if (kPair) st_cg4(xj_dst + idx, b[u]);
           st_cg4(xi4 + idx, a[u]);
         }

@@ -62,6 +62,7 @@ struct SmemSlot {                  // tid 0 copies the running event here for th
   unsigned long long key;
   const float* g;
   float* gout;
+  int absorb;                      // fused passive local step (event k-1) before the pair
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -71,15 +72,20 @@ __device__ void latch_error(const EngineParams& p, unsigned int code) {
   atomicExch(&p.gctl->abort_flag, 1u);
 }
 
-// ticket k = next value of rank 0's counter, if below target (free-running)
-__device__ __noinline__ bool take_ticket(const EngineParams& p, unsigned long long* k) {
+// tickets k, k+1, ..: up to `want` consecutive values of rank 0's counter below
+// the target (free-running).  Returns how many were taken (0 = run is over).
+__device__ __noinline__ int take_tickets(const EngineParams& p, unsigned long long* k, int want) {
   unsigned long long t = ld_relaxed_sys64(&p.gctl0->ticket);
   while (true) {
-    if (t >= p.target) return false;
-    const unsigned long long old = atomicCAS_system(&p.gctl0->ticket, t, t + 1);
-    if (old == t) { *k = t; return true; }
+    if (t >= p.target) return 0;
+    const int got = (t + (unsigned long long)want <= p.target) ? want : (int)(p.target - t);
+    const unsigned long long old = atomicCAS_system(&p.gctl0->ticket, t, t + (unsigned long long)got);
+    if (old == t) { *k = t; return got; }
     t = old;
   }
+}
+__device__ __forceinline__ bool take_ticket(const EngineParams& p, unsigned long long* k) {
+  return take_tickets(p, k, 1) == 1;
 }
 
 __device__ void publish_running(Slot* sl, unsigned int seq) {
@@ -142,6 +148,7 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
     cw->wf_tread_cur = t;
     cw->wf_comp_cur = comp ? 1u : 0u;
     sl->kind = kKindPull;
+    sl->absorb = -1;
     sl->i = w; sl->j = -1; sl->tau = 0; sl->flags = 0u; sl->k = -1;
     sl->key = read_key(t, w);
     sl->xi = dw.x; sl->xj = nullptr;
@@ -178,6 +185,7 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
     return true;
   }
   sl->kind = kKindEvent;
+  sl->absorb = -1;
   sl->i = w; sl->j = j; sl->k = (long long)k; sl->key = k;
   sl->tau = flush ? (int)(k - cw->wf_tread_pub) : 0;
   sl->flags = flush ? (2u | (cw->wf_comp_pub ? 4u : 0u)) : 1u;
@@ -242,7 +250,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     }
     __threadfence_system();                                 // acquire their data
     sl->i = w; sl->j = e.j; sl->tau = 0; sl->flags = e.flags; sl->k = e.k;
-    sl->kind = kKindEvent; sl->g = nullptr;
+    sl->kind = kKindEvent; sl->g = nullptr; sl->absorb = -1;
     sl->key = (e.flags & 2u) ? read_key((unsigned long long)e.k, w) : (unsigned long long)e.k;   // R20
     sl->xi = dw.x; sl->xj = e.j >= 0 ? p.workers[e.j].x : nullptr;
     sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
@@ -271,6 +279,16 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
       st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
       return true;
     }
+    if (p.fuse && p.fuse_wait_ns && now < *(volatile unsigned long long*)&sl->ready_ns + p.fuse_wait_ns) {
+      // stay due but idle for a while: an active that takes our lock now runs
+      // this step inside its pair pass (only if some neighbour lives on this GPU)
+      bool local_nb = false;
+      for (int t = 0; t < dw.nb_cnt && !local_nb; ++t) local_nb = p.workers[p.nbrs[dw.nb_off + t]].local >= 0;
+      if (local_nb) {
+        st_release_gpu(&sl->tag, tag);
+        return false;
+      }
+    }
     lock = &dw.ctl->lock;
   }
   if (atomicCAS_system(lock, 0u, 1u) != 0u) {              // busy: stay pending, never block
@@ -278,13 +296,36 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     return false;
   }
   __threadfence_system();                                   // acquire the previous holder's data
+  // Fusion: holding the passive's lock, take over the passive's own pending
+  // local step if it is due (its slot idle and its compute phase over): event
+  // k is x_j's local update, event k+1 this pair, both in ONE pass (16d bytes
+  // instead of 8d + 16d).  Ticket order = lock order, so the log replays as is.
+  int absorb = -1;
+  unsigned int tj = 0u;
+  if (p.fuse && j >= 0 && p.model != 0) {
+    const int lj = p.workers[j].local;
+    if (lj >= 0) {
+      Slot* sj = p.slots + lj;
+      tj = ld_acquire_gpu(&sj->tag);
+      if ((tj & 3u) == kStateIdle && now >= *(volatile unsigned long long*)&sj->ready_ns &&
+          atomicCAS(&sj->tag, tj, tag_of(tj >> 2, kStateClaimed)) == tj)
+        absorb = lj;
+    }
+  }
   unsigned long long k;
-  if (!take_ticket(p, &k)) {
+  const int got = take_tickets(p, &k, absorb >= 0 ? 2 : 1);
+  if (absorb >= 0 && got < 2) {                             // one ticket left: the pair runs alone
+    st_release_gpu(&p.slots[absorb].tag, tj);
+    absorb = -1;
+  }
+  if (got == 0) {
     __threadfence_system();
     atomicExch_system(lock, 0u);
     st_release_gpu(&sl->tag, tag_of(seq, kStateFinished));
     return true;
   }
+  if (absorb >= 0) ++k;                                     // the pair is the second event
+  sl->absorb = absorb;
   sl->i = w; sl->j = j; sl->tau = 0; sl->flags = p.model == 0 ? 1u : 0u; sl->k = (long long)k;
   sl->kind = kKindEvent; sl->key = k; sl->g = nullptr;
   sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
@@ -327,8 +368,23 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   LogEntry* le = p.log + (k % p.log_cap);
   le->k = k; le->i = i; le->j = j; le->tau = sl->tau; le->flags = flags;
   le->t0 = sl->t0; le->t1 = now;
+  const int ab = sl->absorb;
+  if (ab >= 0) {                          // the fused passive step: event k-1 = (j, -1), W = I
+    atomicAdd(&sl->ctl_j->updates, 1ull);
+    LogEntry* lj = p.log + ((k - 1) % p.log_cap);
+    lj->k = k - 1; lj->i = j; lj->j = -1; lj->tau = 0; lj->flags = 0u;
+    lj->t0 = sl->t0; lj->t1 = now;
+    atomicAdd(&p.gctl->st_events, 1ull);
+    atomicAdd_system(&p.gctl0->committed, 1ull);
+    Slot* sj = p.slots + ab;              // the passive's next compute phase starts now
+    sj->ready_ns = now + (unsigned long long)((double)p.workers[j].straggle * (double)p.compute_ns);
+    sl->absorb = -1;
+    __threadfence();
+    st_release_gpu(&sj->tag, tag_of(sj->tag >> 2, kStateIdle));
+  }
   // stats: algorithmic bytes: pair 16d, local 8d; NVLink 8d per cross
-  // pair; a flushed App. A buffer adds its 4d read
+  // pair; a flushed App. A buffer adds its 4d read; a fused passive step adds
+  // nothing (its row is already read and written by the pair)
   atomicAdd(&p.gctl->st_events, 1ull);
   if (j >= 0) atomicAdd(&p.gctl->st_pair, 1ull);
   if (sl->cross) { atomicAdd(&p.gctl->st_cross, 1ull); atomicAdd(&p.gctl->st_nvl_bytes, 2.0 * d4); }
@@ -380,9 +436,10 @@ constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * 
 template <int kVar>
 using EngineStager = Stager<kTile4, kStages, kVar == 2>;
 
-template <int kVar, bool kPair, int kGrad, bool kFF = false>
+template <int kVar, bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
 __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, EngineStager<kVar>& stg) {
   const uint32_t kk = quad_event_key_h(p.q.noise_key, e.key);
+  const uint32_t kkj = kPreJ ? quad_event_key_h(p.q.noise_key, e.key - 1ull) : 0u;   // the passive's event k-1
   float4* xi4 = reinterpret_cast<float4*>(e.xi);
   float4* xj4 = reinterpret_cast<float4*>(e.xj);
   const float4* g4 = reinterpret_cast<const float4*>(e.g);
@@ -391,7 +448,8 @@ __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, 
       stg.template run_range<kPair, kGrad, kFF>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
                                                 gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk, g4);
     else
-      stg.template run<kPair, kGrad, kFF>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk, g4);
+      stg.template run<kPair, kGrad, kFF, kPreJ>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk, g4,
+                                                 kkj);
   } else {
     const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)blockIdx.x * per;
@@ -490,6 +548,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.key = *(volatile unsigned long long*)&sl->key;
         s_ev.g = *(float* volatile*)&sl->g;
         s_ev.gout = *(float* volatile*)&sl->gout;
+        s_ev.absorb = *(volatile int*)&sl->absorb >= 0 ? 1 : 0;
         s_ev.pair = s_ev.xj != nullptr;
         s_ev.cross = cross;
         s_ev.t0 = t0;
@@ -540,6 +599,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
       } else if (e.pair) {
         if (e.grad) {
           if (kVar != 1 && e.ff) slice<kVar, true, kGradQuadInline, true>(p, e, stg);
+          else if (kVar != 1 && e.absorb) slice<kVar, true, kGradQuadInline, false, true>(p, e, stg);
           else slice<kVar, true, kGradQuadInline>(p, e, stg);
         } else {
           slice<kVar, true, kGradNone>(p, e, stg);

@@ -39,6 +39,7 @@ struct Slot {                      // per local worker, in local device memory
   // slow-link emulation (R21): the passive's lock is released at unlock_at
   unsigned int* held_lock;
   unsigned long long unlock_at;
+  int absorb;                      // slot of a passive whose local step (event k-1) is fused into this pair, -1 none
 };
 constexpr int kKindEvent = 0, kKindPull = 1;
 
@@ -77,6 +78,8 @@ struct EngineParams {
   unsigned int* served;            // [n_local][kMaxGrid] last push request served per CTA (persistent)
   int wait_free;                   // free-running loop: 0 Alg. 1, 1 App. A, 2 App. A + compensation
   long long link_ns;               // nominal model-transfer time of a 1x link (R21)
+  int fuse;                        // fuse a due passive local step into the pair that holds its lock
+  unsigned long long fuse_wait_ns; // a due passive stays absorbable this long before stepping alone
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);

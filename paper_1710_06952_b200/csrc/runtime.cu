@@ -84,6 +84,8 @@ struct adpsgd_ctx {
   long long compute_ns = 0;
   int engine_cps = 0, engine_threads = 512, engine_variant = 0;
   int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
+  int engine_fuse = 1;               // fuse due passive steps into pair passes
+  long long fuse_wait_ns = 0;        // how long a due passive stays absorbable
   std::vector<float> link;           // link slowdown per worker (reading R21)
   long long link_ns = 0;
   float link_max() const { return link.empty() ? 1.0f : *std::max_element(link.begin(), link.end()); }
@@ -579,6 +581,8 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.served = c->served;
   p.wait_free = mode == 0 ? c->wait_free : 0;
   p.link_ns = c->link_ns;
+  p.fuse = c->engine_fuse;
+  p.fuse_wait_ns = (unsigned long long)c->fuse_wait_ns;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
@@ -599,6 +603,7 @@ adpsgd_status reset_slots(adpsgd_ctx* c, cudaStream_t s) {
     Slot& x = c->h_slots[l];
     x.tag = 0;
     x.pending_j = -2;
+    x.absorb = -1;
     x.nb_ctr = c->run_counter << 20;
     x.j = -1;
   }
@@ -746,6 +751,9 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   c->wait_free = cfg->wait_free;
+  c->engine_fuse = cfg->engine_no_fuse ? 0 : 1;
+  c->fuse_wait_ns = cfg->engine_fuse_wait_ns;
+  if (c->fuse_wait_ns < 0) return fail(ADPSGD_E_INVALID, "engine_fuse_wait_ns < 0");
   if (c->wait_free < 0 || c->wait_free > 2) return fail(ADPSGD_E_INVALID, "wait_free must be 0, 1 or 2");
   if (c->wait_free && c->model != ADPSGD_MODEL_QUADRATIC)
     return fail(ADPSGD_E_UNSUPPORTED, "the wait-free (App. A) engine loop supports the QUADRATIC model");
