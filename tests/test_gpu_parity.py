@@ -436,3 +436,29 @@ def test_slow_link_locality_and_log_replay(P):
     cnt = ctx.update_counts()
     assert min(cnt[4], cnt[6]) > max(cnt[0], cnt[2])            # actives not adjacent to worker 1
     ctx.destroy()
+
+
+def test_fused_passive_steps_replay_bitwise(P):
+    """Engine fusion: a due passive's local step run inside the pair pass that
+    holds its lock (events k-1 = (j, -1) and k = (i, j), one pass).  A long
+    passive wait makes fusion frequent; the log must still replay bitwise and
+    every fused step must sit right before its pair, sharing its start time."""
+    n, d, U = 8, (1 << 18) + 44, 3000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(19)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    X0 = synth.x0_uniform(n, d, seed=20)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s, compute_ns=20_000, seed=4,
+                    engine_fuse_wait_ns=200_000)
+    ctx.run(U)
+    ctx.sync()
+    log = ctx.read_log(0)
+    loc = log["j"] < 0
+    fused = loc[:-1] & (log["j"][1:] == log["i"][:-1]) & (log["t0"][1:] == log["t0"][:-1])
+    assert fused.sum() > 20
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, X0, e, r, log_events(log))
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    assert sum(ctx.update_counts().values()) == U
+    ctx.destroy()
