@@ -31,9 +31,14 @@ s = float(np.float32(0.1 * math.sqrt(96)))
 ctx = P.Context(e, a.n, a.d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk),
                 quad_noise_s=s, straggler=synth.stragglers(a.n), compute_ns=int(a.compute_us * 1000))
 if a.what == "engine":
-    for _ in range(a.runs):
+    for it in range(a.runs):
+        s0 = ctx.stats()
         ctx.run(a.updates)
         ctx.sync()
+        s1 = ctx.stats()
+        print(f"run {it}: events {s1['local_events'] - s0['local_events']}, "
+              f"pair {s1['local_pair_events'] - s0['local_pair_events']}, "
+              f"algorithmic_bytes {s1['local_bytes'] - s0['local_bytes']:.6e}", flush=True)
 elif a.what == "event":
     ev, _ = synth.schedule_iid(a.n, e, K=a.updates, seed=1)
     for _ in range(a.runs):
