@@ -497,10 +497,17 @@ def main():
         wf["workload"] = "config 4 workload and straggler, adpsgd_run with wait_free = 1 / 2"
         extras["wait_free_appA"] = wf
         if world > 1:
-            # NVLink stress: pure gossip, interleave placement -> every pair event crosses GPUs
-            cn = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+            # NVLink stress: pure gossip, every pair event crosses GPUs.  World >= 4: the xor
+            # placement also spreads the actives (the GPUs that compute events) evenly; at
+            # world 2 no all-cross placement can (interleave: all actives on GPU 0)
+            # 32 workers per GPU (config 5's count at 4 GPUs) keep enough disjoint pairs in flight
+            ns = 32 * world
+            es, rs = synth.ring(ns)
+            xor = world >= 4 and (world & (world - 1)) == 0
+            cn = P.Context(es, ns, d, role=rs, rank=rank, world_size=world, device=local,
+                           placement=2 if xor else 1, worker_rank=synth.placement_xor(ns, world) if xor else None,
                            engine_variant=a.engine_variant, log_capacity=1 << 16)
-            cn.run(4 * n, stream)
+            cn.run(2 * ns, stream)
             torch.cuda.synchronize()
             cn.sync()
             barrier()
@@ -508,7 +515,7 @@ def main():
             ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             ta.record(stream)
             for _ in range(3):
-                cn.run(16 * n, stream)
+                cn.run(8 * ns, stream)
             tb.record(stream)
             torch.cuda.synchronize()
             cn.sync()
@@ -520,7 +527,8 @@ def main():
             cn.destroy()
             barrier()
             extras["nvlink_stress"] = {
-                "workload": f"pure gossip, n={n} ring, interleave placement (every pair crosses GPUs), d={d}",
+                "workload": f"pure gossip, free-running, n={ns} ring, {'xor' if xor else 'interleave'} placement "
+                            f"(every pair crosses GPUs{'' if xor else '; all actives on even GPUs'}), d={d}",
                 "gossip_steps_per_s": npair / secn,
                 "per_gpu_per_direction_gbs": nvb / secn / world / 1e9,
                 "frac_of_900": nvb / secn / world / 900e9,

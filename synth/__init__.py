@@ -86,6 +86,18 @@ def schedule_iid(n, edges, K, T=0, seed=0, M=0, S=0, no_grad=False, tau=None,
     return ev, bidx
 
 
+def placement_xor(n: int, G: int) -> np.ndarray:
+    """Worker -> GPU for a ring where EVERY edge crosses GPUs and the actives
+    (even workers) are spread over all GPUs: GPU(w) = (w mod G) xor ((w div G)
+    mod 2).  Needs G a power of two >= 4 and n a multiple of 2G.  (With G = 2
+    no such placement exists: a connected bipartite graph has one 2-colouring,
+    so 'every edge crosses' forces GPU = role, i.e. all actives on one GPU.)"""
+    if G < 4 or G & (G - 1) or n % (2 * G):
+        raise ValueError("placement_xor needs G = 4, 8, ... and n % 2G == 0")
+    w = np.arange(n)
+    return ((w % G) ^ ((w // G) % 2)).astype(np.int32)
+
+
 EV_FLUSH_FIRST, EV_COMPENSATE = 2, 4
 
 

@@ -22,25 +22,33 @@ ap.add_argument("--d", type=int, default=25_600_000)
 ap.add_argument("--events", type=int, default=128)
 ap.add_argument("--variants", default="0,3,1")
 ap.add_argument("--model", default="none")
+ap.add_argument("--mode", default="replay", choices=["replay", "run"])
+ap.add_argument("--wpg", type=int, default=8, help="workers per GPU")
+ap.add_argument("--placement", default="interleave", choices=["interleave", "xor"])
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
 dist.init_process_group("nccl", device_id=torch.device("cuda", local))
-n = 8 * world
+n = a.wpg * world
 e, r = synth.ring(n)
 quad = a.model == "quad"
 ev, _ = synth.schedule_iid(n, e, K=a.events, seed=2, no_grad=not quad)
 for v in [int(x) for x in a.variants.split(",")]:
-    ctx = P.Context(e, n, a.d, role=r, rank=rank, world_size=world, device=local, placement=1,
+    xor = a.placement == "xor"
+    ctx = P.Context(e, n, a.d, role=r, rank=rank, world_size=world, device=local, placement=2 if xor else 1,
+                    worker_rank=synth.placement_xor(n, world) if xor else None,
                     model=P.MODEL_QUADRATIC if quad else P.MODEL_NONE, gamma=0.01, batch_M=32,
                     quad_keys=(1, 2), quad_noise_s=0.5, engine_variant=v)
     s = torch.cuda.Stream()
-    ctx.replay(ev, flags=P.REPLAY_ENGINE, stream=s)
+    go = (lambda: ctx.replay(ev, flags=P.REPLAY_ENGINE, stream=s)) if a.mode == "replay" else \
+        (lambda: ctx.run(len(ev), stream=s))
+    go()
     torch.cuda.synchronize()
+    ctx.sync()
     dist.barrier()
     t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     t0.record(s)
-    ctx.replay(ev, flags=P.REPLAY_ENGINE, stream=s)
+    go()
     t1.record(s)
     torch.cuda.synchronize()
     ms = torch.tensor([t0.elapsed_time(t1)], device="cuda")
@@ -49,7 +57,7 @@ for v in [int(x) for x in a.variants.split(",")]:
     cross = len(ev)
     nvl = cross * 8.0 * a.d / world / (ms / 1e3) / 1e9
     if rank == 0:
-        print(f"variant {v}: {len(ev)} cross events in {ms:.2f} ms -> {len(ev) / (ms / 1e3):.0f} events/s, "
+        print(f"{a.mode} {a.placement} wpg={a.wpg} variant {v}: {len(ev)} cross events in {ms:.2f} ms -> {len(ev) / (ms / 1e3):.0f} events/s, "
               f"NVLink {nvl:.0f} GB/s per GPU per direction", flush=True)
     ctx.destroy()
     dist.barrier()

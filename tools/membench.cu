@@ -206,6 +206,41 @@ int peer_main() {
     printf("%-48s %8.1f us %7.0f GB/s per direction\n", mode == 0 ? "bidirectional push (both GPUs write peer)" :
            "bidirectional pull (both GPUs read peer)", s * 1e6, bytes / s / 1e9);
   }
+  // symmetric cross-GPU pair events: GPU0 averages (xi, yi@GPU1) while GPU1 averages
+  // (yi, xi@GPU0) -- the engine's all-cross pattern; per direction 8d per round
+  // (4d of read responses + 4d of written averages)
+  {
+    constexpr int T = 1024, S = 3;
+    size_t smem = (size_t)S * 2 * T * 16 + 64;
+    for (int dev = 0; dev < 2; ++dev) {
+      cudaSetDevice(dev);
+      cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      cudaFuncSetAttribute(avg_tma<T, S, true, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    }
+    cudaSetDevice(0);
+    for (int kind = 0; kind < 3; ++kind) {
+      auto both = [&] {
+        for (int dev = 0; dev < 2; ++dev) {
+          cudaSetDevice(dev);
+          float4* a = dev == 0 ? xi : yi;      // local row
+          float4* b = dev == 0 ? yi : xi;      // peer row
+          cudaStream_t st = dev == 0 ? s0 : s1;
+          if (kind == 0) avg_stride<4><<<sms * 2, 512, 0, st>>>(a, b, n4, 1);
+          else if (kind == 1) avg_tma<T, S, false, true><<<sms * 2, 512, smem, st>>>(a, b, n4, 1);
+          else avg_tma<T, S, true, true><<<sms * 2, 512, smem, st>>>(a, b, n4, 1);
+        }
+        cudaSetDevice(0);
+      };
+      both(); cudaDeviceSynchronize(); cudaSetDevice(1); cudaDeviceSynchronize(); cudaSetDevice(0);
+      auto t0 = std::chrono::steady_clock::now();
+      for (int r = 0; r < it; ++r) both();
+      cudaDeviceSynchronize(); cudaSetDevice(1); cudaDeviceSynchronize(); cudaSetDevice(0);
+      double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / it;
+      const char* nm[3] = {"symmetric pair avg, ldg/stg stride U4 2/SM", "symmetric pair avg, tma T1024 S3 + stg",
+                           "symmetric pair avg, tma T1024 S3 + bulk st"};
+      printf("%-48s %8.1f us %7.0f GB/s per direction\n", nm[kind], s * 1e6, 2.0 * bytes / s / 1e9);
+    }
+  }
   return 0;
 }
 
