@@ -4,6 +4,9 @@
 #include <cstdio>
 #include <chrono>
 #include <cstdint>
+#include <cstdlib>
+#include <cstring>
+#include <vector>
 #include <cuda_runtime.h>
 
 #define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
@@ -244,7 +247,50 @@ int peer_main() {
   return 0;
 }
 
+// G GPUs at once: GPU g pair-averages its row with GPU (g+1)'s row (reads it,
+// writes the average back) -- every GPU both serves and drives NVLink traffic,
+// per direction 8d per round per GPU (the engine's all-cross pattern at G GPUs)
+int ring_main(int G) {
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (ndev < G) { printf("ring: need %d GPUs\n", G); return 0; }
+  const long long d = 25600000, n4 = d / 4;
+  constexpr int T = 1024, S = 3;
+  size_t smem = (size_t)S * 2 * T * 16 + 64;
+  std::vector<float4*> x(G);
+  std::vector<cudaStream_t> st(G);
+  for (int g = 0; g < G; ++g) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < G; ++h) if (h != g) cudaDeviceEnablePeerAccess(h, 0);
+    CK(cudaMalloc(&x[g], d * 4)); CK(cudaMemset(x[g], 0, d * 4));
+    CK(cudaStreamCreate(&st[g]));
+    cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  for (int kind = 0; kind < 2; ++kind) {
+    auto all = [&] {
+      for (int g = 0; g < G; ++g) {
+        cudaSetDevice(g);
+        float4* b = x[(g + 1) % G];
+        if (kind == 0) avg_stride<4><<<sms * 2, 512, 0, st[g]>>>(x[g], b, n4, 1);
+        else avg_tma<T, S, false, true><<<sms * 2, 512, smem, st[g]>>>(x[g], b, n4, 1);
+      }
+    };
+    auto sync = [&] { for (int g = 0; g < G; ++g) { cudaSetDevice(g); cudaDeviceSynchronize(); } };
+    all(); sync();
+    const int it = 20;
+    auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < it; ++r) all();
+    sync();
+    double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / it;
+    printf("ring of %d GPUs, pair avg with next GPU's row, %-22s %8.1f us %7.0f GB/s per GPU per direction\n", G,
+           kind == 0 ? "ldg/stg stride U4" : "tma T1024 S3 + stg", s * 1e6, 8.0 * d / s / 1e9);
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 2 && !strcmp(argv[1], "ring")) return ring_main(atoi(argv[2]));
   if (argc > 1) return peer_main();
   const long long d = 25600000, n4 = d / 4;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
