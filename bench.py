@@ -535,6 +535,9 @@ def main():
                 "frac_of_measured_peer_copy_770": nvb / secn / world / 770e9}
         if world == 1:
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            import gemm_sweep
+            extras["mlp_gemm_sweep"] = gemm_sweep.sweep(reps=10)
 
     cpu = None
     if rank == 0 and world == 1 and not a.no_extras:

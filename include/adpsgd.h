@@ -316,6 +316,15 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
 adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
                                  int32_t splits);
 
+/* Diagnostics: device time of that GEMM alone (tcgen05 utilisation
+ * of the MLP GEMMs swept over M).  Allocates operands of the given shape on the
+ * current device, splits them into tf32 planes once, then times `reps` launches
+ * of the GEMM kernel (+ the split-K partial sum when splits > 1) with CUDA
+ * events after 2 warm-up launches; *ms_out = mean milliseconds per GEMM.
+ * bn = 128 or 256 (N tile).  Shape rules as adpsgd_gemm_tf32x3.  Synchronous. */
+adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t bn, int32_t reps,
+                                       double* ms_out);
+
 #ifdef __cplusplus
 }
 #endif

@@ -34,7 +34,7 @@ EXPORTED = ["adpsgd_abi_version", "adpsgd_last_error", "adpsgd_init", "adpsgd_de
             "adpsgd_model_device_ptr", "adpsgd_worker_rank", "adpsgd_get_ticket", "adpsgd_read_log",
             "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count",
             "adpsgd_gemm_tf32x3", "adpsgd_plan_placement", "adpsgd_plan_replay", "adpsgd_dpsgd",
-            "adpsgd_dpsgd_reset", "adpsgd_dpsgd_read_model"]
+            "adpsgd_dpsgd_reset", "adpsgd_dpsgd_read_model", "adpsgd_gemm_tf32x3_bench"]
 
 
 class AdpsgdError(RuntimeError):
@@ -106,6 +106,7 @@ def lib():
             "adpsgd_plan_replay": ([I32, P, I32, P, I64, I64, P, P, I64, P], I32),
             "adpsgd_dpsgd": ([P, I64, P], I32), "adpsgd_dpsgd_reset": ([P, P], I32),
             "adpsgd_dpsgd_read_model": ([P, I32, P], I32),
+            "adpsgd_gemm_tf32x3_bench": ([I32, I32, I32, I32, I32, I32, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -174,6 +175,13 @@ def gemm_tf32x3(A_ptr, B_ptr, C_ptr, M, N, K, splits=1):
     """Diagnostics: C = A . B^T on tcgen05 (3xTF32), device pointers (see adpsgd.h)."""
     _chk(lib().adpsgd_gemm_tf32x3(C.c_void_p(A_ptr), C.c_void_p(B_ptr), C.c_void_p(C_ptr), M, N, K, splits),
          "gemm_tf32x3")
+
+
+def gemm_tf32x3_bench(M, N, K, splits=1, bn=128, reps=20):
+    """Diagnostics: mean device ms of the tcgen05 3xTF32 GEMM kernel at this shape."""
+    ms = C.c_double()
+    _chk(lib().adpsgd_gemm_tf32x3_bench(M, N, K, splits, bn, reps, C.byref(ms)), "gemm_tf32x3_bench")
+    return ms.value
 
 
 class Context:

@@ -97,6 +97,7 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
                                int M, uint2 batch_key, unsigned long long k, const float* xhat,
                                float* g, long long d, cudaStream_t s);
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s);
+cudaError_t launch_fill_hash(float* x, long long n, uint32_t seed, cudaStream_t s);   // diagnostics
 // App. A local-update compensation of a pulled model: out = fl(x - fl(gamma gp))
 cudaError_t launch_comp_row(const float* x, const float* gp, float gamma, float* out, long long n4, cudaStream_t s);
 cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,

@@ -121,6 +121,12 @@ __global__ void k_copy(float4* __restrict__ dst, const float4* __restrict__ src,
     st_cg4(dst + i, ld_cg4(src + i));
 }
 
+// pseudo-random values in [-1, 1) (diagnostic operands: GEMM timing)
+__global__ void k_fill_hash(float* __restrict__ x, long long n, uint32_t seed) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x)
+    x[i] = __uint_as_float(0x40000000u | (lowbias32((uint32_t)i ^ seed) >> 9)) - 3.0f;
+}
+
 // App. A compensation (footnote at P:1265-1268): out = fl(x - fl(gamma gp))
 __global__ void k_comp_row(const float4* __restrict__ x, const float4* __restrict__ gp, float gamma,
                            float4* __restrict__ out, long long n4) {
@@ -356,6 +362,11 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s) {
   k_copy<<<stream_grid(n4), kThreads, 0, s>>>(reinterpret_cast<float4*>(dst),
                                               reinterpret_cast<const float4*>(src), n4);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fill_hash(float* x, long long n, uint32_t seed, cudaStream_t s) {
+  k_fill_hash<<<4 * sm_count(), 256, 0, s>>>(x, n, seed);
   return cudaGetLastError();
 }
 

@@ -1531,4 +1531,49 @@ adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32
   })
 }
 
+adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t bn, int32_t reps,
+                                       double* ms_out) {
+  GUARD({
+    if (!ms_out || M <= 0 || N <= 0 || K <= 0 || splits < 1 || reps < 1 || (bn != 128 && bn != 256))
+      return fail(ADPSGD_E_INVALID, "gemm bench args");
+    if (M % 128 || N % bn || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
+    const size_t na = (size_t)M * K, nb = (size_t)N * K;
+    float* buf = nullptr;
+    CU(cudaMalloc(&buf, sizeof(float) * (3 * na + 3 * nb + (size_t)(splits + 1) * M * N)));
+    float *a = buf, *b = a + na, *ah = b + nb, *al = ah + na, *bh = al + na, *bl = bh + nb, *part = bl + nb;
+    float* c = part + (size_t)splits * M * N;
+    GemmOperands op;
+    adpsgd_status st = ADPSGD_OK;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    cudaError_t e = launch_fill_hash(a, (long long)na, 1u, nullptr);
+    if (e == cudaSuccess) e = launch_fill_hash(b, (long long)nb, 2u, nullptr);
+    if (e == cudaSuccess) e = launch_split_tf32(a, ah, al, (long long)na, nullptr);
+    if (e == cudaSuccess) e = launch_split_tf32(b, bh, bl, (long long)nb, nullptr);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Ah, ah, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Al, al, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bh, bh, N, K, bn);
+    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bl, bl, N, K, bn);
+    auto once = [&]() {
+      cudaError_t r = launch_gemm_tf32x3(op, splits > 1 ? part : c, M, N, K, splits, bn, nullptr);
+      if (r == cudaSuccess && splits > 1) r = launch_sum_planes(part, c, splits, (long long)M * N, nullptr);
+      return r;
+    };
+    for (int w = 0; w < 2 && e == cudaSuccess; ++w) e = once();
+    if (e == cudaSuccess) e = cudaEventCreate(&e0);
+    if (e == cudaSuccess) e = cudaEventCreate(&e1);
+    if (e == cudaSuccess) e = cudaEventRecord(e0, nullptr);
+    for (int r = 0; r < reps && e == cudaSuccess; ++r) e = once();
+    if (e == cudaSuccess) e = cudaEventRecord(e1, nullptr);
+    if (e == cudaSuccess) e = cudaEventSynchronize(e1);
+    float ms = 0.f;
+    if (e == cudaSuccess) e = cudaEventElapsedTime(&ms, e0, e1);
+    if (e != cudaSuccess) st = fail(ADPSGD_E_CUDA, std::string("gemm bench: ") + cudaGetErrorString(e));
+    else *ms_out = (double)ms / reps;
+    if (e0) cudaEventDestroy(e0);
+    if (e1) cudaEventDestroy(e1);
+    cudaFree(buf);
+    return st;
+  })
+}
+
 }  // extern "C"
