@@ -599,3 +599,73 @@ int oracle_dpsgd_round(const oracle_problem* p, int32_t n, int64_t d, float* X, 
   free(deg); free(Xn); free(g);
   return st;
 }
+
+/* ------------------------------------------------------- super-learner ----
+ * "combining learners on the same computing node as a super-learner
+ * (via Nvidia NCCL AllReduce collectives)".  DESIGN.md reading R22: a
+ * super-learner s is one AD-PSGD worker made of R learners; its gradient is the
+ * all-reduce SUM of the learners' minibatch gradients (batch R*M), each learner r
+ * drawing its noise with key(s, c, r) = 2^61 | s<<44 | c<<8 | r, c = the number
+ * of earlier gradient events of s.  The sum is taken in fp64 and rounded once to
+ * fp32 (for R = 2 this is exactly the fp32 sum an all-reduce computes).        */
+uint64_t oracle_super_key(int32_t s, int64_t c, int32_t r) {
+  return (1ull << 61) | ((uint64_t)(uint32_t)s << 44) | ((uint64_t)c << 8) | (uint64_t)(uint32_t)r;
+}
+
+int oracle_super_gradient(const oracle_problem* p, int64_t d, const float* x, int32_t s, int64_t c, int32_t R,
+                          float* g) {
+  if (!p || !x || !g || R < 1 || p->kind != ORC_MODEL_QUADRATIC) return ORC_E_INVALID;
+  double* acc = (double*)calloc((size_t)d, sizeof(double));
+  float* gr = (float*)malloc(sizeof(float) * (size_t)d);
+  if (!acc || !gr) { free(acc); free(gr); return ORC_E_OOM; }
+  int st = ORC_OK;
+  for (int32_t r = 0; r < R && st == ORC_OK; ++r) {
+    st = oracle_quadratic_grad(p, d, x, oracle_super_key(s, c, r), gr);
+    for (int64_t e = 0; e < d; ++e) acc[e] += (double)gr[e];
+  }
+  for (int64_t e = 0; e < d; ++e) g[e] = (float)acc[e];
+  free(acc); free(gr);
+  return st;
+}
+
+/* Replay of super-learner events (i, j, 0, flags) over S super-learners in
+ * Alg. 1 order (average, then x_i <- m - gamma g), tau = 0, X: S x d (one
+ * model per super-learner: its R replicas are identical by construction).   */
+int oracle_super_replay(const oracle_problem* p, int32_t S, int64_t d, float* X, int32_t n_edges,
+                        const int32_t* edges, const int8_t* role, const int32_t* events, int64_t K, int32_t R) {
+  if (!p || S < 1 || d < 1 || !X || K < 0 || (K > 0 && !events) || R < 1) return ORC_E_INVALID;
+  int8_t* rl = (int8_t*)malloc((size_t)S);
+  int64_t* cnt = (int64_t*)calloc((size_t)S, sizeof(int64_t));
+  float* g = (float*)malloc(sizeof(float) * (size_t)d);
+  if (!rl || !cnt || !g) { free(rl); free(cnt); free(g); return ORC_E_OOM; }
+  int st = oracle_check_graph(S, n_edges, edges, role, rl);
+  if (S == 1 && n_edges == 0) st = ORC_OK;
+  for (int64_t k = 0; k < K && st == ORC_OK; ++k) {
+    const int32_t i = events[4 * k], j = events[4 * k + 1];
+    const uint32_t flags = (uint32_t)events[4 * k + 3];
+    if (i < 0 || i >= S || j < -1 || j >= S || j == i) { st = ORC_E_INVALID; break; }
+    if (j >= 0 && (!is_edge(n_edges, edges, i, j) || rl[i] == rl[j])) { st = ORC_E_NOT_NEIGHBOURS; break; }
+    float* xi = X + (int64_t)i * d;
+    const int grad = !(flags & ORC_EV_NO_GRAD) && p->kind != ORC_MODEL_NONE;
+    if (grad) {
+      st = oracle_super_gradient(p, d, xi, i, cnt[i], R, g);
+      cnt[i] += 1;
+      if (st != ORC_OK) break;
+    }
+    if (j >= 0) {
+      float* xj = X + (int64_t)j * d;
+      for (int64_t c = 0; c < d; ++c) {
+        float s2 = xi[c] + xj[c];
+        float m = s2 * 0.5f;
+        xi[c] = m; xj[c] = m;
+      }
+    }
+    if (grad)
+      for (int64_t c = 0; c < d; ++c) {
+        float step = p->gamma * g[c];
+        xi[c] = xi[c] - step;
+      }
+  }
+  free(rl); free(cnt); free(g);
+  return st;
+}

@@ -73,6 +73,11 @@ def lib():
             L.oracle_mlp_dim.restype = C.c_int64
             L.oracle_read_key.argtypes = [C.c_uint64, C.c_int32]
             L.oracle_read_key.restype = C.c_uint64
+            L.oracle_super_key.argtypes = [C.c_int32, C.c_int64, C.c_int32]
+            L.oracle_super_key.restype = C.c_uint64
+            L.oracle_super_gradient.argtypes = [C.POINTER(Problem), C.c_int64, P, C.c_int32, C.c_int64, C.c_int32, P]
+            L.oracle_super_replay.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int64, P, C.c_int32, P, P, P,
+                                              C.c_int64, C.c_int32]
             _lib = L
     return _lib
 
@@ -202,3 +207,26 @@ def dpsgd_round(prob: OracleProblem, X, edges, k_base=0):
                                      C.c_void_p, C.c_uint64]
     _check(L.oracle_dpsgd_round(prob.ref, X.shape[0], X.shape[1], _p(X), e.shape[0], _p(e), k_base))
     return X
+
+
+def super_gradient(prob: OracleProblem, x, s, c, R):
+    """Super-learner gradient (reading R22): fp64 sum of R learners' quadratic gradients."""
+    x = np.ascontiguousarray(np.asarray(x, np.float32))
+    g = np.zeros_like(x)
+    _check(lib().oracle_super_gradient(prob.ref, x.size, _p(x), s, c, R, _p(g)))
+    return g
+
+
+def super_replay(prob: OracleProblem, X, edges, role, events, R):
+    """Replay super-learner events (i, j, 0, flags) over S = X.shape[0] super-learners."""
+    X = np.ascontiguousarray(np.array(X, np.float32, copy=True))
+    S, d = X.shape
+    e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
+    r = None if role is None else np.ascontiguousarray(np.asarray(role, np.int8))
+    ev = np.ascontiguousarray(np.asarray(events, np.int32).reshape(-1, 4))
+    _check(lib().oracle_super_replay(prob.ref, S, d, _p(X), e.shape[0], _p(e), _p(r), _p(ev), ev.shape[0], R))
+    return X
+
+
+def super_key(s, c, r) -> int:
+    return int(lib().oracle_super_key(s, c, r))

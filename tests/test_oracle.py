@@ -550,3 +550,46 @@ def test_dpsgd_spec_example_and_invariants():
         X = O.dpsgd_round(O.OracleProblem(), X, e)
     assert np.abs(X.astype(np.float64).sum(0) - X0.astype(np.float64).sum(0)).max() < 1e-4
     assert np.abs(X - X.mean(0)).max() < 1e-4 * np.abs(X0).max()
+
+
+# ------------------------------------------------------------ super-learner --
+def test_super_gradient_noiseless_is_R_times_the_learner_gradient():
+    """Reading R22: a super-learner's gradient is the all-reduce SUM of
+    its R learners' minibatch gradients.  With no noise every learner computes
+    M h (x - x*), so the sum is exactly R times it (R a power of two)."""
+    d = 300
+    rng = np.random.default_rng(3)
+    h = rng.uniform(0.1, 1.0, d).astype(np.float32)
+    xs = rng.uniform(-1, 1, d).astype(np.float32)
+    x = rng.uniform(-2, 2, d).astype(np.float32)
+    p = O.OracleProblem(O.MODEL_QUADRATIC, M=8, gamma=0.01, h=h, xstar=xs)
+    g1 = O.gradient(p, x, k=5)
+    for R in (1, 2, 4):
+        assert np.array_equal(O.super_gradient(p, x, s=3, c=7, R=R), (np.float32(R) * g1).astype(np.float32))
+
+
+def test_super_gradient_noise_statistics():
+    """The R learners draw independent noise s*v, v ~ U[-1, 1) (23-bit grid): the
+    summed noise has mean 0 and variance R s^2 / 3."""
+    d, R, s = 200_000, 4, 0.5
+    p = O.OracleProblem(O.MODEL_QUADRATIC, M=1, gamma=0.0, noise_s=s, h=np.zeros(d, np.float32),
+                        xstar=np.zeros(d, np.float32))
+    g = O.super_gradient(p, np.zeros(d, np.float32), s=1, c=0, R=R).astype(np.float64)
+    assert abs(g.mean()) < 5 * math.sqrt(R * s * s / 3 / d)
+    assert abs(g.var() / (R * s * s / 3) - 1) < 0.02
+
+
+def test_super_replay_noiseless_equals_plain_replay_with_R_gamma():
+    """Noiseless super-learner replay with R learners == Alg. 1 replay of the same
+    events with learning rate R*gamma (R = 2: fl(2 gamma g) = fl(gamma fl(2 g))),
+    bitwise -- the super-learner is an AD-PSGD worker with batch R*M."""
+    S, d, K = 8, 257, 300
+    e, r = synth.ring(S)
+    rng = np.random.default_rng(4)
+    h = rng.uniform(0.5, 1.0, d).astype(np.float32)
+    xs = rng.uniform(-1, 1, d).astype(np.float32)
+    X0 = synth.x0_uniform(S, d, seed=9)
+    ev, _ = synth.schedule_iid(S, e, K=K, seed=10, local_prob=0.3)
+    Xs = O.super_replay(O.OracleProblem(O.MODEL_QUADRATIC, M=4, gamma=0.05, h=h, xstar=xs), X0, e, r, ev, R=2)
+    Xp, _ = O.replay(O.OracleProblem(O.MODEL_QUADRATIC, M=4, gamma=0.1, h=h, xstar=xs), X0, e, r, ev)
+    assert np.array_equal(Xs.view(np.uint32), Xp.view(np.uint32))
