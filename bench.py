@@ -533,6 +533,34 @@ def main():
                 "per_gpu_per_direction_gbs": nvb / secn / world / 1e9,
                 "frac_of_900": nvb / secn / world / 900e9,
                 "frac_of_measured_peer_copy_770": nvb / secn / world / 770e9}
+        if world > 1 and world % 2 == 0:
+            # super-learners (reading R22): R = 2 GPUs per super-learner (NCCL all-reduce of
+            # their gradients), S = world / 2 super-learners gossiping over NVLink; one learner per GPU
+            R, S = 2, world // 2
+            es, rs, wrs, _, _ = synth.super_ring(S, R)
+            csl = P.Context(es, world, d, role=rs, rank=rank, world_size=world, device=local, placement=2,
+                            worker_rank=wrs, model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH,
+                            quad_keys=(dk, nk), quad_noise_s=s, seed=1234, super_R=R, log_capacity=1 << 16)
+            csl.super_run(4, stream)
+            torch.cuda.synchronize()
+            csl.sync()
+            barrier()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            steps_sl = 20
+            ta.record(stream)
+            csl.super_run(steps_sl, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            csl.sync()
+            barrier()
+            secs = maxr(ta.elapsed_time(tb)) / 1e3
+            csl.destroy()
+            barrier()
+            extras["super_learner"] = {
+                "workload": f"S={S} super-learners x R={R} GPUs (one learner each), ring of super-learners, d={d}",
+                "super_events_per_s": S * steps_sl / secs,
+                "learner_gradients_per_s": S * R * steps_sl / secs,
+                "samples_per_s": S * R * steps_sl * M_BATCH / secs}
         if world == 1:
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
             sys.path.insert(0, os.path.join(ROOT, "tools"))

@@ -143,6 +143,10 @@ typedef struct {
   int64_t engine_fuse_wait_ns;/* a due passive waits up to this long for an active to take    */
                               /* its lock (and fuse its step) before stepping alone; 0 = never */
                               /* waits.  Scheduling only: any interleaving is an AD-PSGD run.  */
+  int32_t super_R;            /* > 1: super-learner context (adpsgd_super_run, reading R22):  */
+                              /* the graph is R copies of the super-learners' graph and only  */
+                              /* that contracted graph must be connected                      */
+  int32_t reserved2;
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its
@@ -235,6 +239,22 @@ adpsgd_status adpsgd_step(adpsgd_ctx* ctx, int32_t w, const float* grad, adpsgd_
 #define ADPSGD_REPLAY_ENGINE 2u
 adpsgd_status adpsgd_replay(adpsgd_ctx* ctx, const adpsgd_event* schedule, int64_t n_events,
                             const int32_t* batch_idx, uint32_t flags, adpsgd_stream s);
+
+/* Super-learners (reading R22): "combining learners on the same
+ * computing node as a super-learner (via NCCL AllReduce)".  Learner w lives on
+ * rank w (n == world_size, placement 2 with worker_rank[w] = w); learner (s, r)
+ * = s*R + r belongs to super-learner s, and the graph must be R copies of the
+ * super-learners' bipartite graph (learner (s, r) neighbours (s', r) only).
+ * Every rank runs n_steps iterations of its super-learner's loop: its learner
+ * gradient at its replica (quadratic, noise key 2^61 | s<<44 | c<<8 | r, c = the
+ * super-learner's gradient count), NCCL all-reduce SUM over the group; the
+ * group leader takes the passive super-learner's lock (active: a neighbour drawn
+ * uniformly; passive: its own) and the ticket k; every replica r averages with
+ * replica r of the partner over NVLink and applies x <- m - gamma g (Alg. 1
+ * order; a passive only updates); group barrier; the leader logs {k, s, j} and
+ * unlocks.  R = cfg.super_R (1 if unset).  Collective over all ranks; the
+ * replicas of a super-learner stay bitwise equal.                            */
+adpsgd_status adpsgd_super_run(adpsgd_ctx* ctx, int64_t n_steps, adpsgd_stream s);
 
 /* Free-running asynchronous AD-PSGD (the wait-free runtime of App. A,
  * P:1235-1314, realised on the device): one persistent kernel per GPU runs

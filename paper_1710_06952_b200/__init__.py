@@ -34,7 +34,7 @@ EXPORTED = ["adpsgd_abi_version", "adpsgd_last_error", "adpsgd_init", "adpsgd_de
             "adpsgd_model_device_ptr", "adpsgd_worker_rank", "adpsgd_get_ticket", "adpsgd_read_log",
             "adpsgd_read_update_counts", "adpsgd_get_stats", "adpsgd_reset_stats", "adpsgd_launch_count",
             "adpsgd_gemm_tf32x3", "adpsgd_plan_placement", "adpsgd_plan_replay", "adpsgd_dpsgd",
-            "adpsgd_dpsgd_reset", "adpsgd_dpsgd_read_model", "adpsgd_gemm_tf32x3_bench"]
+            "adpsgd_dpsgd_reset", "adpsgd_dpsgd_read_model", "adpsgd_gemm_tf32x3_bench", "adpsgd_super_run"]
 
 
 class AdpsgdError(RuntimeError):
@@ -60,7 +60,8 @@ class Config(C.Structure):
                 ("engine_variant", C.c_int32), ("log_capacity", C.c_int64),
                 ("wait_free", C.c_int32), ("reserved0", C.c_int32),
                 ("link_slow", C.c_void_p), ("link_ns", C.c_int64),
-                ("engine_no_fuse", C.c_int32), ("reserved1", C.c_int32), ("engine_fuse_wait_ns", C.c_int64)]
+                ("engine_no_fuse", C.c_int32), ("reserved1", C.c_int32), ("engine_fuse_wait_ns", C.c_int64),
+                ("super_R", C.c_int32), ("reserved2", C.c_int32)]
 
 
 class Event(C.Structure):
@@ -107,6 +108,7 @@ def lib():
             "adpsgd_dpsgd": ([P, I64, P], I32), "adpsgd_dpsgd_reset": ([P, P], I32),
             "adpsgd_dpsgd_read_model": ([P, I32, P], I32),
             "adpsgd_gemm_tf32x3_bench": ([I32, I32, I32, I32, I32, I32, P], I32),
+            "adpsgd_super_run": ([P, I64, P], I32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -192,7 +194,7 @@ class Context:
                  quad_keys=(0, 0), quad_noise_s=0.0, data_A=None, data_b=None, data_y=None,
                  mlp_dims=(0, 0, 0), x0=None, x0_per_worker=None, straggler=None, compute_ns=0,
                  engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, wait_free=0, link_slow=None, link_ns=0,
-                 engine_fuse=True, engine_fuse_wait_ns=0, connect=True, pg=None):
+                 engine_fuse=True, engine_fuse_wait_ns=0, super_R=0, connect=True, pg=None):
         self.n, self.d, self.rank, self.world = int(n), int(d), int(rank), int(world_size)
         e = _arr(np.asarray(edges).reshape(-1, 2), np.int32)
         r = _arr(role, np.int8)
@@ -222,6 +224,7 @@ class Context:
         cfg.link_slow, cfg.link_ns = _ptr(ls), int(link_ns)
         cfg.engine_no_fuse = 0 if engine_fuse else 1
         cfg.engine_fuse_wait_ns = int(engine_fuse_wait_ns)
+        cfg.super_R = int(super_R)
         h = C.c_void_p()
         _chk(lib().adpsgd_init(C.byref(g), self.n, self.d, C.byref(cfg), C.byref(h)), "adpsgd_init")
         self._h = h
@@ -279,6 +282,10 @@ class Context:
 
     def run(self, n_updates, stream=None):
         _chk(lib().adpsgd_run(self._h, int(n_updates), _stream(stream)), "run")
+
+    def super_run(self, n_steps, stream=None):
+        """Super-learner loop (reading R22, R = super_R): collective over all ranks."""
+        _chk(lib().adpsgd_super_run(self._h, int(n_steps), _stream(stream)), "super_run")
 
     def consensus_mean(self, out_ptr, with_mk=True, stream=None):
         mk = C.c_double()

@@ -114,6 +114,12 @@ cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log
                                long long k, int i, int j, unsigned int flags, int grad,
                                cudaStream_t s);
 cudaError_t launch_set_u64(unsigned long long* p, unsigned long long v, cudaStream_t s);
+// super-learner group leader: lock + ticket, then log + unlock (reading R22)
+cudaError_t launch_super_lock(unsigned int* lock, unsigned long long* ticket, unsigned long long* kout,
+                              unsigned int* err, unsigned long long watchdog_ns, cudaStream_t s);
+cudaError_t launch_super_commit(LogEntry* log, long long log_cap, const unsigned long long* kin, int i, int j,
+                                unsigned int flags, WorkerCtl* ctl_i, unsigned long long* committed,
+                                unsigned int* lock, cudaStream_t s);
 cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, long long d,
                              long long n4, cudaStream_t s);
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t s);

@@ -298,6 +298,37 @@ __global__ void k_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log,
 
 __global__ void k_set_u64(unsigned long long* p, unsigned long long v) { *p = v; }
 
+// Super-learner (reading R22), run by the group leader: take the super-learner's
+// lock (system-scope try-lock, possibly on a peer GPU), then the ticket k
+// (rank 0's counter) while holding it; k goes to *kout for the group broadcast.
+__global__ void k_super_lock(unsigned int* lock, unsigned long long* ticket, unsigned long long* kout,
+                             unsigned int* err, unsigned long long watchdog_ns) {
+  const unsigned long long t0 = globaltimer();
+  while (atomicCAS_system(lock, 0u, 1u) != 0u) {
+    if (globaltimer() - t0 > watchdog_ns) { atomicCAS(err, 0u, 7u); *kout = ~0ull; return; }
+    __nanosleep(500);
+  }
+  __threadfence_system();
+  *kout = atomicAdd_system(ticket, 1ull);
+}
+
+// ... and after every replica of the event is written (group barrier): log
+// {k, i, j, 0, flags}, counters, release the lock.
+__global__ void k_super_commit(LogEntry* log, long long log_cap, const unsigned long long* kin, int i, int j,
+                               unsigned int flags, WorkerCtl* ctl_i, unsigned long long* committed,
+                               unsigned int* lock) {
+  const unsigned long long k = *kin;
+  if (k == ~0ull) return;                        // lock timed out (error latched)
+  const unsigned long long t = globaltimer();
+  LogEntry* e = log + (long long)(k % (unsigned long long)log_cap);
+  e->k = (long long)k; e->i = i; e->j = j; e->tau = 0; e->flags = flags; e->t0 = t; e->t1 = t;
+  if (!(flags & 1u)) atomicAdd_system(&ctl_i->updates, 1ull);
+  if (j >= 0) atomicAdd_system(&ctl_i->gossips, 1ull);
+  atomicAdd_system(committed, 1ull);
+  __threadfence_system();
+  atomicExch_system(lock, 0u);
+}
+
 template <bool P, int G>
 cudaError_t ev(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
                float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s) {
@@ -412,6 +443,19 @@ cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log
                                long long k, int i, int j, unsigned int flags, int grad,
                                cudaStream_t s) {
   k_step_commit<<<1, 1, 0, s>>>(gctl0, ctl_i, log, log_cap, k, i, j, flags, grad);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_super_lock(unsigned int* lock, unsigned long long* ticket, unsigned long long* kout,
+                              unsigned int* err, unsigned long long watchdog_ns, cudaStream_t s) {
+  k_super_lock<<<1, 1, 0, s>>>(lock, ticket, kout, err, watchdog_ns);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_super_commit(LogEntry* log, long long log_cap, const unsigned long long* kin, int i, int j,
+                                unsigned int flags, WorkerCtl* ctl_i, unsigned long long* committed,
+                                unsigned int* lock, cudaStream_t s) {
+  k_super_commit<<<1, 1, 0, s>>>(log, log_cap, kin, i, j, flags, ctl_i, committed, lock);
   return cudaGetLastError();
 }
 

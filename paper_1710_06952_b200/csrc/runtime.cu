@@ -157,6 +157,14 @@ struct adpsgd_ctx {
   std::vector<std::pair<int, int>> dp_send;       // (local worker, destination rank), ascending id
   ncclComm_t comm = nullptr;
   bool connected = false;
+  // super-learner mode (reading R22): this rank's group communicator and buffers
+  ncclComm_t super_comm = nullptr;
+  int super_R = 0;
+  float* super_g = nullptr;                        // learner gradient, then the group's sum
+  unsigned long long* super_k = nullptr;           // ticket broadcast by the group leader
+  int* super_bar = nullptr;                        // group barrier word
+  long long super_c = 0;                           // gradient events of this rank's super-learner
+  std::vector<std::vector<int>> super_nb;          // super-learner ring neighbours
   // ---- host executor state ----
   std::mutex mu;
   std::vector<cudaEvent_t> last_evt;
@@ -192,19 +200,39 @@ adpsgd_status check_graph(adpsgd_ctx* c, const adpsgd_graph* g) {
     c->nb[b].push_back(a);
   }
   for (auto& v : c->nb) std::sort(v.begin(), v.end());
-  // connectivity + 2-colouring (BFS from 0, coloured active)
+  // connectivity + 2-colouring (BFS per component, each started as active)
   std::vector<int> col(n, -1), q;
-  col[0] = 0;
-  q.push_back(0);
   bool bip = true;
-  for (size_t h = 0; h < q.size(); ++h) {
-    const int u = q[h];
-    for (int w : c->nb[u]) {
-      if (col[w] < 0) { col[w] = 1 - col[u]; q.push_back(w); }
-      else if (col[w] == col[u]) bip = false;
+  int comps = 0;
+  for (int s0 = 0; s0 < n; ++s0) {
+    if (col[s0] >= 0) continue;
+    ++comps;
+    col[s0] = 0;
+    q.assign(1, s0);
+    for (size_t h = 0; h < q.size(); ++h) {
+      const int u = q[h];
+      for (int w : c->nb[u]) {
+        if (col[w] < 0) { col[w] = 1 - col[u]; q.push_back(w); }
+        else if (col[w] == col[u]) bip = false;
+      }
     }
   }
-  if ((int)q.size() != n) return fail(ADPSGD_E_DISCONNECTED, "graph is not connected (rho = 1)");
+  if (c->super_R > 1) {
+    // super-learner context (R22): the learners' graph is R copies of the
+    // super-learners' graph; that contracted graph must be connected
+    const int R = c->super_R;
+    if (n % R) return fail(ADPSGD_E_INVALID, "super_R must divide n");
+    const int S = n / R;
+    std::vector<int> seen(S, 0), sq(1, 0);
+    seen[0] = 1;
+    for (size_t h = 0; h < sq.size(); ++h)
+      for (int r = 0; r < R; ++r)
+        for (int v : c->nb[sq[h] * R + r])
+          if (!seen[v / R]) { seen[v / R] = 1; sq.push_back(v / R); }
+    if ((int)sq.size() != S) return fail(ADPSGD_E_DISCONNECTED, "super-learner graph is not connected (rho = 1)");
+  } else if (comps != 1) {
+    return fail(ADPSGD_E_DISCONNECTED, "graph is not connected (rho = 1)");
+  }
   c->role.assign(n, 0);
   if (g->role) {
     for (int v = 0; v < n; ++v) {
@@ -697,6 +725,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   if (!c) return ADPSGD_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
+  if (c->super_comm) ncclCommDestroy(c->super_comm);
   if (c->comm) ncclCommDestroy(c->comm);
   for (size_t r = 0; r < c->peer_models.size(); ++r) {
     if ((int)r == c->rank) continue;
@@ -711,7 +740,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
-                  c->d_dp_wself, c->wf_g, c->comp_row};
+                  c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar};
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -751,6 +780,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   c->wait_free = cfg->wait_free;
+  c->super_R = cfg->super_R > 1 ? cfg->super_R : 0;
   c->engine_fuse = cfg->engine_no_fuse ? 0 : 1;
   c->fuse_wait_ns = cfg->engine_fuse_wait_ns;
   if (c->fuse_wait_ns < 0) return fail(ADPSGD_E_INVALID, "engine_fuse_wait_ns < 0");
@@ -1315,6 +1345,102 @@ adpsgd_status adpsgd_dpsgd_read_model(adpsgd_ctx* c, int32_t w, float* host_out)
     CU(cudaDeviceSynchronize());
     CU(cudaMemcpy(host_out, c->dp_x[c->dp_cur] + (long long)c->worker_local[w] * c->d_pad, sizeof(float) * c->d,
                   cudaMemcpyDeviceToHost));
+    return ADPSGD_OK;
+  })
+}
+
+// --------------------------------------------------------- super-learner --
+// P:952-956, reading R22.  Learner w lives on rank w (explicit placement); the
+// learner graph is R copies of the super-learners' graph, learner (s, r) = s*R + r.
+static adpsgd_status super_setup(adpsgd_ctx* c) {
+  const int R = c->super_R > 1 ? c->super_R : 1;
+  if (c->world % R || c->n != c->world) return fail(ADPSGD_E_INVALID, "super_run: n == world_size, super_R | world");
+  for (int w = 0; w < c->n; ++w)
+    if (c->worker_rank[w] != w) return fail(ADPSGD_E_INVALID, "super_run: learner w must live on rank w");
+  const int S = c->n / R;
+  c->super_nb.assign(S, {});
+  for (int w = 0; w < c->n; ++w) {
+    const int s = w / R, r = w % R;
+    if (c->role[w] != c->role[s * R]) return fail(ADPSGD_E_INVALID, "super_run: a super-learner's learners differ in role");
+    std::vector<int> nb;
+    for (int v : c->nb[w]) {
+      if (v % R != r) return fail(ADPSGD_E_INVALID, "super_run: learner (s, r) may only neighbour learners (s', r)");
+      nb.push_back(v / R);
+    }
+    std::sort(nb.begin(), nb.end());
+    if (r == 0) c->super_nb[s] = nb;
+    else if (nb != c->super_nb[s]) return fail(ADPSGD_E_INVALID, "super_run: learner graphs differ across r");
+  }
+  if (R > 1 && !c->super_comm) NC(ncclCommSplit(c->comm, c->rank / R, c->rank % R, &c->super_comm, nullptr));
+  if (!c->super_g) {
+    CU(cudaMalloc(&c->super_g, sizeof(float) * c->d_pad));
+    CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
+    CU(cudaMalloc(&c->super_bar, sizeof(int)));
+    CU(cudaMemset(c->super_bar, 0, sizeof(int)));
+    CU(cudaDeviceSynchronize());
+  }
+  return ADPSGD_OK;
+}
+
+static uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream strm) {
+  GUARD({
+    CTX_CHECK(c);
+    if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+    if (c->model != ADPSGD_MODEL_QUADRATIC) return fail(ADPSGD_E_UNSUPPORTED, "super_run uses the quadratic model");
+    if (n_steps < 0) return fail(ADPSGD_E_INVALID, "n_steps < 0");
+    ST(super_setup(c));
+    const int R = c->super_R > 1 ? c->super_R : 1;
+    cudaStream_t st = c->use(strm);
+    const int w = c->rank, s = w / R, r = w % R, S = c->n / R;
+    const bool active = c->role[w] == 0 && !c->super_nb[s].empty();
+    float* row = c->row(w);
+    auto ctl_of = [&](int v) { return reinterpret_cast<WorkerCtl*>(c->peer_ctl[v]) + c->worker_local[v]; };
+    auto row_of = [&](int v) { return c->peer_models[v] + (long long)c->worker_local[v] * c->d_pad; };
+    const unsigned long long watchdog = 20ull * 1000000000ull;
+    for (int64_t step = 0; step < n_steps; ++step) {
+      const long long cs = c->super_c;
+      const unsigned long long key = (1ull << 61) | ((unsigned long long)s << 44) | ((unsigned long long)cs << 8) |
+                                     (unsigned long long)r;
+      int js = -1;
+      if (active) {                     // the group's shared neighbour choice (uniform over N(s))
+        const auto& nb = c->super_nb[s];
+        js = nb[splitmix64(c->seed ^ ((uint64_t)s << 40) ^ (uint64_t)cs) % nb.size()];
+      }
+      unsigned int* lock = &ctl_of((active ? js : s) * R)->lock;   // the passive side's leader lock
+      auto gradient = [&]() -> adpsgd_status {
+        CU(launch_quad_grad(row, c->super_g, c->d, c->n4, c->q, key, st));
+        if (R > 1) NC(ncclAllReduce(c->super_g, c->super_g, (size_t)c->d_pad, ncclFloat32, ncclSum, c->super_comm, st));
+        return ADPSGD_OK;
+      };
+      auto lock_and_share_k = [&]() -> adpsgd_status {
+        if (r == 0) CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, watchdog, st));
+        if (R > 1) NC(ncclBroadcast(c->super_k, c->super_k, 1, ncclUint64, 0, c->super_comm, st));
+        return ADPSGD_OK;
+      };
+      if (active) {                     // gradient first: x_s changes only through s's own events
+        ST(gradient());
+        ST(lock_and_share_k());
+        CU(launch_event(row, row_of(js * R + r), c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st));
+      } else {                          // a passive reads its model under its own lock
+        ST(lock_and_share_k());
+        ST(gradient());
+        CU(launch_event(row, nullptr, c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st));
+      }
+      if (R > 1) NC(ncclAllReduce(c->super_bar, c->super_bar, 1, ncclInt32, ncclSum, c->super_comm, st));
+      if (r == 0)
+        CU(launch_super_commit(c->log0, c->log_cap, c->super_k, s, js, 0u, ctl_of(s * R), &c->gctl0->committed, lock,
+                               st));
+      c->launches += 4;
+      c->super_c += 1;
+    }
+    c->host_k += (unsigned long long)S * (unsigned long long)n_steps;
     return ADPSGD_OK;
   })
 }

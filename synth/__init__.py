@@ -86,6 +86,17 @@ def schedule_iid(n, edges, K, T=0, seed=0, M=0, S=0, no_grad=False, tau=None,
     return ev, bidx
 
 
+def super_ring(S: int, R: int):
+    """Super-learner layout (reading R22): learner (s, r) = s*R + r on rank s*R + r;
+    the learner graph is R copies of ring(S) (learner (s, r) -- (s', r)) and a
+    learner takes its super-learner's role.  Returns (edges, roles, worker_rank,
+    super_edges, super_roles)."""
+    se, sr = ring(S)
+    e = np.array([[a * R + r, b * R + r] for a, b in se for r in range(R)], np.int32).reshape(-1, 2)
+    role = np.repeat(sr, R).astype(np.int8)
+    return e, role, np.arange(S * R, dtype=np.int32), se, sr
+
+
 def placement_xor(n: int, G: int) -> np.ndarray:
     """Worker -> GPU for a ring where EVERY edge crosses GPUs and the actives
     (even workers) are spread over all GPUs: GPU(w) = (w mod G) xor ((w div G)

@@ -1,0 +1,81 @@
+"""Super-learner parity worker (reading R22), launched by
+tests/test_multigpu.py through torch.distributed.run.  For every factorisation
+world = S * R: R learners per super-learner (NCCL all-reduce of their
+gradients), S super-learners gossiping on a bipartite ring over NVLink.  Checks
+that every super-learner's R replicas are bitwise equal and that the event log,
+replayed through the oracle's super-learner replay, reproduces them -- bitwise
+for R <= 2, within reading c11's 1e-4 for R > 2 (NCCL's own summation order)."""
+import math
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+import synth
+import paper_1710_06952_b200 as P
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    if rank == 0:
+        from oracle import oracle as O
+    fails = []
+    d, steps = (1 << 16) + 36, 60
+    dk, nk = synth.quad_keys(8)
+    s_noise = float(np.float32(0.1 * math.sqrt(96)))
+    for R in [r for r in range(1, world + 1) if world % r == 0]:
+        S = world // R
+        e, role, wr, se, sr = synth.super_ring(S, R)
+        Xs0 = synth.x0_uniform(S, d, seed=30 + R)                   # one model per super-learner
+        X0 = np.repeat(Xs0, R, axis=0)                               # identical replicas
+        ctx = P.Context(e, world, d, role=role, rank=rank, world_size=world, device=local, placement=2,
+                        worker_rank=wr, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                        quad_keys=(dk, nk), quad_noise_s=s_noise, seed=3 + R, super_R=R)
+        ctx.super_run(steps)
+        ctx.sync()
+        dist.barrier()
+        allm = [None] * world
+        dist.all_gather_object(allm, {w: ctx.read_model(w) for w in ctx.local_workers()})
+        if rank == 0:
+            X = np.zeros((world, d), np.float32)
+            for m in allm:
+                for w, x in m.items():
+                    X[w] = x
+            for s in range(S):
+                for r in range(1, R):
+                    if not np.array_equal(X[s * R].view(np.uint32), X[s * R + r].view(np.uint32)):
+                        fails.append(f"S={S} R={R}: replicas of super-learner {s} differ")
+            log = ctx.read_log(0)
+            if len(log) != S * steps or not np.array_equal(np.sort(log["k"]), np.arange(S * steps)):
+                fails.append(f"S={S} R={R}: log has {len(log)} entries")
+            else:
+                ev = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+                prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk,
+                                       noise_s=s_noise)
+                Xo = O.super_replay(prob, Xs0, se, sr, ev, R)
+                if R <= 2:      # an all-reduce of two fp32 values is one correctly rounded add
+                    if not np.array_equal(X[::R].view(np.uint32), Xo.view(np.uint32)):
+                        fails.append(f"S={S} R={R}: log replay not bit-exact")
+                else:           # NCCL's summation order is its own: reading c11's 1e-4
+                    rms = np.sqrt(np.mean(Xo.astype(np.float64) ** 2, axis=1, keepdims=True))
+                    err = np.abs(X[::R].astype(np.float64) - Xo) / np.maximum(np.abs(Xo), rms)
+                    if err.max() > 1e-4:
+                        fails.append(f"S={S} R={R}: log replay error {err.max():.2e} > 1e-4")
+                if S > 1 and not (ev[:, 1] >= 0).any():
+                    fails.append(f"S={S} R={R}: no averaging events")
+        ctx.destroy()
+        dist.barrier()
+    if rank == 0:
+        print("SUPER", "FAIL" if fails else "OK", fails, flush=True)
+    dist.destroy_process_group()
+    sys.exit(1 if (rank == 0 and fails) else 0)
+
+
+if __name__ == "__main__":
+    main()

@@ -35,3 +35,13 @@ def test_schedule_appa_is_causal():
         assert 0 <= tau <= min(k, T) and t >= last_r[i] and t > prev_k[i]
         assert (j >= 0) == (r[i] == 0)
         prev_k[i], last_k[i], last_r[i] = last_k[i], k, t
+
+
+@pytest.mark.parametrize("S,R", [(2, 2), (4, 2), (1, 4), (8, 1)])
+def test_super_ring_layout(S, R):
+    e, role, wr, se, sr = synth.super_ring(S, R)
+    assert e.shape[0] == se.shape[0] * R
+    for a, b in e:
+        assert a % R == b % R and role[a] != role[b]            # (s, r) -- (s', r), bipartite
+    assert np.array_equal(wr, np.arange(S * R))
+    assert all(role[s * R + r] == sr[s] for s in range(S) for r in range(R))
