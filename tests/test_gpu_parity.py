@@ -462,3 +462,28 @@ def test_fused_passive_steps_replay_bitwise(P):
     assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
     assert sum(ctx.update_counts().values()) == U
     ctx.destroy()
+
+
+def test_max_local_workers_free_running(P):
+    """The engine's limit of 128 workers on one GPU (config 5 at one GPU): a
+    free-running quadratic run at n = 128 replays bitwise; n = 129 is refused."""
+    n, d, U = 128, 4096 + 8, 2000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(23)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    X0 = synth.x0_uniform(n, d, seed=24)
+    ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s, compute_ns=5_000,
+                    straggler=synth.stragglers(n, hetero=True), seed=6)
+    ctx.run(U)
+    ctx.sync()
+    log = ctx.read_log(0)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, X0, e, r, log_events(log))
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    assert len({int(w) for w in log["i"]}) > 100                  # most workers made progress
+    ctx.destroy()
+    e2, r2 = synth.ring(130)
+    with pytest.raises(P.AdpsgdError) as ei:
+        P.Context(e2, 130, 64, role=r2)
+    assert ei.value.code == 12
