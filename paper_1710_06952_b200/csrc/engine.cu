@@ -418,14 +418,17 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
 }
 
 // tile x stages, fixed-mix A/B (tools/ab_engine.py, mixed / local-only GB/s):
-// 512x4 5356/4774, 1024x3 5488/5129, 1536x2 5589/5109, 2048x2 5491/5010
+// 512x4 5356/4774, 1024x3 5488/5129, 1536x2 5589/5109, 2048x2 5491/5010 (2048x2
+// needs 128 KB: one CTA per SM).  Whole bench (tools/ab_build.py + bench.py
+// --no-extras, 3 runs each): 1536x2 0.869-0.871 of the HBM peak, 1024x3
+// 0.863-0.867, 512x6 0.819-0.824.
 #ifndef ADPSGD_TILE4
-#define ADPSGD_TILE4 1024
+#define ADPSGD_TILE4 1536
 #endif
 #ifndef ADPSGD_STAGES
-#define ADPSGD_STAGES 3
+#define ADPSGD_STAGES 2
 #endif
-constexpr int kTile4 = ADPSGD_TILE4;     // float4 per stream per stage (16 KB)
+constexpr int kTile4 = ADPSGD_TILE4;     // float4 per stream per stage (24 KB)
 constexpr int kStages = ADPSGD_STAGES;
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * kStages * sizeof(uint64_t);
 
@@ -492,7 +495,11 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     for (int l = threadIdx.x; l < p.n_local; l += blockDim.x) push_seq[l] = p.served[l * kMaxGrid + blockIdx.x];
   __syncthreads();
   const int L = p.n_local;
+#ifdef ADPSGD_ROT0
+  const int rot = 0;                         // A/B: every CTA prefers the same running event
+#else
   const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
+#endif
   const long long my_tiles = EngineStager<kVar>::tiles_of(blockIdx.x, gridDim.x, p.n4);
   unsigned long long last_progress = globaltimer();
   while (true) {
