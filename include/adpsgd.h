@@ -270,7 +270,9 @@ adpsgd_status adpsgd_run(adpsgd_ctx* ctx, int64_t n_updates, adpsgd_stream s);
  * workers on all ranks (NCCL AllReduce fp64 when world > 1); mk_out (nullable)
  * receives M_k = (1/n) sum_i ||xbar - x_i||^2 (p_i = 1/n).
  * out_device: d floats on this context's device (every rank gets the result).
- * Synchronous w.r.t. the host when mk_out != NULL.                            */
+ * Synchronous w.r.t. the host when mk_out != NULL.  A non-finite model value
+ * (a diverged run) latches ADPSGD_E_DIVERGED for the next adpsgd_sync,
+ * and is returned at once when mk_out != NULL.                               */
 adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* ctx, float* out_device, double* mk_out,
                                     adpsgd_stream s);
 

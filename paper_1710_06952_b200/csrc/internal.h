@@ -102,7 +102,7 @@ cudaError_t launch_fill_hash(float* x, long long n, uint32_t seed, cudaStream_t 
 cudaError_t launch_comp_row(const float* x, const float* gp, float gamma, float* out, long long n4, cudaStream_t s);
 cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,
                                  double* sum, cudaStream_t s);
-cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out,
+cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out, unsigned int* err,
                                       cudaStream_t s);
 cudaError_t launch_consensus_mk(const float* X, int n_rows, long long d_pad, long long d,
                                 const double* sum, int n, double* acc, cudaStream_t s);

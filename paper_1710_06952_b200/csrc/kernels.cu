@@ -150,11 +150,18 @@ __global__ void k_consensus_sum(const float* __restrict__ X, int n_rows, long lo
   }
 }
 
+// x_bar = fl32(sum / n); a non-finite sum means some worker's model diverged
+// (S:289): latch ADPSGD_E_DIVERGED for the next adpsgd_sync
 __global__ void k_consensus_finalize(const double* __restrict__ sum, int n, long long d,
-                                     float* __restrict__ out) {
+                                     float* __restrict__ out, unsigned int* err) {
+  bool bad = false;
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
-       c += (long long)gridDim.x * blockDim.x)
-    out[c] = __double2float_rn(__ddiv_rn(sum[c], (double)n));
+       c += (long long)gridDim.x * blockDim.x) {
+    const double v = sum[c];
+    bad |= !isfinite(v);
+    out[c] = __double2float_rn(__ddiv_rn(v, (double)n));
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(err, 0u, 6u);
 }
 
 // M_k partial: sum over local rows and coordinates of (mean - x)^2, fp64
@@ -414,9 +421,9 @@ cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, lo
   return cudaGetLastError();
 }
 
-cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out,
+cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out, unsigned int* err,
                                       cudaStream_t s) {
-  k_consensus_finalize<<<4 * sm_count(), 256, 0, s>>>(sum, n, d, out);
+  k_consensus_finalize<<<4 * sm_count(), 256, 0, s>>>(sum, n, d, out, err);
   return cudaGetLastError();
 }
 

@@ -1155,7 +1155,7 @@ adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, a
     CU(launch_consensus_sum(c->models, c->n_local, c->d_pad, c->d, c->sum64, st));
     ++c->launches;
     if (c->world > 1) NC(ncclAllReduce(c->sum64, c->sum64, (size_t)c->d, ncclFloat64, ncclSum, c->comm, st));
-    CU(launch_consensus_finalize(c->sum64, c->n, c->d, out, st));
+    CU(launch_consensus_finalize(c->sum64, c->n, c->d, out, &c->gctl->error, st));
     ++c->launches;
     if (mk_out) {
       CU(cudaMemsetAsync(c->mk_acc, 0, sizeof(double), st));
@@ -1165,6 +1165,12 @@ adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, a
       double acc = 0.0;
       CU(cudaMemcpyAsync(&acc, c->mk_acc, sizeof(double), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
+      if (!std::isfinite(acc)) {
+        char buf[96];
+        snprintf(buf, sizeof buf, "non-finite model value at the consensus after event %llu (S:289)",
+                 (unsigned long long)c->host_k);
+        return fail(ADPSGD_E_DIVERGED, buf);
+      }
       *mk_out = acc / (double)c->n;
     }
     return ADPSGD_OK;

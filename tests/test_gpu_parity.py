@@ -487,3 +487,28 @@ def test_max_local_workers_free_running(P):
     with pytest.raises(P.AdpsgdError) as ei:
         P.Context(e2, 130, 64, role=r2)
     assert ei.value.code == 12
+
+
+def test_divergence_is_reported(P):
+    """a diverging run (gamma * M * h_max far above 2) is reported as
+    ADPSGD_E_DIVERGED by the consensus output and the next sync -- as the oracle
+    reports it for the same schedule."""
+    n, d = 4, 1000
+    e, r = synth.ring(n)
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=50.0, batch_M=32, quad_keys=(1, 2),
+                    quad_noise_s=1.0, compute_ns=0)
+    ctx.run(400)
+    out = torch_out(d)
+    with pytest.raises(P.AdpsgdError) as ei:
+        ctx.consensus_mean(out.data_ptr(), with_mk=True)
+    assert ei.value.code == 6
+    with pytest.raises(P.AdpsgdError) as ei:
+        ctx.sync()
+    assert ei.value.code == 6
+    ctx.sync()                                                   # the latch is cleared once reported
+    ctx.destroy()
+    ev, _ = synth.schedule_iid(n, e, K=400, seed=1)
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=50.0, data_key=1, noise_key=2, noise_s=1.0)
+    with pytest.raises(O.OracleError) as eo:
+        O.replay(prob, np.zeros((n, d), np.float32), e, r, ev)
+    assert eo.value.code == 6
