@@ -38,7 +38,11 @@ struct alignas(128) WorkerCtl {
   unsigned int wf_buf;             // which of the worker's two gradient rows is the buffer
   unsigned int wf_comp_cur;        // current gradient was compensated
   unsigned int wf_comp_pub;        // buffered gradient was compensated
-  unsigned int pad[12];
+  // cooperative cross-GPU event (engine): a peer that holds this worker's lock
+  // posts its event here so this GPU's CTAs process half of its tiles
+  unsigned int guest_tag;          // (event seq << 2) | state, written by the initiator (release.sys)
+  int guest_i;                     // initiating worker (its slot holds the event)
+  unsigned int pad[10];
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
 
@@ -65,6 +69,8 @@ struct LogEntry {                  // == adpsgd_log_entry
   unsigned long long t0, t1;
 };
 
+struct Slot;                       // engine slot (internal.h)
+
 // Per-worker descriptor, one table per process: pointers valid in THIS process
 // (local device memory or IPC-mapped peer memory reached over NVLink).
 struct WorkerDesc {
@@ -79,6 +85,7 @@ struct WorkerDesc {
   int local;                       // index among this rank's workers, -1 if remote
   float* gb;                       // App. A: two gradient rows (2 * d_pad), local workers only
   float link;                      // link slowdown L_w >= 1 (emulated slow network, R21)
+  Slot* slot;                      // the worker's engine slot (home GPU's control arena; peer-mapped)
 };
 
 // --------------------------------------------------------------- hashing ----

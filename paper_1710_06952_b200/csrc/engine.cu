@@ -41,6 +41,7 @@ constexpr int kEngineThreads = 512;
 constexpr int kEngineUnroll = 2;
 constexpr int kExit = -2;
 constexpr int kPickPush = 1 << 20;      // pick codes >= kPickPush: push request of local worker
+constexpr int kPickGuest = kPickPush - 1; // a peer's cooperative event posted in a local mailbox
 
 struct SmemSlot {                  // tid 0 copies the running event here for the CTA
   float* xi;
@@ -63,6 +64,15 @@ struct SmemSlot {                  // tid 0 copies the running event here for th
   const float* g;
   float* gout;
   int absorb;                      // fused passive local step (event k-1) before the pair
+  // tile split and arrival: own events use (blockIdx, grid) or, when
+  // cooperative, (blockIdx, 2 grid); a guest (a peer's cooperative event) uses
+  // (grid + blockIdx, 2 grid) and arrives on the initiator's slot
+  long long first, step;
+  int coop;
+  int guest;
+  int gl;                          // local worker whose mailbox carried the guest event
+  unsigned int* gdone;             // initiator's slot->done (peer)
+  unsigned int* gready;            // initiator's slot->commit_ready (peer)
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -91,6 +101,20 @@ __device__ __forceinline__ bool take_ticket(const EngineParams& p, unsigned long
 __device__ void publish_running(Slot* sl, unsigned int seq) {
   __threadfence();                                   // fields before the tag
   st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
+}
+
+// Cooperative cross-GPU event: after publishing event seq+1 in worker w's slot,
+// post it in partner j's guest mailbox (j's home GPU) so that GPU's CTAs take
+// half of the tiles -- both GPUs then drive NVLink (reads of the other row and
+// writes of the results in both directions) instead of one.
+// The mailbox has its own sequence (a partner serves events of several
+// initiators, whose slot sequences may coincide); the poster holds the partner
+// exclusively (its lock or its epoch), so read-increment is race-free.
+__device__ void post_guest(const EngineParams& p, Slot* sl, int w, int j) {
+  WorkerCtl* cj = p.workers[j].ctl;                   // peer memory
+  __threadfence_system();                             // the slot's fields, system-wide
+  *(volatile int*)&cj->guest_i = w;
+  st_release_sys(&cj->guest_tag, tag_of(sl->gseq, kStateRunning));
 }
 
 // cross-GPU event (two-sided): ask j's home GPU to push x_j into our landing row
@@ -149,6 +173,7 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
     cw->wf_comp_cur = comp ? 1u : 0u;
     sl->kind = kKindPull;
     sl->absorb = -1;
+    sl->coop = 0;
     sl->i = w; sl->j = -1; sl->tau = 0; sl->flags = 0u; sl->k = -1;
     sl->key = read_key(t, w);
     sl->xi = dw.x; sl->xj = nullptr;
@@ -186,6 +211,7 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
   }
   sl->kind = kKindEvent;
   sl->absorb = -1;
+  sl->coop = 0;
   sl->i = w; sl->j = j; sl->k = (long long)k; sl->key = k;
   sl->tau = flush ? (int)(k - cw->wf_tread_pub) : 0;
   sl->flags = flush ? (2u | (cw->wf_comp_pub ? 4u : 0u)) : 1u;
@@ -256,10 +282,14 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
     sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
     if (sl->cross && p.two_sided) post_push_request(p, sl, w, e.j, seq);
+    sl->coop = sl->cross && p.coop;
+    sl->commit_ready = 0u;
+    if (sl->coop) sl->gseq = (ld_acquire_sys(&p.workers[e.j].ctl->guest_tag) >> 2) + 1u;
     sl->ev_cur = cur + 1;
     sl->t0 = now;
     sl->done = 0;
     publish_running(sl, seq);
+    if (sl->coop) post_guest(p, sl, w, e.j);
     return true;
   }
   // ------------------------------------------------------- free-running ----
@@ -332,11 +362,15 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
   sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
   sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
   if (sl->cross && p.two_sided) post_push_request(p, sl, w, j, seq);
+  sl->coop = sl->cross && p.coop;
+  sl->commit_ready = 0u;
+  if (sl->coop) sl->gseq = (ld_acquire_sys(&p.workers[j].ctl->guest_tag) >> 2) + 1u;
   sl->pending_j = -2;
   sl->nb_ctr += 1;
   sl->t0 = now;
   sl->done = 0;
   publish_running(sl, seq);
+  if (sl->coop) post_guest(p, sl, w, j);
   return true;
 }
 
@@ -412,6 +446,10 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     // App. A runtime the communication thread never waits for it
     sl->ready_ns = now + hold + (p.wait_free ? 0ull : (unsigned long long)((double)sw * (double)p.compute_ns));
   }
+  if (sl->coop) {                        // every tile of both GPUs is done: clear the partner's mailbox
+    st_release_sys(&p.workers[j].ctl->guest_tag, tag_of(sl->gseq, kStateIdle));
+    sl->coop = 0;
+  }
   atomicAdd_system(&p.gctl0->committed, 1ull);
   const unsigned int seq = sl->tag >> 2;
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
@@ -451,8 +489,7 @@ __device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, 
       stg.template run_range<kPair, kGrad, kFF>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
                                                 gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk, g4);
     else
-      stg.template run<kPair, kGrad, kFF, kPreJ>(xi4, xj4, blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q, kk, g4,
-                                                 kkj);
+      stg.template run<kPair, kGrad, kFF, kPreJ>(xi4, xj4, e.first, e.step, p.n4, p.d, p.gamma, p.q, kk, g4, kkj);
   } else {
     const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
     const long long lo = (long long)blockIdx.x * per;
@@ -469,6 +506,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
   __shared__ unsigned int push_seq[kMaxLocal];   // last push request seq this CTA served, per worker
   __shared__ unsigned int cons_seq[kMaxLocal];   // event seq cons_cnt refers to
   __shared__ unsigned int cons_cnt[kMaxLocal];   // tiles of a cross event consumed so far
+  __shared__ unsigned int gdone_seq[kMaxLocal];  // last guest event seq this CTA finished, per mailbox
   __shared__ int s_pick;
   __shared__ unsigned int s_seq;
   __shared__ SmemSlot s_ev;
@@ -488,6 +526,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     done_seq[s] = 0u;
     cons_seq[s] = 0u;
     cons_cnt[s] = 0u;
+    gdone_seq[s] = 0u;
     push_seq[s] = 0xffffffffu;
   }
   __syncthreads();
@@ -526,6 +565,13 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
       for (int t = 0; t < L && pick == -1; ++t) {
         const int s = (t + rot) % L;
         const unsigned int tag = ld_acquire_gpu(&p.slots[s].tag);
+        if (p.coop && (tag & 3u) == kStateRunning && *(volatile int*)&p.slots[s].coop) {
+          const unsigned int g = *(volatile unsigned int*)&p.slots[s].gseq;
+          if (ld_acquire_sys(&p.slots[s].commit_ready) == g && atomicCAS(&p.slots[s].commit_ready, g, 0u) == g) {
+            commit(p, s);                                   // last arrival was on the partner GPU
+            continue;
+          }
+        }
         if ((tag & 3u) != kStateRunning || (tag >> 2) == done_seq[s]) continue;
         Slot* sl = p.slots + s;
         const int cross = *(volatile int*)&sl->cross;
@@ -560,7 +606,45 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.cross = cross;
         s_ev.t0 = t0;
         s_ev.t1 = t1;
+        s_ev.coop = *(volatile int*)&sl->coop;
+        s_ev.first = blockIdx.x;
+        s_ev.step = s_ev.coop ? 2ll * gridDim.x : (long long)gridDim.x;
+        s_ev.guest = 0;
       }
+      // 2b. cooperative events of peer GPUs posted in our workers' mailboxes
+      if (p.coop)
+        for (int t = 0; t < L && pick == -1; ++t) {
+          const int l = (t + rot) % L;
+          const int wl = p.local_ids[l];
+          WorkerCtl* cl = p.workers[wl].ctl;
+          const unsigned int gt = ld_acquire_sys(&cl->guest_tag);
+          if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
+          const int gi = *(volatile int*)&cl->guest_i;
+          Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
+          const unsigned int fl = *(volatile unsigned int*)&sa->flags;
+          s_ev.xi = p.workers[gi].x;
+          s_ev.xj = p.workers[wl].x;
+          s_ev.k = *(volatile long long*)&sa->k;
+          s_ev.key = *(volatile unsigned long long*)&sa->key;
+          s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+          s_ev.ff = (fl & 2u) ? 1 : 0;
+          s_ev.kind = kKindEvent;
+          s_ev.g = nullptr;
+          s_ev.gout = nullptr;
+          s_ev.absorb = 0;
+          s_ev.pair = 1;
+          s_ev.cross = 1;
+          s_ev.t0 = s_ev.t1 = 0;
+          s_ev.coop = 1;
+          s_ev.first = (long long)gridDim.x + blockIdx.x;
+          s_ev.step = 2ll * gridDim.x;
+          s_ev.guest = 1;
+          s_ev.gl = l;
+          s_ev.gdone = &sa->done;
+          s_ev.gready = &sa->commit_ready;
+          s_seq = gt >> 2;
+          pick = kPickGuest;
+        }
       // 3. scheduler duty
       if (pick == -1) {
         const unsigned long long now = globaltimer();
@@ -575,7 +659,8 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         }
         // local work done; with cross-GPU partners stay to serve push requests
         // until every event of the run is committed system-wide
-        if (n_fin == L && (!p.two_sided || ld_relaxed_sys64(&p.gctl0->committed) >= p.target)) pick = kExit;
+        if (n_fin == L && (!(p.two_sided || p.coop) || ld_relaxed_sys64(&p.gctl0->committed) >= p.target))
+          pick = kExit;
         if (progress) last_progress = now;
         else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
       } else {
@@ -621,14 +706,22 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           cons_cnt[pick] = (unsigned int)e.t1;
           finished = e.t1 >= my_tiles;
         }
-        if (finished) {
+        if (finished && e.guest) {          // our half of a peer's cooperative event
+          gdone_seq[e.gl] = s_seq;
+          __threadfence_system();
+          if (atomicAdd_system(e.gdone, 1u) == 2u * gridDim.x - 1u) st_release_sys(e.gready, s_seq);
+        } else if (finished) {
           done_seq[pick] = s_seq;
           // this CTA's slice is visible before its arrival; P2P stores need the
           // system-scope fence, local ones only gpu scope (the committing CTA
           // issues fence.sys before the cross-GPU release, which is cumulative)
           if (e.cross) __threadfence_system();
           else __threadfence();
-          if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) commit(p, pick);
+          if (e.coop) {
+            if (atomicAdd_system(&p.slots[pick].done, 1u) == 2u * gridDim.x - 1u) commit(p, pick);
+          } else if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) {
+            commit(p, pick);
+          }
         }
       }
     } else if (threadIdx.x == 0) {

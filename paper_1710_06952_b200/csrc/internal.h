@@ -40,6 +40,9 @@ struct Slot {                      // per local worker, in local device memory
   unsigned int* held_lock;
   unsigned long long unlock_at;
   int absorb;                      // slot of a passive whose local step (event k-1) is fused into this pair, -1 none
+  int coop;                        // cross event processed by both GPUs (2 x grid CTAs arrive on `done`)
+  unsigned int commit_ready;       // mailbox seq of a coop event whose last arrival was on the partner GPU
+  unsigned int gseq;               // the partner mailbox's sequence for this coop event
 };
 constexpr int kKindEvent = 0, kKindPull = 1;
 
@@ -80,6 +83,7 @@ struct EngineParams {
   long long link_ns;               // nominal model-transfer time of a 1x link (R21)
   int fuse;                        // fuse a due passive local step into the pair that holds its lock
   unsigned long long fuse_wait_ns; // a due passive stays absorbable this long before stepping alone
+  int coop;                        // cooperative cross-GPU events (both GPUs process the tiles)
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);

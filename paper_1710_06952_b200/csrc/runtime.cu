@@ -57,7 +57,7 @@ struct PeerBlob {
   uint32_t magic, version;
   int32_t rank, n_local;
   int64_t d_pad;
-  int64_t gctl_offset, log_offset, log_cap, pcnt_offset;
+  int64_t gctl_offset, log_offset, log_cap, pcnt_offset, slots_offset;
   int32_t has_land, engine_grid;
   cudaIpcMemHandle_t models, ctl, land;
 };
@@ -85,6 +85,7 @@ struct adpsgd_ctx {
   int engine_cps = 0, engine_threads = 512, engine_variant = 0;
   int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
   int engine_fuse = 1;               // fuse due passive steps into pair passes
+  int engine_coop = 1;               // cooperative cross-GPU events
   long long fuse_wait_ns = 0;        // how long a due passive stays absorbable
   std::vector<float> link;           // link slowdown per worker (reading R21)
   long long link_ns = 0;
@@ -104,11 +105,12 @@ struct adpsgd_ctx {
   cudaStream_t stream = nullptr;
   float* models = nullptr;
   char* ctl_arena = nullptr;
-  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0, pcnt_offset = 0;
+  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0, pcnt_offset = 0, slots_offset = 0;
   float* land = nullptr;             // landing rows [n_local][d_pad] (world > 1)
   unsigned int* served = nullptr;    // [n_local][kMaxGrid] push requests served per CTA
   std::vector<float*> peer_land;
   std::vector<size_t> peer_pcnt_off;
+  std::vector<size_t> peer_slots_off;
   int engine_grid = 0;
   WorkerCtl* ctl = nullptr;
   GlobalCtl* gctl = nullptr;
@@ -285,6 +287,7 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
     x.local = r == c->rank ? c->worker_local[w] : -1;
     x.gb = (r == c->rank && c->wf_g) ? c->wf_g + l * 2 * c->d_pad : nullptr;
     x.link = c->link[w];
+    x.slot = c->peer_ctl[r] ? reinterpret_cast<Slot*>(c->peer_ctl[r] + c->peer_slots_off[r]) + l : nullptr;
   }
   CU(cudaMemcpy(c->d_workers, wd.data(), sizeof(WorkerDesc) * c->n, cudaMemcpyHostToDevice));
   CU(cudaDeviceSynchronize());   // pageable H2D may still be in flight; kernels use non-blocking streams
@@ -611,12 +614,17 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.link_ns = c->link_ns;
   p.fuse = c->engine_fuse;
   p.fuse_wait_ns = (unsigned long long)c->fuse_wait_ns;
+  // cooperative cross-GPU events: the partner GPU's CTAs take half of the tiles
+  // (same grid on every rank, checked at import); not with the register-slice
+  // variant, the two-sided protocol, or the wait-free loop (its gradient rows
+  // are not peer-mapped)
+  p.coop = (c->world > 1 && c->engine_coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
   const int grid = cps * dev_sms;
   // the two-sided protocol pairs CTA b of both GPUs tile by tile: same grid everywhere
-  if (p.two_sided && c->engine_grid && grid != c->engine_grid)
+  if ((p.two_sided || p.coop) && c->engine_grid && grid != c->engine_grid)
     return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (two-sided NVLink protocol)");
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
   CU(launch_engine(p, grid, c->engine_threads, s));
@@ -736,7 +744,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
   for (auto e : c->evring) if (e) cudaEventDestroy(e);
   for (auto st : c->pool) if (st) cudaStreamDestroy(st);
-  void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids, c->d_slots,
+  void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids,
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
@@ -782,6 +790,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->wait_free = cfg->wait_free;
   c->super_R = cfg->super_R > 1 ? cfg->super_R : 0;
   c->engine_fuse = cfg->engine_no_fuse ? 0 : 1;
+  c->engine_coop = cfg->engine_no_coop ? 0 : 1;
   c->fuse_wait_ns = cfg->engine_fuse_wait_ns;
   if (c->fuse_wait_ns < 0) return fail(ADPSGD_E_INVALID, "engine_fuse_wait_ns < 0");
   if (c->wait_free < 0 || c->wait_free > 2) return fail(ADPSGD_E_INVALID, "wait_free must be 0, 1 or 2");
@@ -847,10 +856,12 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     CU(cudaDeviceSynchronize());
     CU(launch_init_rows(c->models, c->n_local, c->d_pad, c->d, c->dx0, c->stream));
   }
-  // control arena: WorkerCtl[n_local] | GlobalCtl | push counters [n_local][kMaxGrid] | (rank 0) log
+  // control arena (peer-mapped): WorkerCtl[n_local] | GlobalCtl | push counters [n_local][kMaxGrid] |
+  // engine Slots[n_local] | (rank 0) log
   c->gctl_offset = sizeof(WorkerCtl) * std::max(1, c->n_local);
   c->pcnt_offset = c->gctl_offset + sizeof(GlobalCtl);
-  c->log_offset = c->pcnt_offset + sizeof(unsigned int) * kMaxGrid * std::max(1, c->n_local);
+  c->slots_offset = c->pcnt_offset + sizeof(unsigned int) * kMaxGrid * std::max(1, c->n_local);
+  c->log_offset = (c->slots_offset + sizeof(Slot) * std::max(1, c->n_local) + 255) / 256 * 256;
   c->ctl_bytes = c->log_offset + (c->rank == 0 ? sizeof(LogEntry) * c->log_cap : 0);
   CU(cudaMalloc(&c->ctl_arena, c->ctl_bytes));
   CU(cudaMemset(c->ctl_arena, 0, c->ctl_bytes));
@@ -881,8 +892,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   CU(cudaMalloc(&c->d_local_ids, sizeof(int) * std::max(1, c->n_local)));
   if (c->n_local)
     CU(cudaMemcpy(c->d_local_ids, c->local_ids.data(), sizeof(int) * c->n_local, cudaMemcpyHostToDevice));
-  CU(cudaMalloc(&c->d_slots, sizeof(Slot) * std::max(1, c->n_local)));
-  CU(cudaMemset(c->d_slots, 0, sizeof(Slot) * std::max(1, c->n_local)));
+  c->d_slots = reinterpret_cast<Slot*>(c->ctl_arena + c->slots_offset);   // zeroed with the arena
   if (c->wait_free && c->n_local) {          // App. A gradient rows: buffer + computing gradient
     CU(cudaMalloc(&c->wf_g, sizeof(float) * 2 * c->d_pad * c->n_local));
     CU(cudaMemset(c->wf_g, 0, sizeof(float) * 2 * c->d_pad * c->n_local));
@@ -893,6 +903,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->peer_ctl.assign(c->world, nullptr);
   c->peer_land.assign(c->world, nullptr);
   c->peer_pcnt_off.assign(c->world, 0);
+  c->peer_slots_off.assign(c->world, 0);
   c->peer_imported.assign(c->world, false);
   if (c->world > 1 && c->n_local) {          // two-sided NVLink protocol state
     CU(cudaMalloc(&c->land, sizeof(float) * c->d_pad * c->n_local));
@@ -910,6 +921,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->peer_ctl[c->rank] = c->ctl_arena;
   c->peer_land[c->rank] = c->land;
   c->peer_pcnt_off[c->rank] = c->pcnt_offset;
+  c->peer_slots_off[c->rank] = c->slots_offset;
   c->peer_imported[c->rank] = true;
   c->last_evt.assign(c->n, nullptr);
   for (auto& e : c->last_evt) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
@@ -972,6 +984,7 @@ adpsgd_status adpsgd_export_peer_info(adpsgd_ctx* c, void* buf, int64_t cap, int
     b.log_offset = (int64_t)c->log_offset;
     b.log_cap = c->log_cap;
     b.pcnt_offset = (int64_t)c->pcnt_offset;
+    b.slots_offset = (int64_t)c->slots_offset;
     b.engine_grid = c->engine_grid;
     CU(cudaIpcGetMemHandle(&b.models, c->models));
     CU(cudaIpcGetMemHandle(&b.ctl, c->ctl_arena));
@@ -1004,6 +1017,7 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
     c->peer_models[rank] = static_cast<float*>(pm);
     c->peer_ctl[rank] = static_cast<char*>(pc);
     c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
+    c->peer_slots_off[rank] = (size_t)b.slots_offset;
     if (b.engine_grid != c->engine_grid)
       return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (different GPU models?)");
     if (b.has_land) {

@@ -25,6 +25,7 @@ ap.add_argument("--model", default="none")
 ap.add_argument("--mode", default="replay", choices=["replay", "run"])
 ap.add_argument("--wpg", type=int, default=8, help="workers per GPU")
 ap.add_argument("--placement", default="interleave", choices=["interleave", "xor"])
+ap.add_argument("--coop", type=int, default=1, help="cooperative cross-GPU events (both GPUs process tiles)")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -36,7 +37,7 @@ ev, _ = synth.schedule_iid(n, e, K=a.events, seed=2, no_grad=not quad)
 for v in [int(x) for x in a.variants.split(",")]:
     xor = a.placement == "xor"
     ctx = P.Context(e, n, a.d, role=r, rank=rank, world_size=world, device=local, placement=2 if xor else 1,
-                    worker_rank=synth.placement_xor(n, world) if xor else None,
+                    worker_rank=synth.placement_xor(n, world) if xor else None, engine_coop=bool(a.coop),
                     model=P.MODEL_QUADRATIC if quad else P.MODEL_NONE, gamma=0.01, batch_M=32,
                     quad_keys=(1, 2), quad_noise_s=0.5, engine_variant=v)
     s = torch.cuda.Stream()
@@ -57,7 +58,7 @@ for v in [int(x) for x in a.variants.split(",")]:
     cross = len(ev)
     nvl = cross * 8.0 * a.d / world / (ms / 1e3) / 1e9
     if rank == 0:
-        print(f"{a.mode} {a.placement} wpg={a.wpg} variant {v}: {len(ev)} cross events in {ms:.2f} ms -> {len(ev) / (ms / 1e3):.0f} events/s, "
+        print(f"{a.mode} {a.placement} wpg={a.wpg} coop={a.coop} variant {v}: {len(ev)} cross events in {ms:.2f} ms -> {len(ev) / (ms / 1e3):.0f} events/s, "
               f"NVLink {nvl:.0f} GB/s per GPU per direction", flush=True)
     ctx.destroy()
     dist.barrier()
