@@ -51,6 +51,7 @@ def parse():
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--topology", default="ring", choices=["ring", "skip"])
     ap.add_argument("--no-fuse", action="store_true", help="never fuse a due passive step into a pair pass")
+    ap.add_argument("--coop", type=int, default=0, help="cooperative cross-GPU events: 0 auto, 1 on, -1 off")
     return ap.parse_args()
 
 
@@ -241,7 +242,7 @@ def main():
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                          quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
                          engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free,
-                         engine_fuse=not a.no_fuse)
+                         engine_fuse=not a.no_fuse, engine_coop=None if a.coop == 0 else a.coop > 0)
 
     stream = torch.cuda.Stream()
     out = torch.empty(d, dtype=torch.float32, device="cuda")

@@ -146,9 +146,10 @@ typedef struct {
   int32_t super_R;            /* > 1: super-learner context (adpsgd_super_run, reading R22):  */
                               /* the graph is R copies of the super-learners' graph and only  */
                               /* that contracted graph must be connected                      */
-  int32_t engine_no_coop;     /* 0 (default, world > 1): a cross-GPU pair event is processed  */
-                              /* by BOTH GPUs' engines (half of the tiles each), so both      */
-                              /* drive NVLink; 1: only the initiator's GPU (one-sided)        */
+  int32_t engine_coop;        /* cooperative cross-GPU events (world > 1): both GPUs' engines */
+                              /* process half of a cross event's tiles, so both drive NVLink. */
+                              /* 0 = auto (on when the GPUs start cross events unevenly, e.g. */
+                              /* all actives on some GPUs, or world == 2), 1 = on, -1 = off    */
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its

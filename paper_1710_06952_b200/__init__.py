@@ -61,7 +61,7 @@ class Config(C.Structure):
                 ("wait_free", C.c_int32), ("reserved0", C.c_int32),
                 ("link_slow", C.c_void_p), ("link_ns", C.c_int64),
                 ("engine_no_fuse", C.c_int32), ("reserved1", C.c_int32), ("engine_fuse_wait_ns", C.c_int64),
-                ("super_R", C.c_int32), ("engine_no_coop", C.c_int32)]
+                ("super_R", C.c_int32), ("engine_coop", C.c_int32)]
 
 
 class Event(C.Structure):
@@ -194,7 +194,7 @@ class Context:
                  quad_keys=(0, 0), quad_noise_s=0.0, data_A=None, data_b=None, data_y=None,
                  mlp_dims=(0, 0, 0), x0=None, x0_per_worker=None, straggler=None, compute_ns=0,
                  engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, wait_free=0, link_slow=None, link_ns=0,
-                 engine_fuse=True, engine_fuse_wait_ns=0, super_R=0, engine_coop=True, connect=True,
+                 engine_fuse=True, engine_fuse_wait_ns=0, super_R=0, engine_coop=None, connect=True,
                  pg=None):
         self.n, self.d, self.rank, self.world = int(n), int(d), int(rank), int(world_size)
         e = _arr(np.asarray(edges).reshape(-1, 2), np.int32)
@@ -226,7 +226,7 @@ class Context:
         cfg.engine_no_fuse = 0 if engine_fuse else 1
         cfg.engine_fuse_wait_ns = int(engine_fuse_wait_ns)
         cfg.super_R = int(super_R)
-        cfg.engine_no_coop = 0 if engine_coop else 1
+        cfg.engine_coop = 0 if engine_coop is None else (1 if engine_coop else -1)   # None = auto
         h = C.c_void_p()
         _chk(lib().adpsgd_init(C.byref(g), self.n, self.d, C.byref(cfg), C.byref(h)), "adpsgd_init")
         self._h = h

@@ -425,6 +425,13 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   atomicAdd(&p.gctl->st_bytes, ((j >= 0 ? 4.0 : (grad ? 2.0 : 0.0)) + (sl->g && grad ? 1.0 : 0.0)) * d4);
   atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
   __threadfence_system();                 // log + data before the release below
+  if (sl->coop) {
+    // every tile of both GPUs is done: clear the partner's mailbox BEFORE the
+    // partner is released (epoch / lock), or the next initiator's post -- maybe
+    // from another GPU -- could be overwritten by this clear
+    st_release_sys(&p.workers[j].ctl->guest_tag, tag_of(sl->gseq, kStateIdle));
+    sl->coop = 0;
+  }
   if (p.mode == 1) {
     atomicAdd_system(&sl->ctl_i->epoch, 1u);
     if (j >= 0) atomicAdd_system(&sl->ctl_j->epoch, 1u);
@@ -445,10 +452,6 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     // Alg. 1 loop: the next gradient is computed before the next event; in the
     // App. A runtime the communication thread never waits for it
     sl->ready_ns = now + hold + (p.wait_free ? 0ull : (unsigned long long)((double)sw * (double)p.compute_ns));
-  }
-  if (sl->coop) {                        // every tile of both GPUs is done: clear the partner's mailbox
-    st_release_sys(&p.workers[j].ctl->guest_tag, tag_of(sl->gseq, kStateIdle));
-    sl->coop = 0;
   }
   atomicAdd_system(&p.gctl0->committed, 1ull);
   const unsigned int seq = sl->tag >> 2;

@@ -85,7 +85,7 @@ struct adpsgd_ctx {
   int engine_cps = 0, engine_threads = 512, engine_variant = 0;
   int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
   int engine_fuse = 1;               // fuse due passive steps into pair passes
-  int engine_coop = 1;               // cooperative cross-GPU events
+  int engine_coop = 0;               // cooperative cross-GPU events: 0 auto, 1 on, -1 off
   long long fuse_wait_ns = 0;        // how long a due passive stays absorbable
   std::vector<float> link;           // link slowdown per worker (reading R21)
   long long link_ns = 0;
@@ -618,7 +618,24 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   // (same grid on every rank, checked at import); not with the register-slice
   // variant, the two-sided protocol, or the wait-free loop (its gradient rows
   // are not peer-mapped)
-  p.coop = (c->world > 1 && c->engine_coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
+  bool coop = c->engine_coop > 0;
+  if (c->engine_coop == 0 && c->world > 1) {
+    // auto: on at two GPUs (measured: N=2 all-cross 455 -> 624 GB/s free-running,
+    // 599 -> 644 replay) or when some GPU starts fewer than half the cross events
+    // another one starts (free-running: only actives start events); off for an
+    // even split at more GPUs (N=4 xor placement: 535 -> 457, the partner's own
+    // queue delays each event's second half)
+    std::vector<int> init(c->world, 0);
+    for (size_t e = 0; e + 1 < c->edges.size(); e += 2) {
+      const int a = c->edges[e], b = c->edges[e + 1];
+      if (c->worker_rank[a] == c->worker_rank[b]) continue;
+      const int act = c->role[a] == 0 ? a : b;
+      init[c->worker_rank[act]]++;
+    }
+    const int mx = *std::max_element(init.begin(), init.end()), mn = *std::min_element(init.begin(), init.end());
+    coop = c->world == 2 || (mode == 0 && mx > 2 * mn);
+  }
+  p.coop = (c->world > 1 && coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
@@ -790,7 +807,8 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->wait_free = cfg->wait_free;
   c->super_R = cfg->super_R > 1 ? cfg->super_R : 0;
   c->engine_fuse = cfg->engine_no_fuse ? 0 : 1;
-  c->engine_coop = cfg->engine_no_coop ? 0 : 1;
+  c->engine_coop = cfg->engine_coop;
+  if (c->engine_coop < -1 || c->engine_coop > 1) return fail(ADPSGD_E_INVALID, "engine_coop must be -1, 0 or 1");
   c->fuse_wait_ns = cfg->engine_fuse_wait_ns;
   if (c->fuse_wait_ns < 0) return fail(ADPSGD_E_INVALID, "engine_fuse_wait_ns < 0");
   if (c->wait_free < 0 || c->wait_free > 2) return fail(ADPSGD_E_INVALID, "wait_free must be 0, 1 or 2");

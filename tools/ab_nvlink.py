@@ -25,7 +25,7 @@ ap.add_argument("--model", default="none")
 ap.add_argument("--mode", default="replay", choices=["replay", "run"])
 ap.add_argument("--wpg", type=int, default=8, help="workers per GPU")
 ap.add_argument("--placement", default="interleave", choices=["interleave", "xor"])
-ap.add_argument("--coop", type=int, default=1, help="cooperative cross-GPU events (both GPUs process tiles)")
+ap.add_argument("--coop", type=int, default=0, help="cooperative cross-GPU events: 0 auto, 1 on, -1 off")
 a = ap.parse_args()
 rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
 torch.cuda.set_device(local)
@@ -37,7 +37,7 @@ ev, _ = synth.schedule_iid(n, e, K=a.events, seed=2, no_grad=not quad)
 for v in [int(x) for x in a.variants.split(",")]:
     xor = a.placement == "xor"
     ctx = P.Context(e, n, a.d, role=r, rank=rank, world_size=world, device=local, placement=2 if xor else 1,
-                    worker_rank=synth.placement_xor(n, world) if xor else None, engine_coop=bool(a.coop),
+                    worker_rank=synth.placement_xor(n, world) if xor else None, engine_coop=None if a.coop == 0 else a.coop > 0,
                     model=P.MODEL_QUADRATIC if quad else P.MODEL_NONE, gamma=0.01, batch_M=32,
                     quad_keys=(1, 2), quad_noise_s=0.5, engine_variant=v)
     s = torch.cuda.Stream()
