@@ -564,6 +564,45 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
             pick = kPickPush + l;
           }
         }
+      auto scan_guests = [&]() {
+        // 2b. cooperative events of peer GPUs posted in our workers' mailboxes
+        if (p.coop)
+          for (int t = 0; t < L && pick == -1; ++t) {
+            const int l = (t + rot) % L;
+            const int wl = p.local_ids[l];
+            WorkerCtl* cl = p.workers[wl].ctl;
+            const unsigned int gt = ld_acquire_sys(&cl->guest_tag);
+            if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
+            const int gi = *(volatile int*)&cl->guest_i;
+            Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
+            const unsigned int fl = *(volatile unsigned int*)&sa->flags;
+            s_ev.xi = p.workers[gi].x;
+            s_ev.xj = p.workers[wl].x;
+            s_ev.k = *(volatile long long*)&sa->k;
+            s_ev.key = *(volatile unsigned long long*)&sa->key;
+            s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+            s_ev.ff = (fl & 2u) ? 1 : 0;
+            s_ev.kind = kKindEvent;
+            s_ev.g = nullptr;
+            s_ev.gout = nullptr;
+            s_ev.absorb = 0;
+            s_ev.pair = 1;
+            s_ev.cross = 1;
+            s_ev.t0 = s_ev.t1 = 0;
+            s_ev.coop = 1;
+            s_ev.first = (long long)gridDim.x + blockIdx.x;
+            s_ev.step = 2ll * gridDim.x;
+            s_ev.guest = 1;
+            s_ev.gl = l;
+            s_ev.gdone = &sa->done;
+            s_ev.gready = &sa->commit_ready;
+            s_seq = gt >> 2;
+            pick = kPickGuest;
+          }
+      };
+#ifdef ADPSGD_GUEST_FIRST
+      scan_guests();
+#endif
       // 2. running events with work for this CTA
       for (int t = 0; t < L && pick == -1; ++t) {
         const int s = (t + rot) % L;
@@ -614,40 +653,9 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.step = s_ev.coop ? 2ll * gridDim.x : (long long)gridDim.x;
         s_ev.guest = 0;
       }
-      // 2b. cooperative events of peer GPUs posted in our workers' mailboxes
-      if (p.coop)
-        for (int t = 0; t < L && pick == -1; ++t) {
-          const int l = (t + rot) % L;
-          const int wl = p.local_ids[l];
-          WorkerCtl* cl = p.workers[wl].ctl;
-          const unsigned int gt = ld_acquire_sys(&cl->guest_tag);
-          if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
-          const int gi = *(volatile int*)&cl->guest_i;
-          Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
-          const unsigned int fl = *(volatile unsigned int*)&sa->flags;
-          s_ev.xi = p.workers[gi].x;
-          s_ev.xj = p.workers[wl].x;
-          s_ev.k = *(volatile long long*)&sa->k;
-          s_ev.key = *(volatile unsigned long long*)&sa->key;
-          s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
-          s_ev.ff = (fl & 2u) ? 1 : 0;
-          s_ev.kind = kKindEvent;
-          s_ev.g = nullptr;
-          s_ev.gout = nullptr;
-          s_ev.absorb = 0;
-          s_ev.pair = 1;
-          s_ev.cross = 1;
-          s_ev.t0 = s_ev.t1 = 0;
-          s_ev.coop = 1;
-          s_ev.first = (long long)gridDim.x + blockIdx.x;
-          s_ev.step = 2ll * gridDim.x;
-          s_ev.guest = 1;
-          s_ev.gl = l;
-          s_ev.gdone = &sa->done;
-          s_ev.gready = &sa->commit_ready;
-          s_seq = gt >> 2;
-          pick = kPickGuest;
-        }
+#ifndef ADPSGD_GUEST_FIRST
+      scan_guests();
+#endif
       // 3. scheduler duty
       if (pick == -1) {
         const unsigned long long now = globaltimer();
