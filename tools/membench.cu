@@ -289,8 +289,55 @@ int ring_main(int G) {
   return 0;
 }
 
+// G GPUs at once, every GPU pair-averaging with ALL other GPUs concurrently
+// (one stream and 1/(G-1) of the SMs per peer): the traffic pattern of the
+// xor placement, where a GPU's cross events go to several peers
+int mesh_main(int G) {
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  if (ndev < G || G < 3) { printf("mesh: need >= 3 GPUs\n"); return 0; }
+  const long long d = 25600000, n4 = d / 4;
+  constexpr int T = 1024, S = 3;
+  size_t smem = (size_t)S * 2 * T * 16 + 64;
+  std::vector<float4*> x(G), y(G);                      // x: row pulled by peers, y: this GPU's own rows
+  std::vector<std::vector<cudaStream_t>> st(G, std::vector<cudaStream_t>(G));
+  for (int g = 0; g < G; ++g) {
+    CK(cudaSetDevice(g));
+    for (int h = 0; h < G; ++h) if (h != g) cudaDeviceEnablePeerAccess(h, 0);
+    CK(cudaMalloc(&x[g], d * 4)); CK(cudaMemset(x[g], 0, d * 4));
+    CK(cudaMalloc(&y[g], d * 4 * (G - 1))); CK(cudaMemset(y[g], 0, d * 4 * (G - 1)));
+    for (int h = 0; h < G; ++h) CK(cudaStreamCreate(&st[g][h]));
+    cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  }
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  const long long part = n4 / (G - 1);                  // each peer pair moves 1/(G-1) of a row
+  auto all = [&] {
+    for (int g = 0; g < G; ++g) {
+      cudaSetDevice(g);
+      int q = 0;
+      for (int h = 0; h < G; ++h) {
+        if (h == g) continue;
+        avg_tma<T, S, false, true><<<2 * sms / (G - 1), 512, smem, st[g][h]>>>(y[g] + q * part, x[h] + q * part, part, 1);
+        ++q;
+      }
+    }
+  };
+  auto sync = [&] { for (int g = 0; g < G; ++g) { cudaSetDevice(g); cudaDeviceSynchronize(); } };
+  all(); sync();
+  const int it = 20;
+  auto t0 = std::chrono::steady_clock::now();
+  for (int r = 0; r < it; ++r) all();
+  sync();
+  double s = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / it;
+  // per GPU per direction: its reads of peers' rows + its written averages, 8 bytes per pair element
+  printf("mesh of %d GPUs, pair avg with every other GPU's row, tma T1024 S3 + stg %8.1f us %7.0f GB/s per GPU per direction\n",
+         G, s * 1e6, 8.0 * (double)part * 4 * (G - 1) / s / 1e9);
+  return 0;
+}
+
 int main(int argc, char** argv) {
   if (argc > 2 && !strcmp(argv[1], "ring")) return ring_main(atoi(argv[2]));
+  if (argc > 2 && !strcmp(argv[1], "mesh")) return mesh_main(atoi(argv[2]));
   if (argc > 1) return peer_main();
   const long long d = 25600000, n4 = d / 4;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
