@@ -148,8 +148,10 @@ typedef struct {
                               /* that contracted graph must be connected                      */
   int32_t engine_coop;        /* cooperative cross-GPU events (world > 1): both GPUs' engines */
                               /* process half of a cross event's tiles, so both drive NVLink. */
-                              /* 0 = auto (on when the GPUs start cross events unevenly, e.g. */
-                              /* all actives on some GPUs, or world == 2), 1 = on, -1 = off    */
+                              /* 0 = auto (on at world 2, when at most half the edges cross,  */
+                              /* or when GPUs start cross events unevenly; off when nearly     */
+                              /* every edge crosses with initiators spread evenly), 1 = on,    */
+                              /* -1 = off                                                      */
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its

@@ -621,19 +621,24 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   bool coop = c->engine_coop > 0;
   if (c->engine_coop == 0 && c->world > 1) {
     // auto: on at two GPUs (measured: N=2 all-cross 455 -> 624 GB/s free-running,
-    // 599 -> 644 replay) or when some GPU starts fewer than half the cross events
-    // another one starts (free-running: only actives start events); off for an
-    // even split at more GPUs (N=4 xor placement: 535 -> 457, the partner's own
-    // queue delays each event's second half)
+    // 599 -> 644 replay; bench block placement +1.8%), when at most half of the
+    // edges cross GPUs (bench at N=4, block placement: +1.9%), or when some GPU
+    // starts fewer than half the cross events another one starts (free-running:
+    // only actives start events).  Off when nearly every edge crosses and the
+    // initiators are spread evenly (N=4 xor placement: 535 -> 457 GB/s, every
+    // event then waits for its second half queued behind the partner's own work).
     std::vector<int> init(c->world, 0);
+    int cross = 0;
     for (size_t e = 0; e + 1 < c->edges.size(); e += 2) {
       const int a = c->edges[e], b = c->edges[e + 1];
       if (c->worker_rank[a] == c->worker_rank[b]) continue;
+      ++cross;
       const int act = c->role[a] == 0 ? a : b;
       init[c->worker_rank[act]]++;
     }
     const int mx = *std::max_element(init.begin(), init.end()), mn = *std::min_element(init.begin(), init.end());
-    coop = c->world == 2 || (mode == 0 && mx > 2 * mn);
+    const bool few_cross = 2 * (size_t)cross <= c->edges.size() / 2;
+    coop = c->world == 2 || few_cross || (mode == 0 && mx > 2 * mn);
   }
   p.coop = (c->world > 1 && coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
