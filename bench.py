@@ -201,6 +201,71 @@ def mlp_leg(P, synth, torch, events=64):
             "algorithmic_tflops": flops * events / sec / 1e12, "kernel_launches": launches}
 
 
+def config1_leg(P, synth, torch, K=2000):
+    """Config 1 (BASELINE configs[0]): least squares, n = 4 ring, d = 1024, M = 32,
+    T = 4, a seeded 2000-event replay with explicit batches.  Latency-bound
+    (4 KB rows): us/event of the HOST executor (gradient + event kernels) next to
+    the launch floor -- the same schedule as pure averaging (one 4 KB pass per
+    event)."""
+    n, d, M, T, S = 4, 1024, 32, 4, 8192
+    e, r = synth.ring(n)
+    A, b = synth.lsq_data(S=S, d=d, seed=1)
+    ev, bi = synth.schedule_iid(n, e, K=K, T=T, M=M, S=S, seed=42)
+    evg = ev.copy()
+    evg[:, 2], evg[:, 3] = 0, 1
+    out = {}
+    for name, sched, kw in (("lsq", ev, dict(model=P.MODEL_LSQ, data_A=A, data_b=b)), ("averaging_only", evg, {})):
+        ctx = P.Context(e, n, d, role=r, T=T, gamma=0.5, batch_M=M, **kw)
+        ctx.replay(sched[:100], batch_idx=bi[:100] if name == "lsq" else None)
+        ctx.sync()
+        s = torch.cuda.Stream()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0 = ctx.launch_count()
+        t0.record(s)
+        ctx.replay(sched, batch_idx=bi if name == "lsq" else None, stream=s)
+        t1.record(s)
+        torch.cuda.synchronize()
+        sec = t0.elapsed_time(t1) / 1e3
+        out[name] = {"us_per_event": 1e6 * sec / K, "events_per_s": K / sec,
+                     "kernel_launches_per_event": (ctx.launch_count() - l0) / K}
+        ctx.destroy()
+    out["workload"] = f"config1: lsq n={n} ring, d={d}, M={M}, T={T}, {K}-event seeded replay (HOST executor)"
+    return out
+
+
+def config2_leg(P, synth, torch, K=4000):
+    """Config 2 (BASELINE configs[1]): pure gossip, n = 16 bipartite ring, d = 2^20,
+    a 4000-event iid schedule: the persistent engine's replay (one launch; the
+    64 MiB working set is L2-resident, so bytes/s can exceed HBM), the HOST
+    executor's replay, and free-running gossip (actives initiate)."""
+    n, d = 16, 1 << 20
+    e, r = synth.ring(n)
+    X0 = synth.x0_uniform(n, d, seed=100)
+    ev, _ = synth.schedule_iid(n, e, K=K, seed=0, no_grad=True)
+    out = {}
+    for name in ("engine_replay", "host_replay", "free_running"):
+        ctx = P.Context(e, n, d, role=r, x0_per_worker=X0, log_capacity=1 << 14)
+        go = (lambda st: ctx.replay(ev, flags=P.REPLAY_ENGINE, stream=st)) if name == "engine_replay" else \
+            (lambda st: ctx.replay(ev, flags=P.REPLAY_HOST, stream=st)) if name == "host_replay" else \
+            (lambda st: ctx.run(K, stream=st))
+        s = torch.cuda.Stream()
+        go(s)
+        torch.cuda.synchronize()
+        ctx.sync()
+        t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        t0.record(s)
+        go(s)
+        t1.record(s)
+        torch.cuda.synchronize()
+        ctx.sync()
+        sec = t0.elapsed_time(t1) / 1e3
+        out[name] = {"gossip_steps_per_s": K / sec, "us_per_event": 1e6 * sec / K,
+                     "algorithmic_gbs": K * 16.0 * d / sec / 1e9}
+        ctx.destroy()
+    out["workload"] = f"config2: pure gossip n={n} ring, d={d}, {K} iid events (64 MiB working set, L2-resident)"
+    return out
+
+
 # ---------------------------------------------------------------- our arm --
 def main():
     a = parse()
@@ -563,6 +628,8 @@ def main():
                 "learner_gradients_per_s": S * R * steps_sl / secs,
                 "samples_per_s": S * R * steps_sl * M_BATCH / secs}
         if world == 1:
+            extras["config1_lsq"] = config1_leg(P, synth, torch)
+            extras["config2_gossip"] = config2_leg(P, synth, torch)
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
             sys.path.insert(0, os.path.join(ROOT, "tools"))
             import gemm_sweep

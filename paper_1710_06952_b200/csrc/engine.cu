@@ -68,6 +68,7 @@ struct SmemSlot {                  // tid 0 copies the running event here for th
   // cooperative, (blockIdx, 2 grid); a guest (a peer's cooperative event) uses
   // (grid + blockIdx, 2 grid) and arrives on the initiator's slot
   long long first, step;
+  int ncta;                        // CTAs that arrive on the event's counter
   int coop;
   int guest;
   int gl;                          // local worker whose mailbox carried the guest event
@@ -543,6 +544,15 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
   const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
 #endif
   const long long my_tiles = EngineStager<kVar>::tiles_of(blockIdx.x, gridDim.x, p.n4);
+  // An event of fewer tiles than CTAs (small d) is taken by `part` CTAs only,
+  // rotated by the slot index so that concurrent small events use disjoint CTAs;
+  // the others neither pick it up nor arrive on its counter.
+#ifndef ADPSGD_MIN_TILES_PER_CTA
+#define ADPSGD_MIN_TILES_PER_CTA 4   // config 2 A/B (d = 2^20): 1 -> 79k, 2 -> 91k, 4 -> 96k, 8 -> 92k replay events/s
+#endif
+  const int tiles_ev = (int)((p.n4 + kTile4 - 1) / kTile4);
+  const int want = (tiles_ev + ADPSGD_MIN_TILES_PER_CTA - 1) / ADPSGD_MIN_TILES_PER_CTA;
+  const int part = (kVar == 1 || want >= (int)gridDim.x) ? (int)gridDim.x : (want > 0 ? want : 1);
   unsigned long long last_progress = globaltimer();
   while (true) {
     if (threadIdx.x == 0) {
@@ -616,6 +626,14 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         }
         if ((tag & 3u) != kStateRunning || (tag >> 2) == done_seq[s]) continue;
         Slot* sl = p.slots + s;
+        int rb = (int)blockIdx.x;
+        const bool small = part < (int)gridDim.x && !*(volatile int*)&sl->coop &&
+                           !(p.two_sided && *(volatile int*)&sl->cross);
+        if (small) {
+          const int base = (int)(((unsigned int)s * (unsigned int)part) % gridDim.x);
+          rb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
+          if (rb >= part) { done_seq[s] = tag >> 2; continue; }   // not one of this event's CTAs
+        }
         const int cross = *(volatile int*)&sl->cross;
         long long t0 = 0, t1 = 0;
         if (cross && p.two_sided && kVar != 1) {
@@ -649,8 +667,9 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.t0 = t0;
         s_ev.t1 = t1;
         s_ev.coop = *(volatile int*)&sl->coop;
-        s_ev.first = blockIdx.x;
-        s_ev.step = s_ev.coop ? 2ll * gridDim.x : (long long)gridDim.x;
+        s_ev.first = rb;
+        s_ev.step = s_ev.coop ? 2ll * gridDim.x : (small ? (long long)part : (long long)gridDim.x);
+        s_ev.ncta = s_ev.coop ? 2 * (int)gridDim.x : (small ? part : (int)gridDim.x);
         s_ev.guest = 0;
       }
 #ifndef ADPSGD_GUEST_FIRST
@@ -694,7 +713,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
       if (e.kind == kKindPull) {
         if (kVar != 1)
           stg.pull(reinterpret_cast<const float4*>(e.xi), reinterpret_cast<const float4*>(e.g),
-                   reinterpret_cast<float4*>(e.gout), blockIdx.x, gridDim.x, p.n4, p.d, p.gamma, p.q,
+                   reinterpret_cast<float4*>(e.gout), e.first, e.step, p.n4, p.d, p.gamma, p.q,
                    quad_event_key_h(p.q.noise_key, e.key));
       } else if (kVar != 1 && e.g) {        // App. A flush of the buffered gradient (staged variants)
         if (e.pair) slice<kVar, true, kGradExternal, true>(p, e, stg);
@@ -730,7 +749,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           else __threadfence();
           if (e.coop) {
             if (atomicAdd_system(&p.slots[pick].done, 1u) == 2u * gridDim.x - 1u) commit(p, pick);
-          } else if (atomicAdd(&p.slots[pick].done, 1u) == gridDim.x - 1) {
+          } else if (atomicAdd(&p.slots[pick].done, 1u) == (unsigned int)e.ncta - 1u) {
             commit(p, pick);
           }
         }
