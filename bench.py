@@ -655,7 +655,9 @@ def main():
         # every byte that crosses NVLink leaves one GPU: per-GPU egress = total / world
         "nvlink": {"algorithmic_bytes_per_s": nvl_bytes / sec, "per_gpu_per_direction_gbs":
                    nvl_bytes / sec / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / max(world, 1) / 900e9,
-                   "frac_of_measured_peer_copy_770": nvl_bytes / sec / max(world, 1) / 770e9},
+                   "frac_of_measured_peer_copy_770": nvl_bytes / sec / max(world, 1) / 770e9,
+                   "note": "this workload's block placement: one ring edge per GPU boundary crosses NVLink; "
+                           "the all-cross figure is under all_cross (extras.nvlink_stress)"},
         "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_per_launch(loc_bytes / a.steps),
                      "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,
@@ -668,6 +670,10 @@ def main():
         "update_counts_rank0": cnts,
     }
     line.update(extras)
+    if "nvlink_stress" in extras:           # the fused kernel's NVLink fraction when every pair crosses GPUs
+        ns = extras["nvlink_stress"]
+        line["nvlink"]["all_cross"] = {"per_gpu_per_direction_gbs": ns["per_gpu_per_direction_gbs"],
+                                       "frac_of_900": ns["frac_of_900"], "workload": ns["workload"]}
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:
