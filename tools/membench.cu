@@ -121,6 +121,69 @@ __global__ void avg_tma(float4* xi, float4* xj, long long n4, int pair) {
   if (BULKST && threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+// warp-specialised variant: warp 15 only issues the bulk copies (waiting on
+// per-stage "empty" barriers the 15 consumer warps arrive on); consumers wait
+// on "full", copy the stage to registers, release it, compute and store.  No
+// CTA-wide barrier in the loop.  Interleaved tiles across CTAs (engine layout).
+template <int TILE4, int S>
+__global__ void __launch_bounds__(512) avg_ws(float4* xi, float4* xj, long long n4, int pair) {
+  constexpr int kCons = 480, kPer = TILE4 / kCons;
+  static_assert(TILE4 % kCons == 0, "tile must be a multiple of the consumer count");
+  extern __shared__ __align__(128) unsigned char sm[];
+  float4* buf = (float4*)sm;
+  uint64_t* full = (uint64_t*)(sm + (size_t)S * 2 * TILE4 * 16);
+  uint64_t* empty = full + S;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(smem_u32(full + s)));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" :: "r"(smem_u32(empty + s)), "r"(kCons / 32));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const long long tot_t = (n4 + TILE4 - 1) / TILE4;
+  const long long nt = tot_t > blockIdx.x ? (tot_t - blockIdx.x + gridDim.x - 1) / gridDim.x : 0;
+  auto wait = [](uint64_t* b, uint32_t ph) {
+    uint32_t ok;
+    do { asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }" : "=r"(ok) : "r"(smem_u32(b)), "r"(ph) : "memory"); } while (!ok);
+  };
+  if (threadIdx.x >= kCons) {                              // producer warp
+    if (threadIdx.x == kCons) {
+      for (long long t = 0; t < nt; ++t) {
+        const int s = t % S;
+        if (t >= S) wait(empty + s, ((t / S) - 1) & 1);
+        const long long base = (blockIdx.x + t * gridDim.x) * TILE4;
+        const uint32_t bytes = (uint32_t)min((long long)TILE4, n4 - base) * 16;
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(smem_u32(full + s)), "r"(pair ? 2 * bytes : bytes) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(smem_u32(buf + (size_t)s * 2 * TILE4)), "l"(xi + base), "r"(bytes), "r"(smem_u32(full + s)) : "memory");
+        if (pair) asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" :: "r"(smem_u32(buf + (size_t)s * 2 * TILE4 + TILE4)), "l"(xj + base), "r"(bytes), "r"(smem_u32(full + s)) : "memory");
+      }
+    }
+    return;
+  }
+  for (long long t = 0; t < nt; ++t) {
+    const int s = t % S;
+    wait(full + s, (t / S) & 1);
+    const float4* sa = buf + (size_t)s * 2 * TILE4;
+    const float4* sb = sa + TILE4;
+    const long long base = (blockIdx.x + t * gridDim.x) * TILE4;
+    float4 a[kPer], b[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) { a[u] = sa[u * kCons + threadIdx.x]; if (pair) b[u] = sb[u * kCons + threadIdx.x]; }
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" :: "r"(smem_u32(empty + s)) : "memory");
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const long long i = base + u * kCons + threadIdx.x;
+      if (i < n4) {
+        float4 m = a[u];
+        if (pair) { m.x = (a[u].x + b[u].x) * 0.5f; m.y = (a[u].y + b[u].y) * 0.5f; m.z = (a[u].z + b[u].z) * 0.5f; m.w = (a[u].w + b[u].w) * 0.5f; __stcg(xj + i, m); } else m.x += 1.f;
+        __stcg(xi + i, m);
+      }
+    }
+  }
+}
+
 int sms;
 #define RUN2(name, launch, bytes) { float ms = timeit([&] { launch; }, it); CK(cudaGetLastError()); printf("%-48s %8.1f us %7.0f GB/s\n", name, ms * 1e3, (bytes) / (ms / 1e3) / 1e9); }
 
@@ -335,7 +398,48 @@ int mesh_main(int G) {
   return 0;
 }
 
+// CTA-barrier TMA staging (the engine's variant 0) vs warp-specialised staging
+int ws_main() {
+  const long long d = 25600000, n4 = d / 4;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+  float4 *xi, *xj;
+  CK(cudaMalloc(&xi, d * 4)); CK(cudaMalloc(&xj, d * 4));
+  CK(cudaMemset(xi, 0, d * 4)); CK(cudaMemset(xj, 0, d * 4));
+  const int it = 30;
+  for (int pair = 0; pair <= 1; ++pair) {
+    const double bytes = (pair ? 16.0 : 8.0) * d;
+    printf("=== %s ===\n", pair ? "pair average 2R2W" : "local update 1R1W");
+#define RUN3(name, launch) { float ms = timeit([&] { launch; }, it); CK(cudaGetLastError()); printf("%-48s %8.1f us %7.0f GB/s\n", name, ms * 1e3, bytes / (ms / 1e3) / 1e9); }
+    {
+      constexpr int T = 1536, S = 2;
+      size_t smem = (size_t)S * 2 * T * 16 + 256;
+      cudaFuncSetAttribute(avg_tma<T, S, false, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN3("IL tma T1536 S2, CTA barrier (engine v0)", (avg_tma<T, S, false, true><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 1440, S = 2;
+      size_t smem = (size_t)S * 2 * T * 16 + 256;
+      cudaFuncSetAttribute(avg_ws<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN3("IL warp-specialised T1440 S2", (avg_ws<T, S><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 960, S = 3;
+      size_t smem = (size_t)S * 2 * T * 16 + 256;
+      cudaFuncSetAttribute(avg_ws<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN3("IL warp-specialised T960 S3", (avg_ws<T, S><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+    {
+      constexpr int T = 480, S = 6;
+      size_t smem = (size_t)S * 2 * T * 16 + 256;
+      cudaFuncSetAttribute(avg_ws<T, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      RUN3("IL warp-specialised T480 S6", (avg_ws<T, S><<<sms * 2, 512, smem>>>(xi, xj, n4, pair)));
+    }
+  }
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc > 1 && !strcmp(argv[1], "ws")) return ws_main();
   if (argc > 2 && !strcmp(argv[1], "ring")) return ring_main(atoi(argv[2]));
   if (argc > 2 && !strcmp(argv[1], "mesh")) return mesh_main(atoi(argv[2]));
   if (argc > 1) return peer_main();
