@@ -235,7 +235,7 @@ adpsgd_status adpsgd_step(adpsgd_ctx* ctx, int32_t w, const float* grad, adpsgd_
 /* Deterministic replay of a schedule (events k = k0 .. k0+n_events-1, where k0
  * is the current ticket).  Result is bitwise independent of interleaving.
  * batch_idx: n_events*M sample indices (host), or NULL for device Philox
- * sampling (idx = (u32*S)>>32, u32 = Philox4x32-10(key=seed, ctr=(k, m, BATCH, 0))).
+ *  sampling (idx = (u32*S)>>32, u32 = Philox4x32-10(key=seed, ctr=(lo32(k), m, BATCH, hi32(k)))).
  * flags: 0 = auto, ADPSGD_REPLAY_HOST = stream-ordered per-event kernels (all
  * models, any tau <= T; world 1), ADPSGD_REPLAY_ENGINE = the persistent NVLink
  * engine with device epoch flags (models NONE/QUADRATIC, tau = 0; any world;

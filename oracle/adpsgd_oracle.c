@@ -207,11 +207,12 @@ double oracle_quadratic_loss(const oracle_problem* p, int64_t d, const float* x)
   return f;
 }
 
-/* device-mode batch index: idx = (u32 * S) >> 32, u32 = Philox(key, (k, m, BATCH, 0)).out0
- * (sampling with replacement)                                          */
+/* device-mode batch index: idx = (u32 * S) >> 32, u32 = Philox(key, (lo32(k), m, BATCH,
+ * hi32(k))).out0 (sampling with replacement).  hi32(k) = 0 for every event index
+ * k < 2^32; it separates the keys of App. A reads (R20) and super-learners (R22). */
 #define ORC_STREAM_BATCH 0x42415443u
-static int32_t batch_index(const oracle_problem* p, uint32_t k, uint32_t m) {
-  uint32_t ctr[4] = {k, m, ORC_STREAM_BATCH, 0u}, out[4];
+static int32_t batch_index(const oracle_problem* p, uint64_t k, uint32_t m) {
+  uint32_t ctr[4] = {(uint32_t)k, m, ORC_STREAM_BATCH, (uint32_t)(k >> 32)}, out[4];
   oracle_philox4x32_10(ctr, p->batch_key, out);
   return (int32_t)(((uint64_t)out[0] * (uint64_t)(uint32_t)p->S) >> 32);
 }
@@ -329,7 +330,7 @@ int oracle_gradient(const oracle_problem* p, int64_t d, const float* xhat, uint6
   int32_t* idx = (int32_t*)malloc(sizeof(int32_t) * (size_t)p->M);
   if (!idx) return ORC_E_OOM;
   for (int32_t m = 0; m < p->M; ++m)
-    idx[m] = idx_in ? idx_in[m] : batch_index(p, (uint32_t)k, (uint32_t)m);
+    idx[m] = idx_in ? idx_in[m] : batch_index(p, k, (uint32_t)m);
   int st;
   if (p->kind == ORC_MODEL_LSQ) st = lsq_grad(p, d, xhat, idx, g);
   else if (p->kind == ORC_MODEL_LOGREG) st = logreg_grad(p, d, xhat, idx, g);
@@ -614,13 +615,15 @@ uint64_t oracle_super_key(int32_t s, int64_t c, int32_t r) {
 
 int oracle_super_gradient(const oracle_problem* p, int64_t d, const float* x, int32_t s, int64_t c, int32_t R,
                           float* g) {
-  if (!p || !x || !g || R < 1 || p->kind != ORC_MODEL_QUADRATIC) return ORC_E_INVALID;
+  if (!p || !x || !g || R < 1 || p->kind == ORC_MODEL_NONE) return ORC_E_INVALID;
   double* acc = (double*)calloc((size_t)d, sizeof(double));
   float* gr = (float*)malloc(sizeof(float) * (size_t)d);
   if (!acc || !gr) { free(acc); free(gr); return ORC_E_OOM; }
   int st = ORC_OK;
+  /* any built-in model: learner r's minibatch (Philox indices for lsq / logreg /
+     mlp, noise for the quadratic) is drawn with key(s, c, r) */
   for (int32_t r = 0; r < R && st == ORC_OK; ++r) {
-    st = oracle_quadratic_grad(p, d, x, oracle_super_key(s, c, r), gr);
+    st = oracle_gradient(p, d, x, oracle_super_key(s, c, r), NULL, gr, NULL);
     for (int64_t e = 0; e < d; ++e) acc[e] += (double)gr[e];
   }
   for (int64_t e = 0; e < d; ++e) g[e] = (float)acc[e];

@@ -75,7 +75,7 @@ constexpr int kLinThreads = 256;
 constexpr int kMaxM = 1024;
 
 __device__ __forceinline__ int32_t batch_index(uint2 key, unsigned long long k, uint32_t m, int S) {
-  const uint4 o = philox4x32_10(make_uint4((uint32_t)k, m, 0x42415443u, 0u), key);
+  const uint4 o = philox4x32_10(make_uint4((uint32_t)k, m, 0x42415443u, (uint32_t)(k >> 32)), key);
   return (int32_t)(((unsigned long long)o.x * (unsigned long long)(uint32_t)S) >> 32);
 }
 

@@ -11,12 +11,12 @@ namespace adp {
 
 namespace {
 
-// batch indices: explicit, or Philox4x32-10(key = seed, ctr = (k, m, "BATC", 0)) (shared with lsq/logreg)
+// batch indices: explicit, or Philox4x32-10(key = seed, ctr = (lo32(k), m, "BATC", hi32(k))) (as lsq/logreg)
 __global__ void k_mlp_idx(const int* __restrict__ idx_in, int M, uint2 key, unsigned long long k, int S,
                           int* __restrict__ idx) {
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < M; m += gridDim.x * blockDim.x) {
     if (idx_in) { idx[m] = idx_in[m]; continue; }
-    const uint4 o = philox4x32_10(make_uint4((uint32_t)k, (uint32_t)m, 0x42415443u, 0u), key);
+    const uint4 o = philox4x32_10(make_uint4((uint32_t)k, (uint32_t)m, 0x42415443u, (uint32_t)(k >> 32)), key);
     idx[m] = (int)(((unsigned long long)o.x * (unsigned long long)(uint32_t)S) >> 32);
   }
 }

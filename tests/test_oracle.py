@@ -593,3 +593,23 @@ def test_super_replay_noiseless_equals_plain_replay_with_R_gamma():
     Xs = O.super_replay(O.OracleProblem(O.MODEL_QUADRATIC, M=4, gamma=0.05, h=h, xstar=xs), X0, e, r, ev, R=2)
     Xp, _ = O.replay(O.OracleProblem(O.MODEL_QUADRATIC, M=4, gamma=0.1, h=h, xstar=xs), X0, e, r, ev)
     assert np.array_equal(Xs.view(np.uint32), Xp.view(np.uint32))
+
+
+def test_super_gradient_any_model_and_distinct_batches():
+    """Super-learner gradients for a sampled model (lsq, device Philox batches):
+    (a) with every sample identical, each learner's minibatch gradient is the
+    same closed form, so the sum over R learners is exactly R times it;
+    (b) with distinct samples, two super-learners at the same count draw
+    different minibatches (the key's high word enters the Philox counter)."""
+    d, S, M = 64, 512, 8
+    a = np.random.default_rng(1).standard_normal(d).astype(np.float32) / 8
+    A = np.tile(a, (S, 1))
+    b = np.full(S, 0.25, np.float32)
+    p = O.OracleProblem(O.MODEL_LSQ, M=M, gamma=0.1, A=A, b=b, batch_key=(3, 4))
+    x = np.random.default_rng(2).standard_normal(d).astype(np.float32) / 4
+    g1 = O.gradient(p, x, k=0)
+    for R in (1, 2, 4):
+        assert np.array_equal(O.super_gradient(p, x, s=1, c=5, R=R), (np.float32(R) * g1).astype(np.float32))
+    A2, b2 = synth.lsq_data(S=S, d=d, seed=3)
+    p2 = O.OracleProblem(O.MODEL_LSQ, M=M, gamma=0.1, A=A2, b=b2, batch_key=(3, 4))
+    assert not np.array_equal(O.super_gradient(p2, x, s=0, c=7, R=1), O.super_gradient(p2, x, s=1, c=7, R=1))
