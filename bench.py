@@ -632,6 +632,35 @@ def main():
                 "super_events_per_s": S * steps_sl / secs,
                 "learner_gradients_per_s": S * R * steps_sl / secs,
                 "samples_per_s": S * R * steps_sl * M_BATCH / secs}
+        if world > 1:
+            # config 3 as stated (n workers, one per B200): the tcgen05 MLP 3072 -> 512 -> 10, M = 128,
+            # free-running through the host-driven per-GPU loop (super-learners with R = 1, R22)
+            I, H, O_, Mm = 3072, 512, 10, 128
+            Xd, yd = synth.mlp_data(S=8192, n_in=I, n_out=O_, s=0.02, seed=3)
+            w0 = synth.mlp_init(I, H, O_, seed=4)
+            e3, r3, wr3, _, _ = synth.super_ring(world, 1)
+            c3m = P.Context(e3, world, w0.size, role=r3, rank=rank, world_size=world, device=local, placement=2,
+                            worker_rank=wr3, model=P.MODEL_MLP, gamma=0.002, batch_M=Mm, data_A=Xd, data_y=yd,
+                            mlp_dims=(I, H, O_), x0=w0, seed=99, super_R=1, log_capacity=1 << 16)
+            c3m.super_run(5, stream)
+            torch.cuda.synchronize()
+            c3m.sync()
+            barrier()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            steps3 = 40
+            ta.record(stream)
+            c3m.super_run(steps3, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            c3m.sync()
+            barrier()
+            sec3 = maxr(ta.elapsed_time(tb)) / 1e3
+            c3m.destroy()
+            barrier()
+            extras["mlp_config3_one_per_gpu"] = {
+                "workload": f"config3: MLP {I}->{H}->{O_}, M={Mm}, n={world} workers one per GPU on a ring, "
+                            "free-running host-driven loop (super-learners with R=1), device Philox batches",
+                "updates_per_s": world * steps3 / sec3, "samples_per_s": world * steps3 * Mm / sec3}
         if world == 1:
             extras["config1_lsq"] = config1_leg(P, synth, torch)
             extras["config2_gossip"] = config2_leg(P, synth, torch)

@@ -251,8 +251,9 @@ adpsgd_status adpsgd_replay(adpsgd_ctx* ctx, const adpsgd_event* schedule, int64
  * = s*R + r belongs to super-learner s, and the graph must be R copies of the
  * super-learners' bipartite graph (learner (s, r) neighbours (s', r) only).
  * Every rank runs n_steps iterations of its super-learner's loop: its learner
- * gradient at its replica (quadratic, noise key 2^61 | s<<44 | c<<8 | r, c = the
- * super-learner's gradient count), NCCL all-reduce SUM over the group; the
+ * gradient at its replica (any built-in model; its noise / Philox minibatch keyed
+ * by 2^61 | s<<44 | c<<8 | r, c = the super-learner's gradient count), NCCL
+ * all-reduce SUM over the group; the
  * group leader takes the passive super-learner's lock (active: a neighbour drawn
  * uniformly; passive: its own) and the ticket k; every replica r averages with
  * replica r of the partner over NVLink and applies x <- m - gamma g (Alg. 1

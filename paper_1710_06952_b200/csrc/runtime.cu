@@ -1436,7 +1436,8 @@ adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream str
   GUARD({
     CTX_CHECK(c);
     if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
-    if (c->model != ADPSGD_MODEL_QUADRATIC) return fail(ADPSGD_E_UNSUPPORTED, "super_run uses the quadratic model");
+    if (c->model == ADPSGD_MODEL_NONE || c->model == ADPSGD_MODEL_EXTERNAL)
+      return fail(ADPSGD_E_UNSUPPORTED, "super_run needs a built-in model (quadratic, lsq, logreg, mlp)");
     if (n_steps < 0) return fail(ADPSGD_E_INVALID, "n_steps < 0");
     ST(super_setup(c));
     const int R = c->super_R > 1 ? c->super_R : 1;
@@ -1457,8 +1458,8 @@ adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream str
         js = nb[splitmix64(c->seed ^ ((uint64_t)s << 40) ^ (uint64_t)cs) % nb.size()];
       }
       unsigned int* lock = &ctl_of((active ? js : s) * R)->lock;   // the passive side's leader lock
-      auto gradient = [&]() -> adpsgd_status {
-        CU(launch_quad_grad(row, c->super_g, c->d, c->n4, c->q, key, st));
+      auto gradient = [&]() -> adpsgd_status {   // learner r's minibatch gradient (device Philox batches)
+        ST(model_grad(c, row, c->super_g, key, nullptr, st));
         if (R > 1) NC(ncclAllReduce(c->super_g, c->super_g, (size_t)c->d_pad, ncclFloat32, ncclSum, c->super_comm, st));
         return ADPSGD_OK;
       };
@@ -1480,7 +1481,7 @@ adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream str
       if (r == 0)
         CU(launch_super_commit(c->log0, c->log_cap, c->super_k, s, js, 0u, ctl_of(s * R), &c->gctl0->committed, lock,
                                st));
-      c->launches += 4;
+      c->launches += 3;                 // lock, event, commit (model_grad counts its own)
       c->super_c += 1;
     }
     c->host_k += (unsigned long long)S * (unsigned long long)n_steps;

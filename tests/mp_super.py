@@ -71,6 +71,51 @@ def main():
                     fails.append(f"S={S} R={R}: no averaging events")
         ctx.destroy()
         dist.barrier()
+    # sampled models (device Philox minibatches keyed by the super-learner key):
+    # the tcgen05 MLP (config 3 with one worker per GPU when R = 1) and lsq
+    I, H, O_, M, S = 256, 128, 10, 128, 2048
+    Xd, yd = synth.mlp_data(S=S, n_in=I, n_out=O_, s=0.02, seed=3)
+    w0 = synth.mlp_init(I, H, O_, seed=4)
+    A, b = synth.lsq_data(S=S, d=1024, seed=1)
+    seed = 0x5EED_0000_1234
+    for kind in ("mlp", "lsq"):
+        for R in [r for r in range(1, world + 1) if world % r == 0]:
+            S_ = world // R
+            e, role, wr, se, sr = synth.super_ring(S_, R)
+            if kind == "mlp":
+                dm, x0 = w0.size, w0
+                kw = dict(model=P.MODEL_MLP, gamma=0.002, batch_M=M, data_A=Xd, data_y=yd, mlp_dims=(I, H, O_))
+            else:
+                dm, x0 = 1024, np.zeros(1024, np.float32)
+                kw = dict(model=P.MODEL_LSQ, gamma=0.02, batch_M=32, data_A=A, data_b=b)
+            ctx = P.Context(e, world, dm, role=role, rank=rank, world_size=world, device=local, placement=2,
+                            worker_rank=wr, x0=x0, seed=seed, super_R=R, **kw)
+            ctx.super_run(20)
+            ctx.sync()
+            dist.barrier()
+            allm = [None] * world
+            dist.all_gather_object(allm, {w: ctx.read_model(w) for w in ctx.local_workers()})
+            if rank == 0:
+                X = np.zeros((world, dm), np.float32)
+                for m in allm:
+                    for w, x in m.items():
+                        X[w] = x
+                for s_ in range(S_):
+                    for r_ in range(1, R):
+                        if not np.array_equal(X[s_ * R].view(np.uint32), X[s_ * R + r_].view(np.uint32)):
+                            fails.append(f"{kind} S={S_} R={R}: replicas differ")
+                log = ctx.read_log(0)
+                ev = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+                bk = (seed & 0xFFFFFFFF, seed >> 32)
+                prob = O.OracleProblem(O.MODEL_MLP, M=M, gamma=0.002, A=Xd, y=yd, dims=(I, H, O_), batch_key=bk) \
+                    if kind == "mlp" else O.OracleProblem(O.MODEL_LSQ, M=32, gamma=0.02, A=A, b=b, batch_key=bk)
+                Xo = O.super_replay(prob, np.tile(x0, (S_, 1)), se, sr, ev, R)
+                rms = np.sqrt(np.mean(Xo.astype(np.float64) ** 2, axis=1, keepdims=True))
+                err = np.abs(X[::R].astype(np.float64) - Xo) / np.maximum(np.abs(Xo), rms)
+                if len(log) != S_ * 20 or err.max() > 1e-4:
+                    fails.append(f"{kind} S={S_} R={R}: {len(log)} events, log replay error {err.max():.2e}")
+            ctx.destroy()
+            dist.barrier()
     if rank == 0:
         print("SUPER", "FAIL" if fails else "OK", fails, flush=True)
     dist.destroy_process_group()
