@@ -108,6 +108,8 @@ cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, lo
                                  double* sum, cudaStream_t s);
 cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out, unsigned int* err,
                                       cudaStream_t s);
+cudaError_t launch_consensus_fused(const float* X, int n_rows, long long d_pad, long long d, int n, float* out,
+                                   double* acc, unsigned int* err, cudaStream_t s);   // world 1
 cudaError_t launch_consensus_mk(const float* X, int n_rows, long long d_pad, long long d,
                                 const double* sum, int n, double* acc, cudaStream_t s);
 cudaError_t launch_ar_grad_sum(const float* x, float* gsum, long long d, long long n4,

@@ -234,6 +234,41 @@ __global__ void k_consensus_finalize(const double* __restrict__ sum, int n, long
   if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(err, 0u, 6u);
 }
 
+// World 1: x_bar = fl32(fp64 sum / n) and, when acc != null, M_k's sum of
+// (mean - x)^2 in ONE read of the rows (the second loop re-reads the same lines
+// from L2).  x_bar is bitwise the sum + finalize result (same fp64 row order).
+__global__ void k_consensus_fused(const float* __restrict__ X, int n_rows, long long d_pad, long long d, int n,
+                                  float* __restrict__ out, double* acc, unsigned int* err) {
+  double part = 0.0;
+  bool bad = false;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d;
+       c += (long long)gridDim.x * blockDim.x) {
+    double s = 0.0;
+    for (int r = 0; r < n_rows; ++r) s += (double)__ldcg(X + (long long)r * d_pad + c);
+    bad |= !isfinite(s);
+    const double mean = __ddiv_rn(s, (double)n);
+    out[c] = __double2float_rn(mean);
+    if (acc)
+      for (int r = 0; r < n_rows; ++r) {
+        const double e = mean - (double)__ldcg(X + (long long)r * d_pad + c);
+        part += e * e;
+      }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(err, 0u, 6u);
+  if (!acc) return;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(acc, v);
+  }
+}
+
 // M_k partial: sum over local rows and coordinates of (mean - x)^2, fp64
 __global__ void k_consensus_mk(const float* __restrict__ X, int n_rows, long long d_pad, long long d,
                                const double* __restrict__ sum, int n, double* acc) {
@@ -497,6 +532,12 @@ cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, lo
 cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, float* out, unsigned int* err,
                                       cudaStream_t s) {
   k_consensus_finalize<<<4 * sm_count(), 256, 0, s>>>(sum, n, d, out, err);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_consensus_fused(const float* X, int n_rows, long long d_pad, long long d, int n, float* out,
+                                   double* acc, unsigned int* err, cudaStream_t s) {
+  k_consensus_fused<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, n, out, acc, err);
   return cudaGetLastError();
 }
 

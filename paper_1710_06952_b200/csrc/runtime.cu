@@ -1188,6 +1188,25 @@ adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, a
     cudaStream_t st = c->use(s);
     // quiesce: every rank's engine (and its P2P stores into our rows) has
     // finished once this tiny all-reduce completes on our stream
+    if (c->world == 1) {               // one pass over the rows: x_bar (+ M_k)
+      if (mk_out) CU(cudaMemsetAsync(c->mk_acc, 0, sizeof(double), st));
+      CU(launch_consensus_fused(c->models, c->n_local, c->d_pad, c->d, c->n, out, mk_out ? c->mk_acc : nullptr,
+                                &c->gctl->error, st));
+      ++c->launches;
+      if (mk_out) {
+        double acc = 0.0;
+        CU(cudaMemcpyAsync(&acc, c->mk_acc, sizeof(double), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        if (!std::isfinite(acc)) {
+          char buf[96];
+          snprintf(buf, sizeof buf, "non-finite model value at the consensus after event %llu (S:289)",
+                   (unsigned long long)c->host_k);
+          return fail(ADPSGD_E_DIVERGED, buf);
+        }
+        *mk_out = acc / (double)c->n;
+      }
+      return ADPSGD_OK;
+    }
     if (c->world > 1) NC(ncclAllReduce(c->mk_acc, c->mk_acc, 1, ncclFloat64, ncclSum, c->comm, st));
     CU(launch_consensus_sum(c->models, c->n_local, c->d_pad, c->d, c->sum64, st));
     ++c->launches;
