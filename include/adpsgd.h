@@ -228,7 +228,13 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* ctx, int32_t i, int32_t j, adpsgd_stream
  * neighbour j drawn uniformly from N(w) and apply x_w <- m - gamma g (Alg. 1
  * order, reading R1); if w is passive, x_w <- x_w - gamma g (W_k = I).
  * Serialised against other adpsgd_step calls of the same context by stream
- * order; world_size must be 1.  *ticket_out (nullable) receives k.             */
+ * order.  world_size > 1: w must live on this rank; the passive side's lock
+ * (the partner's, or w's own for a passive step) and the ticket k are taken
+ * on the device -- other ranks may step concurrently -- then the fused pass
+ * runs over NVLink and a commit kernel logs and unlocks; end such a step phase
+ * with adpsgd_sync on every rank and a barrier before the next collective call
+ * (run/replay/super_run), which otherwise fails with ADPSGD_E_STATE.
+ * *ticket_out (nullable) receives k.                                           */
 adpsgd_status adpsgd_step(adpsgd_ctx* ctx, int32_t w, const float* grad, adpsgd_stream s,
                           int64_t* ticket_out);
 

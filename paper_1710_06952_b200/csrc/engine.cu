@@ -432,6 +432,8 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     // from another GPU -- could be overwritten by this clear
     st_release_sys(&p.workers[j].ctl->guest_tag, tag_of(sl->gseq, kStateIdle));
     sl->coop = 0;
+    __threadfence_system();   // the clear must be visible before the release below (a relaxed
+                              // unlock / epoch bump is not ordered after a release store)
   }
   if (p.mode == 1) {
     atomicAdd_system(&sl->ctl_i->epoch, 1u);

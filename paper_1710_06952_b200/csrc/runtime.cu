@@ -172,6 +172,7 @@ struct adpsgd_ctx {
   std::vector<cudaEvent_t> last_evt;
   std::vector<uint64_t> step_ctr;
   unsigned long long host_k = 0;
+  bool ticket_dirty = false;         // multi-GPU adpsgd_step moved the device counter
   std::vector<unsigned int> epochs;  // per-worker committed-replay-event counts (mirror)
   long long launches = 0;
   unsigned int run_counter = 0;
@@ -301,7 +302,30 @@ adpsgd_status read_ticket(adpsgd_ctx* c, unsigned long long* k) {
   return ADPSGD_OK;
 }
 
+// After multi-GPU adpsgd_step calls the device counter moved under every rank.
+// adpsgd_sync re-reads it (every rank syncs before the barrier that ends the
+// step phase, so no rank's next collective call can have moved it yet); a
+// collective call made without that sync fails instead of deriving a target
+// from a counter another rank's engine may already be advancing.
+adpsgd_status settle_ticket(adpsgd_ctx* c) {
+  if (!c->ticket_dirty) return ADPSGD_OK;
+  if (c->world > 1)
+    return fail(ADPSGD_E_STATE, "after multi-GPU adpsgd_step calls, call adpsgd_sync on every rank and a "
+                                "barrier before the next collective call");
+  return ADPSGD_OK;
+}
+
+adpsgd_status resync_ticket(adpsgd_ctx* c) {   // from adpsgd_sync (device quiescent)
+  if (!c->ticket_dirty) return ADPSGD_OK;
+  unsigned long long t = 0;
+  CU(cudaMemcpy(&t, &c->gctl0->ticket, sizeof t, cudaMemcpyDeviceToHost));
+  c->host_k = t;
+  c->ticket_dirty = false;
+  return ADPSGD_OK;
+}
+
 adpsgd_status host_ticket(adpsgd_ctx* c, unsigned long long* k) {
+  ST(settle_ticket(c));
   *k = c->host_k;          // authoritative on every rank (see replay_engine)
   return ADPSGD_OK;
 }
@@ -727,6 +751,7 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   // through collective calls whose effect is known: a replay advances k by K
   // and the epochs by the schedule, a run ends at exactly its target), so no
   // rank reads device state that another rank's engine may already be moving.
+  ST(settle_ticket(c));
   const unsigned long long k0 = c->host_k;
   std::vector<std::vector<ReplayEv>> per;
   plan_replay(c->worker_rank, c->worker_local, c->rank, c->n_local, ev, K, k0, c->epochs, per);
@@ -1104,14 +1129,67 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s
   })
 }
 
+// adpsgd_step at world_size > 1: the passive side's lock (the partner's when w
+// is active, w's own when it steps alone) and the ticket k are taken on the
+// device -- the lock may live on a peer GPU and other ranks step concurrently --
+// k is read back (a built-in gradient's draws are keyed by k), then gradient,
+// fused pass over NVLink, and a commit kernel that logs and unlocks.
+static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_stream s, int64_t* ticket_out) {
+  if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
+  if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "adpsgd_step: worker w must live on this rank");
+  std::lock_guard<std::mutex> lk(c->mu);
+  int j = -1;
+  if (c->role[w] == 0 && !c->nb[w].empty()) {
+    uint64_t st = c->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(w + 1)) ^ (c->step_ctr[w]++ << 20);
+    const uint64_t r = splitmix64(st);
+    j = c->nb[w][(size_t)((r >> 32) * c->nb[w].size() >> 32)];
+  }
+  auto ctl_of = [&](int v) {
+    return reinterpret_cast<WorkerCtl*>(c->peer_ctl[c->worker_rank[v]]) + c->worker_local[v];
+  };
+  auto row_of = [&](int v) {
+    return c->peer_models[c->worker_rank[v]] + (long long)c->worker_local[v] * c->d_pad;
+  };
+  if (!c->super_k) {
+    CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
+    CU(cudaDeviceSynchronize());
+  }
+  cudaStream_t st = c->use(s);
+  unsigned int* lock = &ctl_of(j >= 0 ? j : w)->lock;
+  CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, 20ull * 1000000000ull, st));
+  unsigned long long k = 0;
+  CU(cudaMemcpyAsync(&k, c->super_k, sizeof k, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  if (k == ~0ull) return fail(ADPSGD_E_TIMEOUT, "adpsgd_step: lock wait exceeded the watchdog");
+  int mode = kGradExternal;
+  const float* g = grad;
+  if (!grad) {
+    if (c->model == ADPSGD_MODEL_QUADRATIC) {
+      mode = kGradQuadInline;
+    } else {
+      if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+      float* gb = c->gstep + (long long)c->worker_local[w] * c->d_pad;
+      ST(model_grad(c, c->row(w), gb, k, nullptr, st));
+      g = gb;
+    }
+  }
+  CU(launch_event(c->row(w), j >= 0 ? row_of(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma, c->q, k, mode, st));
+  CU(launch_super_commit(c->log0, c->log_cap, c->super_k, w, j, 0u, c->ctl + c->worker_local[w],
+                         &c->gctl0->committed, lock, st));
+  c->launches += 3;
+  c->ticket_dirty = true;                 // other ranks move the counter too: re-read before the next run
+  if (ticket_out) *ticket_out = (int64_t)k;
+  return ADPSGD_OK;
+}
+
 adpsgd_status adpsgd_step(adpsgd_ctx* c, int32_t w, const float* grad, adpsgd_stream s,
                           int64_t* ticket_out) {
   GUARD({
     CTX_CHECK(c);
     if (w < 0 || w >= c->n) return fail(ADPSGD_E_INVALID, "worker");
-    if (c->world != 1) return fail(ADPSGD_E_UNSUPPORTED, "adpsgd_step needs world_size 1 (use adpsgd_run)");
     if (!grad && (c->model == ADPSGD_MODEL_NONE || c->model == ADPSGD_MODEL_EXTERNAL))
       return fail(ADPSGD_E_INVALID, "no gradient: pass grad or configure a built-in model");
+    if (c->world > 1) return step_multi(c, w, grad, s, ticket_out);
     std::lock_guard<std::mutex> lk(c->mu);
     int j = -1;
     if (c->role[w] == 0 && !c->nb[w].empty()) {
@@ -1171,6 +1249,7 @@ adpsgd_status adpsgd_run(adpsgd_ctx* c, int64_t n_updates, adpsgd_stream s) {
     if (n_updates < 0) return fail(ADPSGD_E_INVALID, "n_updates");
     std::lock_guard<std::mutex> lk(c->mu);
     // the run ends with the ticket at exactly k0 + n_updates on every rank
+    ST(settle_ticket(c));
     const unsigned long long k0 = c->host_k;
     cudaStream_t st = c->use(s);
     ST(reset_slots(c, st));
@@ -1459,6 +1538,7 @@ adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream str
       return fail(ADPSGD_E_UNSUPPORTED, "super_run needs a built-in model (quadratic, lsq, logreg, mlp)");
     if (n_steps < 0) return fail(ADPSGD_E_INVALID, "n_steps < 0");
     ST(super_setup(c));
+    ST(settle_ticket(c));
     const int R = c->super_R > 1 ? c->super_R : 1;
     cudaStream_t st = c->use(strm);
     const int w = c->rank, s = w / R, r = w % R, S = c->n / R;
@@ -1512,6 +1592,7 @@ adpsgd_status adpsgd_sync(adpsgd_ctx* c) {
   GUARD({
     CTX_CHECK(c);
     CU(cudaDeviceSynchronize());
+    ST(resync_ticket(c));
     unsigned int err = 0;
     CU(cudaMemcpy(&err, &c->gctl->error, sizeof err, cudaMemcpyDeviceToHost));
     if (err) {

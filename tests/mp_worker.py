@@ -38,6 +38,10 @@ def gather_models(ctx):
     return X
 
 
+def progress(rank, what):
+    print(f"[rank {rank}] {what}", file=sys.stderr, flush=True)
+
+
 def main():
     rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
     torch.cuda.set_device(local)
@@ -78,6 +82,7 @@ def main():
         if variant == 3:
             ctx.destroy()
             dist.barrier()
+    progress(rank, "1 pure-gossip replay done")
     # 4. consensus mean (NCCL fp64)
     out = torch.empty(d, dtype=torch.float32, device="cuda")
     mk = ctx.consensus_mean(out.data_ptr())
@@ -91,6 +96,7 @@ def main():
     ctx.destroy()
     dist.barrier()
 
+    progress(rank, "4 consensus done")
     # 2./3. quadratic: engine replay then free-running, block placement
     d = 1 << 20
     ev, _ = synth.schedule_iid(n, e, K=400, seed=8, local_prob=0.3)
@@ -118,6 +124,7 @@ def main():
         if not np.array_equal(X2.view(np.uint32), Xo2.view(np.uint32)):
             bad = np.where((X2 != Xo2).any(1))[0]
             fails.append(f"free-running multi-GPU log replay not bit-exact (workers {bad.tolist()})")
+    progress(rank, "2/3 quadratic replay + free-running done")
     # 6. D-PSGD baseline: halo exchange of neighbour rows by NCCL send/recv
     X0d = synth.x0_uniform(n, d, seed=23)
     ctx.dpsgd_reset(X0d)
@@ -149,6 +156,40 @@ def main():
     ctx.destroy()
     dist.barrier()
 
+    progress(rank, "5/6 baselines done")
+    # 8. host-driven adpsgd_step across GPUs (device try-lock + ticket, fused pass over
+    #    NVLink, commit): ranks step their own workers concurrently; the log replays bitwise
+    d = (1 << 14) + 20
+    X0s = synth.x0_uniform(n, d, seed=27)
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+                    model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
+                    x0_per_worker=X0s, seed=13)
+    for _ in range(25):
+        for w in ctx.local_workers():
+            ctx.step(w)
+    ctx.sync()
+    dist.barrier()
+    Xs = gather_models(ctx)
+    if rank == 0:
+        log = ctx.read_log(0)
+        evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+        if len(log) != 25 * n or not np.array_equal(np.sort(log["k"]), np.arange(25 * n)):
+            fails.append(f"multi-GPU step log: {len(log)} entries")
+        else:
+            order = np.argsort(log["k"])
+            Xso, _ = O.replay(prob_q, X0s, e, r, evs[order])
+            if not np.array_equal(Xs.view(np.uint32), Xso.view(np.uint32)):
+                fails.append("multi-GPU adpsgd_step log replay not bit-exact")
+    progress(rank, "8 steps done")
+    ctx.run(200)                                  # the device ticket is settled before the collective run
+    ctx.sync()
+    dist.barrier()
+    if rank == 0 and ctx.ticket() != 25 * n + 200:
+        fails.append(f"ticket after steps + run: {ctx.ticket()}")
+    ctx.destroy()
+    dist.barrier()
+
+    progress(rank, "8 run after steps done")
     # 7. App. A wait-free engine loop (reading R20), interleave placement: pulls,
     #    buffered-gradient flushes and continuous averages across NVLink; the log
     #    (tau = k - t_read, FLUSH_FIRST | COMPENSATE) replays bitwise
