@@ -231,9 +231,10 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* ctx, int32_t i, int32_t j, adpsgd_stream
  * order.  world_size > 1: w must live on this rank; the passive side's lock
  * (the partner's, or w's own for a passive step) and the ticket k are taken
  * on the device -- other ranks may step concurrently -- then the fused pass
- * runs over NVLink and a commit kernel logs and unlocks; end such a step phase
- * with adpsgd_sync on every rank and a barrier before the next collective call
- * (run/replay/super_run), which otherwise fails with ADPSGD_E_STATE.
+ * runs over NVLink and a commit kernel logs and unlocks.  Collective calls
+ * (run/replay/super_run) made after such steps first agree on the device
+ * counter across ranks (a small NCCL all-reduce), so every rank must have
+ * finished its steps before any rank enters one (e.g. a barrier).
  * *ticket_out (nullable) receives k.                                           */
 adpsgd_status adpsgd_step(adpsgd_ctx* ctx, int32_t w, const float* grad, adpsgd_stream s,
                           int64_t* ticket_out);

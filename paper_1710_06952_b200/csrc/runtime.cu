@@ -173,6 +173,7 @@ struct adpsgd_ctx {
   std::vector<uint64_t> step_ctr;
   unsigned long long host_k = 0;
   bool ticket_dirty = false;         // multi-GPU adpsgd_step moved the device counter
+  unsigned long long* agree64 = nullptr;   // ticket agreement scratch (collective calls, world > 1)
   std::vector<unsigned int> epochs;  // per-worker committed-replay-event counts (mirror)
   long long launches = 0;
   unsigned int run_counter = 0;
@@ -302,23 +303,21 @@ adpsgd_status read_ticket(adpsgd_ctx* c, unsigned long long* k) {
   return ADPSGD_OK;
 }
 
-// After multi-GPU adpsgd_step calls the device counter moved under every rank.
-// adpsgd_sync re-reads it (every rank syncs before the barrier that ends the
-// step phase, so no rank's next collective call can have moved it yet); a
-// collective call made without that sync fails instead of deriving a target
-// from a counter another rank's engine may already be advancing.
+// Multi-GPU adpsgd_step moves the device counter under every rank, so at the
+// start of a collective call (world > 1) the ranks agree on it: each reads the
+// device ticket after its own work has drained, then an NCCL all-reduce (MIN)
+// -- no rank can launch the collective's engine before every rank has
+// contributed its read, so all reads see the same settled value.
 adpsgd_status settle_ticket(adpsgd_ctx* c) {
-  if (!c->ticket_dirty) return ADPSGD_OK;
-  if (c->world > 1)
-    return fail(ADPSGD_E_STATE, "after multi-GPU adpsgd_step calls, call adpsgd_sync on every rank and a "
-                                "barrier before the next collective call");
-  return ADPSGD_OK;
-}
-
-adpsgd_status resync_ticket(adpsgd_ctx* c) {   // from adpsgd_sync (device quiescent)
-  if (!c->ticket_dirty) return ADPSGD_OK;
+  if (c->world == 1 || !c->comm) return ADPSGD_OK;
+  CU(cudaStreamSynchronize(c->stream));
+  CU(cudaDeviceSynchronize());
+  if (!c->agree64) CU(cudaMalloc(&c->agree64, sizeof(unsigned long long)));
+  CU(cudaMemcpy(c->agree64, &c->gctl0->ticket, sizeof(unsigned long long), cudaMemcpyDeviceToDevice));
+  NC(ncclAllReduce(c->agree64, c->agree64, 1, ncclUint64, ncclMin, c->comm, c->stream));
   unsigned long long t = 0;
-  CU(cudaMemcpy(&t, &c->gctl0->ticket, sizeof t, cudaMemcpyDeviceToHost));
+  CU(cudaMemcpyAsync(&t, c->agree64, sizeof t, cudaMemcpyDeviceToHost, c->stream));
+  CU(cudaStreamSynchronize(c->stream));
   c->host_k = t;
   c->ticket_dirty = false;
   return ADPSGD_OK;
@@ -795,7 +794,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
-                  c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar};
+                  c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar, c->agree64};
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -1592,7 +1591,6 @@ adpsgd_status adpsgd_sync(adpsgd_ctx* c) {
   GUARD({
     CTX_CHECK(c);
     CU(cudaDeviceSynchronize());
-    ST(resync_ticket(c));
     unsigned int err = 0;
     CU(cudaMemcpy(&err, &c->gctl->error, sizeof err, cudaMemcpyDeviceToHost));
     if (err) {
