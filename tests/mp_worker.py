@@ -12,6 +12,8 @@ Checks (DESIGN.md 'Multi-GPU'):
   5. AllReduce-SGD baseline (NCCL fp32) within 1e-5 relative;
   6. D-PSGD baseline (NCCL halo exchange) bitwise;
   7. App. A wait-free engine loop across GPUs: log replay bitwise.
+  8. host-driven adpsgd_step across GPUs (ranks step concurrently): log replay
+     bitwise; a collective run afterwards starts from the agreed device ticket.
 """
 import math
 import os
