@@ -555,6 +555,16 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
   const int tiles_ev = (int)((p.n4 + kTile4 - 1) / kTile4);
   const int want = (tiles_ev + ADPSGD_MIN_TILES_PER_CTA - 1) / ADPSGD_MIN_TILES_PER_CTA;
   const int part = (kVar == 1 || want >= (int)gridDim.x) ? (int)gridDim.x : (want > 0 ? want : 1);
+  // A cross-GPU event is bound by NVLink (~1/8 of HBM), so it is given a
+  // fraction of the CTAs (rotated by slot, like small events): the rest keep
+  // streaming local events from HBM meanwhile instead of every CTA stalling on
+  // its share of the remote tiles.  Both GPUs of a cooperative event use the same
+  // fraction (same grid), so the arrival count is 2 * xpart.
+#ifndef ADPSGD_CROSS_DIV
+#define ADPSGD_CROSS_DIV 4   // N=2 A/B (bench --no-extras, coop auto): 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k gossip-steps/s
+#endif
+  const int xpart = kVar == 1 ? (int)gridDim.x
+                    : max(1, min(part, (int)gridDim.x / (ADPSGD_CROSS_DIV > 1 ? ADPSGD_CROSS_DIV : 1)));
   unsigned long long last_progress = globaltimer();
   while (true) {
     if (threadIdx.x == 0) {
@@ -585,6 +595,12 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
             WorkerCtl* cl = p.workers[wl].ctl;
             const unsigned int gt = ld_acquire_sys(&cl->guest_tag);
             if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
+            int grb = (int)blockIdx.x;
+            if (xpart < (int)gridDim.x) {
+              const int base = (int)(((unsigned int)l * (unsigned int)xpart) % gridDim.x);
+              grb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
+              if (grb >= xpart) { gdone_seq[l] = gt >> 2; continue; }  // not one of this event's CTAs
+            }
             const int gi = *(volatile int*)&cl->guest_i;
             Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
             const unsigned int fl = *(volatile unsigned int*)&sa->flags;
@@ -602,8 +618,9 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
             s_ev.cross = 1;
             s_ev.t0 = s_ev.t1 = 0;
             s_ev.coop = 1;
-            s_ev.first = (long long)gridDim.x + blockIdx.x;
-            s_ev.step = 2ll * gridDim.x;
+            s_ev.first = (long long)xpart + grb;
+            s_ev.step = 2ll * xpart;
+            s_ev.ncta = 2 * xpart;
             s_ev.guest = 1;
             s_ev.gl = l;
             s_ev.gdone = &sa->done;
@@ -629,14 +646,15 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         if ((tag & 3u) != kStateRunning || (tag >> 2) == done_seq[s]) continue;
         Slot* sl = p.slots + s;
         int rb = (int)blockIdx.x;
-        const bool small = part < (int)gridDim.x && !*(volatile int*)&sl->coop &&
-                           !(p.two_sided && *(volatile int*)&sl->cross);
-        if (small) {
-          const int base = (int)(((unsigned int)s * (unsigned int)part) % gridDim.x);
-          rb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
-          if (rb >= part) { done_seq[s] = tag >> 2; continue; }   // not one of this event's CTAs
-        }
         const int cross = *(volatile int*)&sl->cross;
+        const int coop = *(volatile int*)&sl->coop;
+        // CTAs that take this event: all, `part` (small d) or `xpart` (cross-GPU, one-sided or cooperative)
+        const int evp = (cross && !p.two_sided) ? xpart : ((!coop && !(p.two_sided && cross)) ? part : (int)gridDim.x);
+        if (evp < (int)gridDim.x) {
+          const int base = (int)(((unsigned int)s * (unsigned int)evp) % gridDim.x);
+          rb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
+          if (rb >= evp) { done_seq[s] = tag >> 2; continue; }    // not one of this event's CTAs
+        }
         long long t0 = 0, t1 = 0;
         if (cross && p.two_sided && kVar != 1) {
           if (cons_seq[s] != (tag >> 2)) { cons_seq[s] = tag >> 2; cons_cnt[s] = 0u; }
@@ -668,10 +686,10 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.cross = cross;
         s_ev.t0 = t0;
         s_ev.t1 = t1;
-        s_ev.coop = *(volatile int*)&sl->coop;
+        s_ev.coop = coop;
         s_ev.first = rb;
-        s_ev.step = s_ev.coop ? 2ll * gridDim.x : (small ? (long long)part : (long long)gridDim.x);
-        s_ev.ncta = s_ev.coop ? 2 * (int)gridDim.x : (small ? part : (int)gridDim.x);
+        s_ev.step = coop ? 2ll * evp : (long long)evp;
+        s_ev.ncta = coop ? 2 * evp : evp;
         s_ev.guest = 0;
       }
 #ifndef ADPSGD_GUEST_FIRST
@@ -741,7 +759,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         if (finished && e.guest) {          // our half of a peer's cooperative event
           gdone_seq[e.gl] = s_seq;
           __threadfence_system();
-          if (atomicAdd_system(e.gdone, 1u) == 2u * gridDim.x - 1u) st_release_sys(e.gready, s_seq);
+          if (atomicAdd_system(e.gdone, 1u) == (unsigned int)e.ncta - 1u) st_release_sys(e.gready, s_seq);
         } else if (finished) {
           done_seq[pick] = s_seq;
           // this CTA's slice is visible before its arrival; P2P stores need the
@@ -750,7 +768,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           if (e.cross) __threadfence_system();
           else __threadfence();
           if (e.coop) {
-            if (atomicAdd_system(&p.slots[pick].done, 1u) == 2u * gridDim.x - 1u) commit(p, pick);
+            if (atomicAdd_system(&p.slots[pick].done, 1u) == (unsigned int)e.ncta - 1u) commit(p, pick);
           } else if (atomicAdd(&p.slots[pick].done, 1u) == (unsigned int)e.ncta - 1u) {
             commit(p, pick);
           }
