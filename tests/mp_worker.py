@@ -13,8 +13,12 @@ Checks (DESIGN.md 'Multi-GPU'):
   6. D-PSGD baseline (NCCL halo exchange) bitwise;
   7. App. A wait-free engine loop across GPUs: log replay bitwise.
   8. host-driven adpsgd_step across GPUs (ranks step concurrently): log replay
-     bitwise; a collective run afterwards starts from the agreed device ticket.
+     bitwise; a collective run afterwards starts from the agreed device ticket;
+  9. the bench workload at full size (d = 25.6M, 8 workers/GPU, block placement,
+     10x straggler, cooperative cross events on their grid/4 CTA footprint):
+     free-running log replay bitwise, compared through per-row SHA-1 digests.
 """
+import hashlib
 import math
 import os
 import sys
@@ -215,6 +219,38 @@ def main():
             Xwo, _ = O.replay(prob_q, X0w, e, r, evs, T=int(evs[:, 2].max()))
             if not np.array_equal(Xw.view(np.uint32), Xwo.view(np.uint32)):
                 fails.append("wait-free multi-GPU log replay not bit-exact")
+    ctx.destroy()
+    dist.barrier()
+
+    progress(rank, "7 wait-free done")
+    # 9. full-size bench workload across GPUs: digests of every row vs the oracle's replay
+    d, U = 25_600_000, 32 * world
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=0,
+                    model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
+                    straggler=synth.stragglers(n), compute_ns=50_000, seed=17)
+    ctx.run(U)
+    ctx.sync()
+    dist.barrier()
+    mine = {w: hashlib.sha1(ctx.read_model(w).tobytes()).hexdigest() for w in ctx.local_workers()}
+    cross = ctx.stats()["local_cross_events"]
+    alld, allc = [None] * world, [None] * world
+    dist.all_gather_object(alld, mine)
+    dist.all_gather_object(allc, cross)
+    if rank == 0:
+        dig = {w: h for m in alld for w, h in m.items()}
+        log = ctx.read_log(0)
+        evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
+        if len(log) != U:
+            fails.append(f"full-size log has {len(log)} entries")
+        else:
+            Xf, _ = O.replay(prob_q, np.zeros((n, d), np.float32), e, r, evs)
+            bad = [w for w in range(n) if hashlib.sha1(Xf[w].tobytes()).hexdigest() != dig[w]]
+            if bad:
+                fails.append(f"full-size multi-GPU log replay not bit-exact (workers {bad})")
+            del Xf
+        if sum(allc) == 0:
+            fails.append("full-size run had no cross-GPU event")
+        progress(rank, f"9 full size: {sum(allc)} cross events of {U}")
     ctx.destroy()
     dist.barrier()
     if rank == 0:
