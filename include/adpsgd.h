@@ -187,7 +187,9 @@ typedef struct {
   int64_t local_events;      /* events committed by this rank's engine/executor            */
   int64_t local_pair_events; /* of which pair averages                                     */
   int64_t local_cross_events;/* of which the partner lives on another rank (NVLink)       */
-  double  local_bytes;       /* algorithmic HBM+NVLink bytes moved by this rank's passes   */
+  double  local_bytes;       /* algorithmic HBM bytes of this GPU: rows resident here that
+                                committed events read + wrote (a cross pair credits each GPU
+                                its own row: 8d bytes, the initiator's g row extra)          */
   double  local_nvlink_bytes;/* algorithmic bytes that crossed NVLink (both directions)    */
   double  engine_busy_ns;    /* sum over events of (t_end - t_start)                       */
 } adpsgd_stats;

@@ -42,7 +42,10 @@ struct alignas(128) WorkerCtl {
   // posts its event here so this GPU's CTAs process half of its tiles
   unsigned int guest_tag;          // (event seq << 2) | state, written by the initiator (release.sys)
   int guest_i;                     // initiating worker (its slot holds the event)
-  unsigned int pad[10];
+  // algorithmic HBM bytes moved in this worker's row by cross-GPU events that a
+  // peer committed (this GPU's share of them; engine stats)
+  double peer_bytes;
+  unsigned int pad[8];
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
 

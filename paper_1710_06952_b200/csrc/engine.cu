@@ -422,8 +422,15 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   // nothing (its row is already read and written by the pair)
   atomicAdd(&p.gctl->st_events, 1ull);
   if (j >= 0) atomicAdd(&p.gctl->st_pair, 1ull);
-  if (sl->cross) { atomicAdd(&p.gctl->st_cross, 1ull); atomicAdd(&p.gctl->st_nvl_bytes, 2.0 * d4); }
-  atomicAdd(&p.gctl->st_bytes, ((j >= 0 ? 4.0 : (grad ? 2.0 : 0.0)) + (sl->g && grad ? 1.0 : 0.0)) * d4);
+  // a cross pair's rows live on two GPUs: each HBM moves its own row (2 rows of
+  // the 4), the partner's share is credited to the partner's WorkerCtl
+  if (sl->cross) {
+    atomicAdd(&p.gctl->st_cross, 1ull);
+    atomicAdd(&p.gctl->st_nvl_bytes, 2.0 * d4);
+    atomicAdd_system(&p.workers[j].ctl->peer_bytes, 2.0 * d4);
+  }
+  atomicAdd(&p.gctl->st_bytes,
+            ((j >= 0 ? (sl->cross ? 2.0 : 4.0) : (grad ? 2.0 : 0.0)) + (sl->g && grad ? 1.0 : 0.0)) * d4);
   atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
   __threadfence_system();                 // log + data before the release below
   if (sl->coop) {

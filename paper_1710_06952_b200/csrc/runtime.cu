@@ -1695,6 +1695,11 @@ adpsgd_status adpsgd_get_stats(adpsgd_ctx* c, adpsgd_stats* o) {
     o->local_pair_events = (int64_t)g.st_pair;
     o->local_cross_events = (int64_t)g.st_cross;
     o->local_bytes = g.st_bytes;
+    if (c->n_local > 0) {                  // this GPU's share of cross pairs committed by peers
+      std::vector<WorkerCtl> h(c->n_local);
+      CU(cudaMemcpy(h.data(), c->ctl, sizeof(WorkerCtl) * c->n_local, cudaMemcpyDeviceToHost));
+      for (const WorkerCtl& w : h) o->local_bytes += w.peer_bytes;
+    }
     o->local_nvlink_bytes = g.st_nvl_bytes;
     o->engine_busy_ns = (double)g.st_busy_ns;
     return ADPSGD_OK;
@@ -1710,6 +1715,7 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* c) {
     g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = 0;
     g.st_bytes = g.st_nvl_bytes = 0.0;
     CU(cudaMemcpy(c->gctl, &g, sizeof g, cudaMemcpyHostToDevice));
+    for (int l = 0; l < c->n_local; ++l) CU(cudaMemset(&c->ctl[l].peer_bytes, 0, sizeof(double)));
     CU(cudaDeviceSynchronize());
     return ADPSGD_OK;
   })

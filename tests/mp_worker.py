@@ -78,9 +78,13 @@ def main():
         dist.barrier()
         st = ctx.stats()
         X = gather_models(ctx)
-        cross = [None] * world
+        cross, hbm = [None] * world, [None] * world
         dist.all_gather_object(cross, st["local_cross_events"])
+        dist.all_gather_object(hbm, st["local_bytes"])
         if rank == 0:
+            # every pair reads + writes two rows: 16d bytes system-wide, 8d on each GPU's HBM
+            if abs(sum(hbm) - 1500 * 16.0 * d) > 1e-6 * 1500 * 16.0 * d or min(hbm) <= 0:
+                fails.append(f"HBM byte accounting {hbm} != {1500 * 16 * d} (variant {variant})")
             if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
                 fails.append(f"pure-gossip engine replay over NVLink not bit-exact (variant {variant})")
             if sum(cross) != 1500:
