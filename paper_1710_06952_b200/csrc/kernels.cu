@@ -269,6 +269,52 @@ __global__ void k_consensus_fused(const float* __restrict__ X, int n_rows, long 
   }
 }
 
+// float4 form for R <= 8 local rows (d % 4 == 0): the R rows' values stay in
+// registers for the M_k pass, and each coordinate's fp64 sum is accumulated in the
+// same row order as k_consensus_fused, so x-bar is bitwise the same.
+template <int R>
+__global__ void __launch_bounds__(256) k_consensus_fused4(const float4* __restrict__ X, long long d_pad4, long long d4,
+                                                          int n, float4* __restrict__ out, double* acc,
+                                                          unsigned int* err) {
+  double part = 0.0;
+  bool bad = false;
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d4;
+       c += (long long)gridDim.x * blockDim.x) {
+    float4 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = __ldcg(X + (long long)r * d_pad4 + c);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      s0 += (double)v[r].x; s1 += (double)v[r].y; s2 += (double)v[r].z; s3 += (double)v[r].w;
+    }
+    bad |= !isfinite(s0) || !isfinite(s1) || !isfinite(s2) || !isfinite(s3);
+    const double m0 = __ddiv_rn(s0, (double)n), m1 = __ddiv_rn(s1, (double)n);
+    const double m2 = __ddiv_rn(s2, (double)n), m3 = __ddiv_rn(s3, (double)n);
+    out[c] = make_float4(__double2float_rn(m0), __double2float_rn(m1), __double2float_rn(m2), __double2float_rn(m3));
+    if (acc)
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const double e0 = m0 - (double)v[r].x, e1 = m1 - (double)v[r].y;
+        const double e2 = m2 - (double)v[r].z, e3 = m3 - (double)v[r].w;
+        part += e0 * e0 + e1 * e1 + e2 * e2 + e3 * e3;
+      }
+  }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicCAS(err, 0u, 6u);
+  if (!acc) return;
+#pragma unroll
+  for (int o = 16; o; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+  __shared__ double red[32];
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = part;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    double v = threadIdx.x < (blockDim.x >> 5) ? red[threadIdx.x] : 0.0;
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if (threadIdx.x == 0) atomicAdd(acc, v);
+  }
+}
+
 // M_k partial: sum over local rows and coordinates of (mean - x)^2, fp64
 __global__ void k_consensus_mk(const float* __restrict__ X, int n_rows, long long d_pad, long long d,
                                const double* __restrict__ sum, int n, double* acc) {
@@ -537,6 +583,17 @@ cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, flo
 
 cudaError_t launch_consensus_fused(const float* X, int n_rows, long long d_pad, long long d, int n, float* out,
                                    double* acc, unsigned int* err, cudaStream_t s) {
+  if (d % 4 == 0 && d_pad % 4 == 0 && n_rows >= 1 && n_rows <= 8) {
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    float4* o4 = reinterpret_cast<float4*>(out);
+    const int g = 4 * sm_count();
+    switch (n_rows) {
+#define ADPSGD_CF4(R) case R: k_consensus_fused4<R><<<g, 256, 0, s>>>(X4, d_pad / 4, d / 4, n, o4, acc, err); break;
+      ADPSGD_CF4(1) ADPSGD_CF4(2) ADPSGD_CF4(3) ADPSGD_CF4(4) ADPSGD_CF4(5) ADPSGD_CF4(6) ADPSGD_CF4(7) ADPSGD_CF4(8)
+#undef ADPSGD_CF4
+    }
+    return cudaGetLastError();
+  }
   k_consensus_fused<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, n, out, acc, err);
   return cudaGetLastError();
 }

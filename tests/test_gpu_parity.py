@@ -177,8 +177,9 @@ def test_device_batch_sampling_matches_oracle_philox(P):
 
 
 # -------------------------------------------------------- consensus output ---
-def test_consensus_mean_within_one_ulp(P):
-    n, d = 16, 1 << 20
+@pytest.mark.parametrize("n,d", [(16, 1 << 20), (8, 1 << 20), (6, 4100), (4, 1001), (2, 4)])
+def test_consensus_mean_within_one_ulp(P, n, d):
+    """n > 8 or d % 4 != 0: scalar kernel; otherwise the float4 register form."""
     e, r = synth.ring(n)
     X0 = synth.x0_uniform(n, d, seed=9) * np.float32(1000.0)
     ctx = P.Context(e, n, d, role=r, x0_per_worker=X0)
