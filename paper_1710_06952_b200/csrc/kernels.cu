@@ -220,6 +220,26 @@ __global__ void k_consensus_sum(const float* __restrict__ X, int n_rows, long lo
   }
 }
 
+// float4 form of k_consensus_sum for R <= 8 local rows (same fp64 row order)
+template <int R>
+__global__ void __launch_bounds__(256) k_consensus_sum4(const float4* __restrict__ X, long long d_pad4, long long d4,
+                                                        double* __restrict__ sum) {
+  for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < d4;
+       c += (long long)gridDim.x * blockDim.x) {
+    float4 v[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[r] = __ldcg(X + (long long)r * d_pad4 + c);
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      s0 += (double)v[r].x; s1 += (double)v[r].y; s2 += (double)v[r].z; s3 += (double)v[r].w;
+    }
+    double2* o = reinterpret_cast<double2*>(sum + 4 * c);
+    o[0] = make_double2(s0, s1);
+    o[1] = make_double2(s2, s3);
+  }
+}
+
 // x_bar = fl32(sum / n); a non-finite sum means some worker's model diverged
 // (S:289): latch ADPSGD_E_DIVERGED for the next adpsgd_sync
 __global__ void k_consensus_finalize(const double* __restrict__ sum, int n, long long d,
@@ -571,6 +591,16 @@ cudaError_t launch_comp_row(const float* x, const float* gp, float gamma, float*
 
 cudaError_t launch_consensus_sum(const float* X, int n_rows, long long d_pad, long long d,
                                  double* sum, cudaStream_t s) {
+  if (d % 4 == 0 && d_pad % 4 == 0 && n_rows >= 1 && n_rows <= 8) {
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    const int g = 4 * sm_count();
+    switch (n_rows) {
+#define ADPSGD_CS4(R) case R: k_consensus_sum4<R><<<g, 256, 0, s>>>(X4, d_pad / 4, d / 4, sum); break;
+      ADPSGD_CS4(1) ADPSGD_CS4(2) ADPSGD_CS4(3) ADPSGD_CS4(4) ADPSGD_CS4(5) ADPSGD_CS4(6) ADPSGD_CS4(7) ADPSGD_CS4(8)
+#undef ADPSGD_CS4
+    }
+    return cudaGetLastError();
+  }
   k_consensus_sum<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, sum);
   return cudaGetLastError();
 }
