@@ -192,6 +192,7 @@ typedef struct {
                                 its own row: 8d bytes, the initiator's g row extra)          */
   double  local_nvlink_bytes;/* algorithmic bytes that crossed NVLink (both directions)    */
   double  engine_busy_ns;    /* sum over events of (t_end - t_start)                       */
+  double  engine_busy_cross_ns; /* the part of engine_busy_ns spent in cross-GPU events    */
 } adpsgd_stats;
 
 /* ---------------------------------------------------------------- lifecycle -- */

@@ -75,7 +75,8 @@ LOG_DTYPE = np.dtype([("k", np.int64), ("i", np.int32), ("j", np.int32), ("tau",
 class Stats(C.Structure):
     _fields_ = [("ticket", C.c_int64), ("local_events", C.c_int64), ("local_pair_events", C.c_int64),
                 ("local_cross_events", C.c_int64), ("local_bytes", C.c_double),
-                ("local_nvlink_bytes", C.c_double), ("engine_busy_ns", C.c_double)]
+                ("local_nvlink_bytes", C.c_double), ("engine_busy_ns", C.c_double),
+                ("engine_busy_cross_ns", C.c_double)]
 
 
 def lib():

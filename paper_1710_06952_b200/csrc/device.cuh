@@ -62,7 +62,8 @@ struct alignas(128) GlobalCtl {
   unsigned int abort_flag;
   unsigned int pad0;
   unsigned long long committed;    // rank 0: events committed system-wide (== ticket when quiescent)
-  unsigned int pad[10];
+  unsigned long long st_busy_cross_ns;   // part of st_busy_ns spent in cross-GPU events
+  unsigned int pad[8];
 };
 
 struct LogEntry {                  // == adpsgd_log_entry

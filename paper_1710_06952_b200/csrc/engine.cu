@@ -432,6 +432,7 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   atomicAdd(&p.gctl->st_bytes,
             ((j >= 0 ? (sl->cross ? 2.0 : 4.0) : (grad ? 2.0 : 0.0)) + (sl->g && grad ? 1.0 : 0.0)) * d4);
   atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
+  if (sl->cross) atomicAdd(&p.gctl->st_busy_cross_ns, now - sl->t0);
   __threadfence_system();                 // log + data before the release below
   if (sl->coop) {
     // every tile of both GPUs is done: clear the partner's mailbox BEFORE the
@@ -567,6 +568,10 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
   // streaming local events from HBM meanwhile instead of every CTA stalling on
   // its share of the remote tiles.  Both GPUs of a cooperative event use the same
   // fraction (same grid), so the arrival count is 2 * xpart.
+#ifndef ADPSGD_CROSS_RESERVE
+#define ADPSGD_CROSS_RESERVE 0   // A/B (tools/ab_reserve.sh): 1 -> N=2 13.5k vs 14.5k, N=4 26.5k vs 28.4k (dropped)
+#endif
+  constexpr bool kReserve = ADPSGD_CROSS_RESERVE != 0;
 #ifndef ADPSGD_CROSS_DIV
 #define ADPSGD_CROSS_DIV 4   // N=2 A/B (bench --no-extras, coop auto): 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k gossip-steps/s
 #endif
@@ -604,7 +609,8 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
             if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
             int grb = (int)blockIdx.x;
             if (xpart < (int)gridDim.x) {
-              const int base = (int)(((unsigned int)l * (unsigned int)xpart) % gridDim.x);
+              const int base = kReserve && p.reserve ? (int)gridDim.x - xpart
+                                                     : (int)(((unsigned int)l * (unsigned int)xpart) % gridDim.x);
               grb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
               if (grb >= xpart) { gdone_seq[l] = gt >> 2; continue; }  // not one of this event's CTAs
             }
@@ -656,9 +662,15 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         const int cross = *(volatile int*)&sl->cross;
         const int coop = *(volatile int*)&sl->coop;
         // CTAs that take this event: all, `part` (small d) or `xpart` (cross-GPU, one-sided or cooperative)
-        const int evp = (cross && !p.two_sided) ? xpart : ((!coop && !(p.two_sided && cross)) ? part : (int)gridDim.x);
+        int evp = (cross && !p.two_sided) ? xpart : ((!coop && !(p.two_sided && cross)) ? part : (int)gridDim.x);
+        int base = (int)(((unsigned int)s * (unsigned int)evp) % gridDim.x);
+        if (kReserve && p.reserve && xpart < (int)gridDim.x) {
+          // cross events keep to the last xpart CTAs and large local events to the
+          // others, so a CTA busy on NVLink never holds up a local event's arrival
+          if (cross) base = (int)gridDim.x - xpart;
+          else if (evp == (int)gridDim.x) { evp = (int)gridDim.x - xpart; base = 0; }
+        }
         if (evp < (int)gridDim.x) {
-          const int base = (int)(((unsigned int)s * (unsigned int)evp) % gridDim.x);
           rb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
           if (rb >= evp) { done_seq[s] = tag >> 2; continue; }    // not one of this event's CTAs
         }

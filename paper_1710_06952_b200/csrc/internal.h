@@ -84,6 +84,7 @@ struct EngineParams {
   int fuse;                        // fuse a due passive local step into the pair that holds its lock
   unsigned long long fuse_wait_ns; // a due passive stays absorbable this long before stepping alone
   int coop;                        // cooperative cross-GPU events (both GPUs process the tiles)
+  int reserve;                     // world > 1: cross events on a fixed CTA range, local events on the rest
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);

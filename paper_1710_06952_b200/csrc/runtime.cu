@@ -664,6 +664,7 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
     coop = c->world == 2 || few_cross || (mode == 0 && mx > 2 * mn);
   }
   p.coop = (c->world > 1 && coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
+  p.reserve = (c->world > 1 && p.variant != 1 && !p.two_sided) ? 1 : 0;
   int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
   if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
@@ -1702,6 +1703,7 @@ adpsgd_status adpsgd_get_stats(adpsgd_ctx* c, adpsgd_stats* o) {
     }
     o->local_nvlink_bytes = g.st_nvl_bytes;
     o->engine_busy_ns = (double)g.st_busy_ns;
+    o->engine_busy_cross_ns = (double)g.st_busy_cross_ns;
     return ADPSGD_OK;
   })
 }
@@ -1712,7 +1714,7 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* c) {
     CU(cudaDeviceSynchronize());
     GlobalCtl g;
     CU(cudaMemcpy(&g, c->gctl, sizeof g, cudaMemcpyDeviceToHost));
-    g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = 0;
+    g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = g.st_busy_cross_ns = 0;
     g.st_bytes = g.st_nvl_bytes = 0.0;
     CU(cudaMemcpy(c->gctl, &g, sizeof g, cudaMemcpyHostToDevice));
     for (int l = 0; l < c->n_local; ++l) CU(cudaMemset(&c->ctl[l].peer_bytes, 0, sizeof(double)));
