@@ -109,12 +109,13 @@ class ClockSampler:
 def traffic_per_launch(alg_bytes):
     """DRAM bytes per engine launch: the dram/algorithmic ratio of the committed
     ncu --set full capture (profiles/engine_traffic.json) times this launch's
-    algorithmic bytes; None if no capture is committed."""
+    algorithmic bytes, and the capture it came from; (None, None) if no capture
+    is committed."""
     try:
         t = json.load(open(os.path.join(ROOT, "profiles", "engine_traffic.json")))
-        return {"bytes": alg_bytes * t["dram_bytes_per_algorithmic_byte"], "source": t["source"]}
+        return alg_bytes * t["dram_bytes_per_algorithmic_byte"], t["source"]
     except Exception:
-        return None
+        return None, None
 
 
 def peaks():
@@ -675,6 +676,7 @@ def main():
         cpu = {"value": pairs_c / dt_c, "unit": "gossip-steps/s", "cores": 1, "kind": "oracle",
                "sample": f"{a.cpu_events} iid events (ring n={n}, d={d}) of the oracle's Alg. 1 replay"}
 
+    traffic_bytes, traffic_src = traffic_per_launch(loc_bytes / a.steps)
     line = {
         "metric": "gossip-steps/s", "value": gossip_s, "unit": "gossip-steps/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
@@ -693,7 +695,7 @@ def main():
                    "note": "this workload's block placement: one ring edge per GPU boundary crosses NVLink; "
                            "the all-cross figure is under all_cross (extras.nvlink_stress)"},
         "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic_per_launch(loc_bytes / a.steps),
+                     "frac": achieved / hbm_peak, "traffic": traffic_bytes, "traffic_source": traffic_src,
                      "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "clocks": clocks,
