@@ -1,6 +1,6 @@
 /*
  * adpsgd.h -- C ABI of the B200-native AD-PSGD hot path (arXiv 1710.06952).
- * ABI version 2.  Implemented by paper_1710_06952_b200/libadpsgd.so (sm_100a).
+ * ABI version 3.  Implemented by paper_1710_06952_b200/libadpsgd.so (sm_100a).
  *
  * Citations: P:n = PAPER.md line n, S:n = SPEC.md line n.
  *
@@ -12,12 +12,16 @@
  * Problem statement: min_x f(x) = sum_i p_i f_i(x), f_i = E_xi F_i(x; xi)
  * (Eq. 1); all workers see all data (Strategy-1).
  *
- * PROCESS MODEL.  One context per process, one GPU per context
- * (cfg.device).  n workers are placed on world_size ranks (cfg.placement).  With
- * world_size > 1 the ranks exchange opaque peer blobs (adpsgd_export_peer_info ->
- * any transport -> adpsgd_import_peer_info) and call adpsgd_connect; peers'
- * model and control memory is then mapped over NVLink (CUDA IPC) and the fused
- * kernels read/write neighbours' models directly.
+ * PROCESS MODEL.  One context per rank, one GPU per context (cfg.device).  n
+ * workers are placed on world_size ranks (cfg.placement).  With world_size > 1
+ * the ranks exchange opaque peer blobs (adpsgd_export_peer_info -> any
+ * transport -> adpsgd_import_peer_info) and call adpsgd_connect; peers' model
+ * and control memory is then mapped over NVLink (CUDA IPC) and the fused
+ * kernels read/write neighbours' models directly.  Production: one process per
+ * GPU, NCCL collectives.  cfg.comm_local = 1: the ranks are host threads of one
+ * process (e.g. several virtual ranks on ONE GPU, which runs the same
+ * cross-rank protocol -- remote locks, mailboxes, tickets -- with local
+ * pointers); collectives are in-process fixed-order reductions.
  *
  * ERRORS.  Every call returns adpsgd_status; nothing throws, aborts or exits
  * across the ABI.  Out-params are written only on ADPSGD_OK.  Asynchronous
@@ -45,7 +49,7 @@
 extern "C" {
 #endif
 
-#define ADPSGD_ABI_VERSION 2
+#define ADPSGD_ABI_VERSION 3
 
 typedef struct adpsgd_ctx adpsgd_ctx;
 typedef void* adpsgd_stream;
@@ -152,6 +156,18 @@ typedef struct {
                               /* or when GPUs start cross events unevenly; off when nearly     */
                               /* every edge crosses with initiators spread evenly), 1 = on,    */
                               /* -1 = off                                                      */
+  /* --- in-process ranks (appended in ABI version 3) --- */
+  int32_t comm_local;         /* 0: one process per rank -- peers mapped with CUDA IPC, NCCL    */
+                              /*    collectives (the production path);                          */
+                              /* 1: the world_size ranks are host threads of ONE process (any   */
+                              /*    devices, several ranks may share one GPU): peers' memory is */
+                              /*    addressed directly and collectives are fixed-order device   */
+                              /*    reductions between host barriers (comm.h).  adpsgd_connect's*/
+                              /*    id is then any 128-byte token common to the group, and each */
+                              /*    rank's calls must come from its own host thread.            */
+  int32_t engine_grid;        /* engine CTAs per rank; 0 = ctas_per_sm x SMs, divided by        */
+                              /* world_size when comm_local (ranks sharing a GPU must all be    */
+                              /* resident).  Must be equal on every rank.                       */
 } adpsgd_config;
 
 /* A schedule event (reading R5): worker i makes the gradient update; j is its

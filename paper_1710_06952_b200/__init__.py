@@ -61,7 +61,8 @@ class Config(C.Structure):
                 ("wait_free", C.c_int32), ("reserved0", C.c_int32),
                 ("link_slow", C.c_void_p), ("link_ns", C.c_int64),
                 ("engine_no_fuse", C.c_int32), ("reserved1", C.c_int32), ("engine_fuse_wait_ns", C.c_int64),
-                ("super_R", C.c_int32), ("engine_coop", C.c_int32)]
+                ("super_R", C.c_int32), ("engine_coop", C.c_int32),
+                ("comm_local", C.c_int32), ("engine_grid", C.c_int32)]
 
 
 class Event(C.Structure):
@@ -174,6 +175,72 @@ def exchange_peer_blobs(mine: bytes, rank: int, world: int, make_nccl_id=None, p
     return allb, obj[0]
 
 
+class ThreadGroup:
+    """In-process rank group for comm_local contexts (include/adpsgd.h): the
+    ranks are host threads of this process; this object carries the wiring
+    exchange (peer blobs, the group token) between them, the role
+    torch.distributed plays for one-process-per-GPU ranks."""
+
+    def __init__(self, world):
+        import threading
+        self.world = int(world)
+        self._bar = threading.Barrier(self.world)
+        self._buf = [None] * self.world
+
+    def barrier(self, timeout=600):
+        self._bar.wait(timeout)
+
+    def abort(self):
+        """Break the barrier: ranks waiting in it raise instead of hanging."""
+        self._bar.abort()
+
+    def all_gather_object(self, out, obj, rank):
+        self._buf[rank] = obj
+        self.barrier()
+        out[:] = list(self._buf)
+        self.barrier()
+
+    def broadcast_object(self, obj, src, rank):
+        if rank == src:
+            self._buf[src] = obj
+        self.barrier()
+        v = self._buf[src]
+        self.barrier()
+        return v
+
+
+def run_ranks(world, fn, timeout=1800, group=None):
+    """Run fn(rank) on `world` host threads (one per in-process rank); re-raise
+    the first exception (a failing rank aborts `group`'s barrier so the others
+    do not wait for it).  ctypes releases the GIL inside every library call."""
+    import threading
+    res, errs = [None] * world, [None] * world
+
+    def body(r):
+        try:
+            res[r] = fn(r)
+        except BaseException as ex:  # surfaced below
+            errs[r] = ex
+            if group is not None:
+                group.abort()
+
+    ts = [threading.Thread(target=body, args=(r,), daemon=True) for r in range(world)]
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join(timeout)
+    import threading as _th
+    for r, ex in enumerate(errs):       # the root cause first, not a broken barrier
+        if ex is not None and not isinstance(ex, _th.BrokenBarrierError):
+            raise RuntimeError(f"in-process rank {r} failed: {ex!r}") from ex
+    for r, ex in enumerate(errs):
+        if ex is not None:
+            raise RuntimeError(f"in-process rank {r} failed: {ex!r}") from ex
+    if any(t.is_alive() for t in ts):
+        raise TimeoutError("in-process ranks did not finish")
+    return res
+
+
 def gemm_tf32x3(A_ptr, B_ptr, C_ptr, M, N, K, splits=1):
     """Diagnostics: C = A . B^T on tcgen05 (3xTF32), device pointers (see adpsgd.h)."""
     _chk(lib().adpsgd_gemm_tf32x3(C.c_void_p(A_ptr), C.c_void_p(B_ptr), C.c_void_p(C_ptr), M, N, K, splits),
@@ -196,7 +263,7 @@ class Context:
                  mlp_dims=(0, 0, 0), x0=None, x0_per_worker=None, straggler=None, compute_ns=0,
                  engine_ctas_per_sm=0, engine_variant=0, log_capacity=0, wait_free=0, link_slow=None, link_ns=0,
                  engine_fuse=True, engine_fuse_wait_ns=0, super_R=0, engine_coop=None, connect=True,
-                 pg=None):
+                 pg=None, group=None, engine_grid=0):
         self.n, self.d, self.rank, self.world = int(n), int(d), int(rank), int(world_size)
         e = _arr(np.asarray(edges).reshape(-1, 2), np.int32)
         r = _arr(role, np.int8)
@@ -228,11 +295,17 @@ class Context:
         cfg.engine_fuse_wait_ns = int(engine_fuse_wait_ns)
         cfg.super_R = int(super_R)
         cfg.engine_coop = 0 if engine_coop is None else (1 if engine_coop else -1)   # None = auto
+        cfg.comm_local = 1 if group is not None else 0       # in-process ranks (ThreadGroup)
+        cfg.engine_grid = int(engine_grid)
+        self.group = group
         h = C.c_void_p()
         _chk(lib().adpsgd_init(C.byref(g), self.n, self.d, C.byref(cfg), C.byref(h)), "adpsgd_init")
         self._h = h
         if world_size > 1 and connect:
-            self.connect_distributed(pg)
+            if group is not None:
+                self.connect_local(group)
+            else:
+                self.connect_distributed(pg)
 
     # ---------------------------------------------------------- lifecycle --
     def connect_distributed(self, pg=None):
@@ -257,6 +330,26 @@ class Context:
         nid2 = (C.c_ubyte * 128).from_buffer_copy(nccl_id)
         _chk(lib().adpsgd_connect(self._h, nid2), "connect")
         dist.barrier(group=pg)
+
+    def _export(self):
+        sz = C.c_int64()
+        _chk(lib().adpsgd_peer_info_size(C.byref(sz)), "peer_info_size")
+        buf = (C.c_ubyte * sz.value)()
+        n = C.c_int64()
+        _chk(lib().adpsgd_export_peer_info(self._h, buf, sz.value, C.byref(n)), "export_peer_info")
+        return bytes(buf[:n.value])
+
+    def connect_local(self, group):
+        """In-process ranks (comm_local): exchange raw-pointer peer blobs and a
+        random group token through a ThreadGroup; call from this rank's thread."""
+        allb = [None] * self.world
+        group.all_gather_object(allb, self._export(), self.rank)
+        for r, blob in enumerate(allb):
+            if r != self.rank:
+                _chk(lib().adpsgd_import_peer_info(self._h, r, blob, len(blob)), "import_peer_info")
+        tok = group.broadcast_object(os.urandom(128) if self.rank == 0 else None, 0, self.rank)
+        _chk(lib().adpsgd_connect(self._h, (C.c_ubyte * 128).from_buffer_copy(tok)), "connect")
+        group.barrier()
 
     def destroy(self):
         if getattr(self, "_h", None):

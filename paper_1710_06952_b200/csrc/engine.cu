@@ -821,14 +821,17 @@ int engine_max_ctas_per_sm(int threads, int variant) {
   return n;
 }
 
-cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s) {
+cudaError_t launch_engine(const EngineParams& p, int grid, int threads, bool cooperative, cudaStream_t s) {
   EngineParams pp = p;
   void* args[] = {&pp};
   if (threads != kEngineThreads || grid > kMaxGrid) return cudaErrorInvalidValue;
   size_t smem = 0;
   const void* fn = engine_fn(p.variant, &smem);
   if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  if (cooperative) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s);
 }
+
+const void* engine_module_anchor() { return (const void*)k_engine<0>; }
 
 }  // namespace adp

@@ -240,4 +240,6 @@ cudaError_t launch_gemm_tf32x3(const GemmOperands& op, float* C, int M, int N, i
   return cudaGetLastError();
 }
 
+const void* gemm_module_anchor() { return (const void*)k_sum_planes; }
+
 }  // namespace adp

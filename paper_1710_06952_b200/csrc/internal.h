@@ -87,14 +87,14 @@ struct EngineParams {
   int reserve;                     // world > 1: cross events on a fixed CTA range, local events on the rest
 };
 
-cudaError_t launch_engine(const EngineParams& p, int grid, int threads, cudaStream_t s);
+cudaError_t launch_engine(const EngineParams& p, int grid, int threads, bool cooperative, cudaStream_t s);
 int engine_max_ctas_per_sm(int threads, int variant);
 
 // ---------------------------------------------------- standalone kernels ----
 // Pair/local update with external, inline-quadratic, snapshot-quadratic or no gradient.
 cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat, long long d,
                          long long n4, float gamma, const QuadParams& q, unsigned long long k,
-                         int grad_mode, cudaStream_t s);
+                         int grad_mode, cudaStream_t s, const unsigned long long* guard = nullptr);
 cudaError_t launch_quad_grad(const float* xhat, float* g, long long d, long long n4,
                              const QuadParams& q, unsigned long long k, cudaStream_t s);
 // lsq (kind 3) / logreg (kind 4): g = sum_m grad F(xhat; (A[idx_m], b[idx_m]))
@@ -163,5 +163,12 @@ cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch);
 cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx,
                             uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s);
 constexpr int kMlpLaunches = 7;
+
+// one kernel of each translation unit (CUDA module), see preload_modules()
+const void* kernels_module_anchor();
+const void* engine_module_anchor();
+const void* gemm_module_anchor();
+const void* mlp_module_anchor();
+const void* comm_module_anchor();
 
 }  // namespace adp

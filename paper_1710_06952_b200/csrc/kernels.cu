@@ -39,7 +39,9 @@ int stream_grid(long long n4) {
 template <bool kPair, int kGrad, bool kFF = false>
 __global__ void __launch_bounds__(kThreads, 2) k_event(float* xi, float* xj, const float* g,
                                                     const float* xhat, long long d, long long n4,
-                                                    float gamma, QuadParams q, uint32_t kk) {
+                                                    float gamma, QuadParams q, uint32_t kk,
+                                                    const unsigned long long* guard) {
+  if (guard && *guard == ~0ull) return;     // the event's lock wait timed out (error latched): skip
   const long long per = (n4 + gridDim.x - 1) / gridDim.x;
   const long long lo = (long long)blockIdx.x * per;
   const long long hi = lo + per < n4 ? lo + per : n4;
@@ -509,15 +511,15 @@ __global__ void k_super_commit(LogEntry* log, long long log_cap, const unsigned 
 
 template <bool P, int G>
 cudaError_t ev(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
-               float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s) {
-  k_event<P, G><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk);
+               float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s, const unsigned long long* guard) {
+  k_event<P, G><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk, guard);
   return cudaGetLastError();
 }
 
 template <int G>
 cudaError_t ev_ff(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
-                  float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s) {
-  k_event<true, G, true><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk);
+                  float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s, const unsigned long long* guard) {
+  k_event<true, G, true><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk, guard);
   return cudaGetLastError();
 }
 
@@ -526,30 +528,30 @@ cudaError_t ev_ff(float* xi, float* xj, const float* g, const float* xh, long lo
 // k: random-draw key of the gradient (the event's k, or read_key for App. A events)
 cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat, long long d,
                          long long n4, float gamma, const QuadParams& q, unsigned long long k,
-                         int grad_mode, cudaStream_t s) {
+                         int grad_mode, cudaStream_t s, const unsigned long long* guard) {
   const uint32_t kk = quad_event_key_h(q.noise_key, k);
   const bool pair = xj != nullptr;
   if ((grad_mode & kModeFlushFirst) && pair) {     // App. A order; a local flush is Alg. 1's local step
     switch (grad_mode & 0xf) {
-      case kGradNone: return ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
-      case kGradExternal: return ev_ff<kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
-      case kGradQuadInline: return ev_ff<kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      case kGradNone: return ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
+      case kGradExternal: return ev_ff<kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
+      case kGradQuadInline: return ev_ff<kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
       default: return cudaErrorInvalidValue;
     }
   }
   switch (grad_mode & 0xf) {
     case kGradNone:
-      return pair ? ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
+      return pair ? ev<true, kGradNone>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard)
                   : cudaSuccess;
     case kGradExternal:
-      return pair ? ev<true, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
-                  : ev<false, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      return pair ? ev<true, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard)
+                  : ev<false, kGradExternal>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
     case kGradQuadInline:
-      return pair ? ev<true, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
-                  : ev<false, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      return pair ? ev<true, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard)
+                  : ev<false, kGradQuadInline>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
     case kGradQuadSnapshot:
-      return pair ? ev<true, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s)
-                  : ev<false, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s);
+      return pair ? ev<true, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard)
+                  : ev<false, kGradQuadSnapshot>(xi, xj, g, xhat, d, n4, gamma, q, kk, s, guard);
   }
   return cudaErrorInvalidValue;
 }
@@ -613,7 +615,8 @@ cudaError_t launch_consensus_finalize(const double* sum, int n, long long d, flo
 
 cudaError_t launch_consensus_fused(const float* X, int n_rows, long long d_pad, long long d, int n, float* out,
                                    double* acc, unsigned int* err, cudaStream_t s) {
-  if (d % 4 == 0 && d_pad % 4 == 0 && n_rows >= 1 && n_rows <= 8) {
+  // float4 form: the caller's out (any d floats, ABI) must be 16-byte aligned for it
+  if (d % 4 == 0 && d_pad % 4 == 0 && n_rows >= 1 && n_rows <= 8 && (reinterpret_cast<uintptr_t>(out) & 15) == 0) {
     const float4* X4 = reinterpret_cast<const float4*>(X);
     float4* o4 = reinterpret_cast<float4*>(out);
     const int g = 4 * sm_count();
@@ -693,5 +696,8 @@ cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d,
   k_init_rows<<<4 * sm_count(), 256, 0, s>>>(X, n_rows, d_pad, d, x0);
   return cudaGetLastError();
 }
+
+// one kernel of this translation unit (module), for preload_modules()
+const void* kernels_module_anchor() { return (const void*)k_set_u64; }
 
 }  // namespace adp

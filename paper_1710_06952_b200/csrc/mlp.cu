@@ -214,4 +214,6 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   return cudaGetLastError();
 }
 
+const void* mlp_module_anchor() { return (const void*)k_mlp_idx; }
+
 }  // namespace adp

@@ -14,8 +14,10 @@
 #include <vector>
 
 #include <nccl.h>
+#include <unistd.h>
 
 #include "../../include/adpsgd.h"
+#include "comm.h"
 #include "internal.h"
 
 using namespace adp;
@@ -43,6 +45,12 @@ adpsgd_status fail(adpsgd_status s, const std::string& m) {
     if (r_ != ncclSuccess)                                                             \
       return fail(ADPSGD_E_NCCL, std::string(#x) + ": " + ncclGetErrorString(r_));     \
   } while (0)
+#define CO(x)                                                                          \
+  do {                                                                                 \
+    std::string m_;                                                                    \
+    const int r_ = (x);                                                                \
+    if (r_ != 0) return fail((adpsgd_status)r_, m_.empty() ? std::string(#x) : m_);    \
+  } while (0)
 #define ST(x)                                                                          \
   do {                                                                                 \
     adpsgd_status s_ = (x);                                                            \
@@ -60,6 +68,9 @@ struct PeerBlob {
   int64_t gctl_offset, log_offset, log_cap, pcnt_offset, slots_offset;
   int32_t has_land, engine_grid;
   cudaIpcMemHandle_t models, ctl, land;
+  // in-process ranks (cfg.comm_local): raw device addresses, valid in this process
+  int32_t local, device;
+  uint64_t pid, models_ptr, ctl_ptr, land_ptr;
 };
 
 uint64_t splitmix64(uint64_t& s) {
@@ -157,10 +168,11 @@ struct adpsgd_ctx {
   unsigned long long dp_k = 0;
   std::vector<int> dp_halo_w;                     // remote rows received each round (ascending id)
   std::vector<std::pair<int, int>> dp_send;       // (local worker, destination rank), ascending id
-  ncclComm_t comm = nullptr;
+  Comm* comm = nullptr;              // NCCL (processes) or in-process (threads), comm.h
+  bool comm_local = false;           // ranks are host threads of this process (cfg.comm_local)
   bool connected = false;
   // super-learner mode (reading R22): this rank's group communicator and buffers
-  ncclComm_t super_comm = nullptr;
+  Comm* super_comm = nullptr;
   int super_R = 0;
   float* super_g = nullptr;                        // learner gradient, then the group's sum
   unsigned long long* super_k = nullptr;           // ticket broadcast by the group leader
@@ -305,16 +317,19 @@ adpsgd_status read_ticket(adpsgd_ctx* c, unsigned long long* k) {
 
 // Multi-GPU adpsgd_step moves the device counter under every rank, so at the
 // start of a collective call (world > 1) the ranks agree on it: each reads the
-// device ticket after its own work has drained, then an NCCL all-reduce (MIN)
-// -- no rank can launch the collective's engine before every rank has
-// contributed its read, so all reads see the same settled value.
+// device ticket after its own work has drained, then an all-reduce (MAX).  A
+// rank's read follows all of its own steps, so the latest read -- the maximum
+// -- covers every ticket taken; no rank can launch the collective's engine
+// before every rank has contributed its read.  The read is a stream-ordered
+// copy on c->stream, the stream the all-reduce runs on.
 adpsgd_status settle_ticket(adpsgd_ctx* c) {
   if (c->world == 1 || !c->comm) return ADPSGD_OK;
   CU(cudaStreamSynchronize(c->stream));
   CU(cudaDeviceSynchronize());
   if (!c->agree64) CU(cudaMalloc(&c->agree64, sizeof(unsigned long long)));
-  CU(cudaMemcpy(c->agree64, &c->gctl0->ticket, sizeof(unsigned long long), cudaMemcpyDeviceToDevice));
-  NC(ncclAllReduce(c->agree64, c->agree64, 1, ncclUint64, ncclMin, c->comm, c->stream));
+  CU(cudaMemcpyAsync(c->agree64, &c->gctl0->ticket, sizeof(unsigned long long), cudaMemcpyDeviceToDevice,
+                     c->stream));
+  CO(c->comm->allreduce(c->agree64, c->agree64, 1, DType::U64, ROp::Max, c->stream, m_));
   unsigned long long t = 0;
   CU(cudaMemcpyAsync(&t, c->agree64, sizeof t, cudaMemcpyDeviceToHost, c->stream));
   CU(cudaStreamSynchronize(c->stream));
@@ -623,8 +638,6 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.compute_ns = c->compute_ns;
   p.seed = make_uint2((uint32_t)(c->seed ^ 0x5bd1e995u), (uint32_t)(c->seed >> 32) ^ c->run_counter);
   p.watchdog_ns = 60ull * 1000000000ull;
-  int dev_sms = 0;
-  CU(cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, c->device));
   p.variant = c->engine_variant;
   // variant 3 = variant 0 with the two-sided push protocol for cross-GPU pairs.
   // tools/ab_nvlink.py (2 B200, every event cross-GPU): one-sided 604/616 GB/s
@@ -665,15 +678,13 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   }
   p.coop = (c->world > 1 && coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
   p.reserve = (c->world > 1 && p.variant != 1 && !p.two_sided) ? 1 : 0;
-  int occ = engine_max_ctas_per_sm(c->engine_threads, p.variant);
-  if (occ < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
-  int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
-  const int grid = cps * dev_sms;
-  // the two-sided protocol pairs CTA b of both GPUs tile by tile: same grid everywhere
-  if ((p.two_sided || p.coop) && c->engine_grid && grid != c->engine_grid)
-    return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (two-sided NVLink protocol)");
+  // the grid is fixed at init (and checked equal across ranks at import: the
+  // cooperative and two-sided protocols pair CTA b of both GPUs tile by tile)
+  if (c->engine_grid < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
-  CU(launch_engine(p, grid, c->engine_threads, s));
+  // processes: a cooperative launch guarantees co-residency of the grid; in-process
+  // ranks sharing a device launch normally (their grids together fit the device)
+  CU(launch_engine(p, c->engine_grid, c->engine_threads, !c->comm_local, s));
   ++c->launches;
   ++c->run_counter;
   return ADPSGD_OK;
@@ -780,9 +791,9 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   if (!c) return ADPSGD_OK;
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
-  if (c->super_comm) ncclCommDestroy(c->super_comm);
-  if (c->comm) ncclCommDestroy(c->comm);
-  for (size_t r = 0; r < c->peer_models.size(); ++r) {
+  delete c->super_comm;
+  delete c->comm;
+  for (size_t r = 0; r < c->peer_models.size() && !c->comm_local; ++r) {
     if ((int)r == c->rank) continue;
     if (c->peer_models[r]) cudaIpcCloseMemHandle(c->peer_models[r]);
     if (c->peer_ctl[r]) cudaIpcCloseMemHandle(c->peer_ctl[r]);
@@ -799,6 +810,47 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   for (void* b : bufs) if (b) cudaFree(b);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
+  return ADPSGD_OK;
+}
+
+// Load every kernel of the library on the current device now.  Under lazy
+// module loading (the CUDA 12 default) a kernel's first launch loads it, and
+// loading can wait for the device to drain -- which never happens while another
+// rank's kernel on the same device spins on work this launch belongs to (a peer
+// lock kernel waiting for our commit, a cooperative engine).  Each translation
+// unit is one module: enumerate its functions from one anchor kernel.
+adpsgd_status preload_modules(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;
+  std::lock_guard<std::mutex> lk(mu);
+  if (std::find(done.begin(), done.end(), device) != done.end()) return ADPSGD_OK;
+  using FnGetModule = CUresult (*)(CUmodule*, CUfunction);
+  using FnCount = CUresult (*)(unsigned int*, CUmodule);
+  using FnEnum = CUresult (*)(CUfunction*, unsigned int, CUmodule);
+  using FnLoad = CUresult (*)(CUfunction);
+  void *p_mod = nullptr, *p_cnt = nullptr, *p_enum = nullptr, *p_load = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  CU(cudaGetDriverEntryPointByVersion("cuFuncGetModule", &p_mod, 12040, cudaEnableDefault, &q));
+  CU(cudaGetDriverEntryPointByVersion("cuModuleGetFunctionCount", &p_cnt, 12040, cudaEnableDefault, &q));
+  CU(cudaGetDriverEntryPointByVersion("cuModuleEnumerateFunctions", &p_enum, 12040, cudaEnableDefault, &q));
+  CU(cudaGetDriverEntryPointByVersion("cuFuncLoad", &p_load, 12040, cudaEnableDefault, &q));
+  if (!p_mod || !p_cnt || !p_enum || !p_load) return fail(ADPSGD_E_UNSUPPORTED, "driver lacks module enumeration");
+  const void* anchors[] = {kernels_module_anchor(), engine_module_anchor(), gemm_module_anchor(),
+                           mlp_module_anchor(), comm_module_anchor()};
+  for (const void* a : anchors) {
+    cudaFunction_t f = nullptr;
+    CU(cudaGetFuncBySymbol(&f, a));          // loads the anchor, yields its module
+    CUmodule mod = nullptr;
+    unsigned int cnt = 0;
+    if (((FnGetModule)p_mod)(&mod, (CUfunction)f) != CUDA_SUCCESS || ((FnCount)p_cnt)(&cnt, mod) != CUDA_SUCCESS)
+      return fail(ADPSGD_E_CUDA, "module enumeration failed");
+    std::vector<CUfunction> fns(cnt);
+    if (cnt && ((FnEnum)p_enum)(fns.data(), cnt, mod) != CUDA_SUCCESS)
+      return fail(ADPSGD_E_CUDA, "module enumeration failed");
+    for (CUfunction fn : fns)
+      if (((FnLoad)p_load)(fn) != CUDA_SUCCESS) return fail(ADPSGD_E_CUDA, "cuFuncLoad failed");
+  }
+  done.push_back(device);
   return ADPSGD_OK;
 }
 
@@ -838,6 +890,8 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->super_R = cfg->super_R > 1 ? cfg->super_R : 0;
   c->engine_fuse = cfg->engine_no_fuse ? 0 : 1;
   c->engine_coop = cfg->engine_coop;
+  c->comm_local = cfg->comm_local != 0;
+  if (cfg->engine_grid < 0) return fail(ADPSGD_E_INVALID, "engine_grid < 0");
   if (c->engine_coop < -1 || c->engine_coop > 1) return fail(ADPSGD_E_INVALID, "engine_coop must be -1, 0 or 1");
   c->fuse_wait_ns = cfg->engine_fuse_wait_ns;
   if (c->fuse_wait_ns < 0) return fail(ADPSGD_E_INVALID, "engine_fuse_wait_ns < 0");
@@ -887,6 +941,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     if (c->M > 1024) return fail(ADPSGD_E_UNSUPPORTED, "batch_M > 1024");
   }
   CU(cudaSetDevice(c->device));
+  ST(preload_modules(c->device));
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
   // models
   CU(cudaMalloc(&c->models, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
@@ -964,6 +1019,11 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     const int occ = engine_max_ctas_per_sm(c->engine_threads, c->engine_variant);
     const int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
     c->engine_grid = cps * sms;
+    // in-process ranks may share one device: by default each takes 1/world of it
+    // so that every rank's persistent engine is resident at once
+    if (c->comm_local && c->world > 1) c->engine_grid = std::max(1, c->engine_grid / c->world);
+    if (cfg->engine_grid > 0) c->engine_grid = std::min(c->engine_grid, (int)cfg->engine_grid);
+    if (c->engine_grid > kMaxGrid) c->engine_grid = kMaxGrid;
   }
   c->peer_models[c->rank] = c->models;
   c->peer_ctl[c->rank] = c->ctl_arena;
@@ -1038,6 +1098,12 @@ adpsgd_status adpsgd_export_peer_info(adpsgd_ctx* c, void* buf, int64_t cap, int
     CU(cudaIpcGetMemHandle(&b.ctl, c->ctl_arena));
     b.has_land = c->land ? 1 : 0;
     if (c->land) CU(cudaIpcGetMemHandle(&b.land, c->land));
+    b.local = c->comm_local ? 1 : 0;
+    b.device = c->device;
+    b.pid = (uint64_t)getpid();
+    b.models_ptr = (uint64_t)(uintptr_t)c->models;
+    b.ctl_ptr = (uint64_t)(uintptr_t)c->ctl_arena;
+    b.land_ptr = (uint64_t)(uintptr_t)c->land;
     memcpy(buf, &b, sizeof b);
     if (n_out) *n_out = (int64_t)sizeof b;
     return ADPSGD_OK;
@@ -1054,6 +1120,33 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
     memcpy(&b, buf, sizeof b);
     if (b.magic != kBlobMagic || b.rank != rank || b.d_pad != c->d_pad)
       return fail(ADPSGD_E_INVALID, "peer blob mismatch (magic/rank/d)");
+    if (b.engine_grid != c->engine_grid)
+      return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (different GPU models?)");
+    if (c->comm_local) {
+      // in-process rank: its memory is addressable here as is (same device, or a
+      // peer device once peer access is enabled)
+      if (!b.local || b.pid != (uint64_t)getpid())
+        return fail(ADPSGD_E_INVALID, "comm_local: peer blob is not from an in-process rank");
+      if (b.device != c->device) {
+        cudaError_t pe = cudaDeviceEnablePeerAccess(b.device, 0);
+        if (pe == cudaErrorPeerAccessAlreadyEnabled) cudaGetLastError();
+        else if (pe != cudaSuccess)
+          return fail(ADPSGD_E_UNSUPPORTED, std::string("peer access: ") + cudaGetErrorString(pe));
+      }
+      c->peer_models[rank] = reinterpret_cast<float*>((uintptr_t)b.models_ptr);
+      c->peer_ctl[rank] = reinterpret_cast<char*>((uintptr_t)b.ctl_ptr);
+      c->peer_land[rank] = b.has_land ? reinterpret_cast<float*>((uintptr_t)b.land_ptr) : nullptr;
+      c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
+      c->peer_slots_off[rank] = (size_t)b.slots_offset;
+      c->peer_imported[rank] = true;
+      if (rank == 0) {
+        c->gctl0 = reinterpret_cast<GlobalCtl*>(c->peer_ctl[0] + b.gctl_offset);
+        c->log0 = reinterpret_cast<LogEntry*>(c->peer_ctl[0] + b.log_offset);
+        c->log_cap = b.log_cap;
+      }
+      return ADPSGD_OK;
+    }
+    if (b.local) return fail(ADPSGD_E_INVALID, "peer blob is from an in-process rank (set comm_local)");
     void* pm = nullptr;
     void* pc = nullptr;
     cudaError_t e = cudaIpcOpenMemHandle(&pm, b.models, cudaIpcMemLazyEnablePeerAccess);
@@ -1066,8 +1159,6 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
     c->peer_ctl[rank] = static_cast<char*>(pc);
     c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
     c->peer_slots_off[rank] = (size_t)b.slots_offset;
-    if (b.engine_grid != c->engine_grid)
-      return fail(ADPSGD_E_UNSUPPORTED, "engine grid differs across ranks (different GPU models?)");
     if (b.has_land) {
       void* pl = nullptr;
       e = cudaIpcOpenMemHandle(&pl, b.land, cudaIpcMemLazyEnablePeerAccess);
@@ -1102,9 +1193,8 @@ adpsgd_status adpsgd_connect(adpsgd_ctx* c, const void* nccl_id) {
     ST(upload_workers(c));
     if (c->world > 1) {
       if (!nccl_id) return fail(ADPSGD_E_INVALID, "nccl_id required when world_size > 1");
-      ncclUniqueId id;
-      memcpy(&id, nccl_id, sizeof id);
-      NC(ncclCommInitRank(&c->comm, c->world, id, c->rank));
+      if (c->comm_local) CO(make_local_comm(nccl_id, c->world, c->rank, c->device, &c->comm, m_));
+      else CO(make_nccl_comm(nccl_id, c->world, c->rank, &c->comm, m_));
     }
     c->connected = true;
     return ADPSGD_OK;
@@ -1154,7 +1244,18 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
     CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
     CU(cudaDeviceSynchronize());
   }
+  // allocate before taking the lock: nothing that may synchronise the device
+  // (which would wait for a peer's lock kernel spinning on our lock) runs under it
+  if (!grad && c->model != ADPSGD_MODEL_QUADRATIC) {
+    if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+    if (c->model == ADPSGD_MODEL_MLP) ST(ensure_mlp_scratch(c, 1));
+  }
   cudaStream_t st = c->use(s);
+  // rows of local workers stay ordered with this context's other streams (as
+  // the single-GPU adpsgd_step / adpsgd_gossip order them)
+  const bool j_local = j >= 0 && c->is_local(j);
+  CU(cudaStreamWaitEvent(st, c->last_evt[w], 0));
+  if (j_local) CU(cudaStreamWaitEvent(st, c->last_evt[j], 0));
   unsigned int* lock = &ctl_of(j >= 0 ? j : w)->lock;
   CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, 20ull * 1000000000ull, st));
   unsigned long long k = 0;
@@ -1167,7 +1268,6 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
     if (c->model == ADPSGD_MODEL_QUADRATIC) {
       mode = kGradQuadInline;
     } else {
-      if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
       float* gb = c->gstep + (long long)c->worker_local[w] * c->d_pad;
       ST(model_grad(c, c->row(w), gb, k, nullptr, st));
       g = gb;
@@ -1176,6 +1276,8 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
   CU(launch_event(c->row(w), j >= 0 ? row_of(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma, c->q, k, mode, st));
   CU(launch_super_commit(c->log0, c->log_cap, c->super_k, w, j, 0u, c->ctl + c->worker_local[w],
                          &c->gctl0->committed, lock, st));
+  CU(cudaEventRecord(c->last_evt[w], st));
+  if (j_local) CU(cudaEventRecord(c->last_evt[j], st));
   c->launches += 3;
   c->ticket_dirty = true;                 // other ranks move the counter too: re-read before the next run
   if (ticket_out) *ticket_out = (int64_t)k;
@@ -1286,17 +1388,17 @@ adpsgd_status adpsgd_consensus_mean(adpsgd_ctx* c, float* out, double* mk_out, a
       }
       return ADPSGD_OK;
     }
-    if (c->world > 1) NC(ncclAllReduce(c->mk_acc, c->mk_acc, 1, ncclFloat64, ncclSum, c->comm, st));
+    if (c->world > 1) CO(c->comm->allreduce(c->mk_acc, c->mk_acc, 1, DType::F64, ROp::Sum, st, m_));
     CU(launch_consensus_sum(c->models, c->n_local, c->d_pad, c->d, c->sum64, st));
     ++c->launches;
-    if (c->world > 1) NC(ncclAllReduce(c->sum64, c->sum64, (size_t)c->d, ncclFloat64, ncclSum, c->comm, st));
+    if (c->world > 1) CO(c->comm->allreduce(c->sum64, c->sum64, (size_t)c->d, DType::F64, ROp::Sum, st, m_));
     CU(launch_consensus_finalize(c->sum64, c->n, c->d, out, &c->gctl->error, st));
     ++c->launches;
     if (mk_out) {
       CU(cudaMemsetAsync(c->mk_acc, 0, sizeof(double), st));
       CU(launch_consensus_mk(c->models, c->n_local, c->d_pad, c->d, c->sum64, c->n, c->mk_acc, st));
       ++c->launches;
-      if (c->world > 1) NC(ncclAllReduce(c->mk_acc, c->mk_acc, 1, ncclFloat64, ncclSum, c->comm, st));
+      if (c->world > 1) CO(c->comm->allreduce(c->mk_acc, c->mk_acc, 1, DType::F64, ROp::Sum, st, m_));
       double acc = 0.0;
       CU(cudaMemcpyAsync(&acc, c->mk_acc, sizeof(double), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
@@ -1345,7 +1447,7 @@ adpsgd_status adpsgd_allreduce_sgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_strea
       if (delay) { CU(launch_delay(delay, st)); ++c->launches; }
       CU(launch_ar_grad_sum(c->xr, c->gsum, c->d, c->n4, c->q, c->ar_k, c->n_local, c->d_local_ids, st));
       if (c->world > 1)
-        NC(ncclAllReduce(c->gsum, c->gsum, (size_t)c->d_pad, ncclFloat32, ncclSum, c->comm, st));
+        CO(c->comm->allreduce(c->gsum, c->gsum, (size_t)c->d_pad, DType::F32, ROp::Sum, st, m_));
       CU(launch_ar_update(c->xr, c->gsum, c->gamma, c->n, c->d, c->n4, st));
       c->launches += 2;
       c->ar_k += (unsigned long long)c->n;
@@ -1457,14 +1559,12 @@ adpsgd_status adpsgd_dpsgd(adpsgd_ctx* c, int64_t n_rounds, adpsgd_stream s) {
       if (delay) { CU(launch_delay(delay, st)); ++c->launches; }     // the round waits for its slowest worker
       float* xin = c->dp_x[c->dp_cur];
       if (c->world > 1) {                                            // halo exchange (synchronous round)
-        NC(ncclGroupStart());
+        std::vector<P2POp> sends, recvs;
         for (size_t h = 0; h < c->dp_halo_w.size(); ++h)
-          NC(ncclRecv(c->dp_halo + (long long)h * c->d_pad, (size_t)c->d_pad, ncclFloat32,
-                      c->worker_rank[c->dp_halo_w[h]], c->comm, st));
+          recvs.push_back({c->dp_halo + (long long)h * c->d_pad, (size_t)c->d_pad, c->worker_rank[c->dp_halo_w[h]]});
         for (auto& ps : c->dp_send)
-          NC(ncclSend(xin + (long long)c->worker_local[ps.first] * c->d_pad, (size_t)c->d_pad, ncclFloat32,
-                      ps.second, c->comm, st));
-        NC(ncclGroupEnd());
+          sends.push_back({xin + (long long)c->worker_local[ps.first] * c->d_pad, (size_t)c->d_pad, ps.second});
+        CO(c->comm->exchange(sends, recvs, st, m_));
       }
       if (c->n_local) {
         CU(launch_dpsgd(c->d_dp_nbr[c->dp_cur], c->d_dp_deg, c->d_dp_wself, c->dp_wnb, xin, c->dp_x[1 - c->dp_cur],
@@ -1512,10 +1612,14 @@ static adpsgd_status super_setup(adpsgd_ctx* c) {
     if (r == 0) c->super_nb[s] = nb;
     else if (nb != c->super_nb[s]) return fail(ADPSGD_E_INVALID, "super_run: learner graphs differ across r");
   }
-  if (R > 1 && !c->super_comm) NC(ncclCommSplit(c->comm, c->rank / R, c->rank % R, &c->super_comm, nullptr));
+  if (R > 1 && !c->super_comm) CO(c->comm->split(c->rank / R, c->rank % R, &c->super_comm, m_));
   if (!c->super_g) {
     CU(cudaMalloc(&c->super_g, sizeof(float) * c->d_pad));
-    CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
+    if (!c->super_k) CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));   // step_multi may own it
+    // MLP scratch now: its first allocation synchronises the device, which must
+    // not happen under a lock (in-process ranks share the device with the
+    // lock kernels spinning on it)
+    if (c->model == ADPSGD_MODEL_MLP) ST(ensure_mlp_scratch(c, 1));
     CU(cudaMalloc(&c->super_bar, sizeof(int)));
     CU(cudaMemset(c->super_bar, 0, sizeof(int)));
     CU(cudaDeviceSynchronize());
@@ -1559,24 +1663,31 @@ adpsgd_status adpsgd_super_run(adpsgd_ctx* c, int64_t n_steps, adpsgd_stream str
       unsigned int* lock = &ctl_of((active ? js : s) * R)->lock;   // the passive side's leader lock
       auto gradient = [&]() -> adpsgd_status {   // learner r's minibatch gradient (device Philox batches)
         ST(model_grad(c, row, c->super_g, key, nullptr, st));
-        if (R > 1) NC(ncclAllReduce(c->super_g, c->super_g, (size_t)c->d_pad, ncclFloat32, ncclSum, c->super_comm, st));
+        if (R > 1) CO(c->super_comm->allreduce(c->super_g, c->super_g, (size_t)c->d_pad, DType::F32, ROp::Sum, st, m_));
         return ADPSGD_OK;
       };
       auto lock_and_share_k = [&]() -> adpsgd_status {
-        if (r == 0) CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, watchdog, st));
-        if (R > 1) NC(ncclBroadcast(c->super_k, c->super_k, 1, ncclUint64, 0, c->super_comm, st));
+        if (r == 0) {
+          CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, watchdog, st));
+          // in-process ranks share the device's hardware queues: nothing that
+          // depends on a spinning lock kernel may be queued behind it, where it
+          // could block the release another rank has queued (as step_multi does)
+          if (c->comm_local) CU(cudaStreamSynchronize(st));
+        }
+        if (R > 1) CO(c->super_comm->broadcast(c->super_k, 1, DType::U64, 0, st, m_));
         return ADPSGD_OK;
       };
       if (active) {                     // gradient first: x_s changes only through s's own events
         ST(gradient());
         ST(lock_and_share_k());
-        CU(launch_event(row, row_of(js * R + r), c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st));
+        CU(launch_event(row, row_of(js * R + r), c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st,
+                        c->super_k));   // skipped if the leader's lock wait timed out
       } else {                          // a passive reads its model under its own lock
         ST(lock_and_share_k());
         ST(gradient());
-        CU(launch_event(row, nullptr, c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st));
+        CU(launch_event(row, nullptr, c->super_g, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradExternal, st, c->super_k));
       }
-      if (R > 1) NC(ncclAllReduce(c->super_bar, c->super_bar, 1, ncclInt32, ncclSum, c->super_comm, st));
+      if (R > 1) CO(c->super_comm->allreduce(c->super_bar, c->super_bar, 1, DType::I32, ROp::Sum, st, m_));
       if (r == 0)
         CU(launch_super_commit(c->log0, c->log_cap, c->super_k, s, js, 0u, ctl_of(s * R), &c->gctl0->committed, lock,
                                st));
@@ -1712,11 +1823,13 @@ adpsgd_status adpsgd_reset_stats(adpsgd_ctx* c) {
   GUARD({
     CTX_CHECK(c);
     CU(cudaDeviceSynchronize());
-    GlobalCtl g;
-    CU(cudaMemcpy(&g, c->gctl, sizeof g, cudaMemcpyDeviceToHost));
-    g.st_events = g.st_pair = g.st_cross = g.st_busy_ns = g.st_busy_cross_ns = 0;
-    g.st_bytes = g.st_nvl_bytes = 0.0;
-    CU(cudaMemcpy(c->gctl, &g, sizeof g, cudaMemcpyHostToDevice));
+    // zero the statistics fields only: ticket, committed, error and abort_flag
+    // live in the same struct and peers may advance rank 0's ticket / committed
+    // (system-scope atomics over NVLink) at any time
+    char* base = reinterpret_cast<char*>(c->gctl);
+    CU(cudaMemset(base + offsetof(GlobalCtl, st_events), 0,
+                  offsetof(GlobalCtl, abort_flag) - offsetof(GlobalCtl, st_events)));
+    CU(cudaMemset(base + offsetof(GlobalCtl, st_busy_cross_ns), 0, sizeof(unsigned long long)));
     for (int l = 0; l < c->n_local; ++l) CU(cudaMemset(&c->ctl[l].peer_bytes, 0, sizeof(double)));
     CU(cudaDeviceSynchronize());
     return ADPSGD_OK;

@@ -1,5 +1,7 @@
-"""Super-learner parity worker (reading R22), launched by
-tests/test_multigpu.py through torch.distributed.run.  For every factorisation
+"""Super-learner parity worker (reading R22), run one process per GPU
+(tests/test_multigpu.py through torch.distributed.run) or as in-process ranks on
+host threads sharing one GPU (comm_local; tests/test_multigpu.py::
+test_virtual_super_learner) -- the same body.  For every factorisation
 world = S * R: R learners per super-learner (NCCL all-reduce of their
 gradients), S super-learners gossiping on a bipartite ring over NVLink.  Checks
 that every super-learner's R replicas are bitwise equal and that the event log,
@@ -10,6 +12,7 @@ import os
 import sys
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import numpy as np
 import torch
@@ -19,10 +22,9 @@ import synth
 import paper_1710_06952_b200 as P
 
 
-def main():
-    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+def body(rank, world, local, G):
+    """G: mp_worker.DistGroup or ThreadRanks.  Returns rank 0's failures."""
+    ckw = G.ctx_kw()
     if rank == 0:
         from oracle import oracle as O
     fails = []
@@ -34,14 +36,13 @@ def main():
         e, role, wr, se, sr = synth.super_ring(S, R)
         Xs0 = synth.x0_uniform(S, d, seed=30 + R)                   # one model per super-learner
         X0 = np.repeat(Xs0, R, axis=0)                               # identical replicas
-        ctx = P.Context(e, world, d, role=role, rank=rank, world_size=world, device=local, placement=2,
+        ctx = P.Context(e, world, d, role=role, rank=rank, world_size=world, device=local, **ckw, placement=2,
                         worker_rank=wr, x0_per_worker=X0, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
                         quad_keys=(dk, nk), quad_noise_s=s_noise, seed=3 + R, super_R=R)
         ctx.super_run(steps)
         ctx.sync()
-        dist.barrier()
-        allm = [None] * world
-        dist.all_gather_object(allm, {w: ctx.read_model(w) for w in ctx.local_workers()})
+        G.barrier()
+        allm = G.all_gather({w: ctx.read_model(w) for w in ctx.local_workers()})
         if rank == 0:
             X = np.zeros((world, d), np.float32)
             for m in allm:
@@ -70,7 +71,7 @@ def main():
                 if S > 1 and not (ev[:, 1] >= 0).any():
                     fails.append(f"S={S} R={R}: no averaging events")
         ctx.destroy()
-        dist.barrier()
+        G.barrier()
     # sampled models (device Philox minibatches keyed by the super-learner key):
     # the tcgen05 MLP (config 3 with one worker per GPU when R = 1) and lsq
     I, H, O_, M, S = 256, 128, 10, 128, 2048
@@ -88,13 +89,12 @@ def main():
             else:
                 dm, x0 = 1024, np.zeros(1024, np.float32)
                 kw = dict(model=P.MODEL_LSQ, gamma=0.02, batch_M=32, data_A=A, data_b=b)
-            ctx = P.Context(e, world, dm, role=role, rank=rank, world_size=world, device=local, placement=2,
+            ctx = P.Context(e, world, dm, role=role, rank=rank, world_size=world, device=local, **ckw, placement=2,
                             worker_rank=wr, x0=x0, seed=seed, super_R=R, **kw)
             ctx.super_run(20)
             ctx.sync()
-            dist.barrier()
-            allm = [None] * world
-            dist.all_gather_object(allm, {w: ctx.read_model(w) for w in ctx.local_workers()})
+            G.barrier()
+            allm = G.all_gather({w: ctx.read_model(w) for w in ctx.local_workers()})
             if rank == 0:
                 X = np.zeros((world, dm), np.float32)
                 for m in allm:
@@ -115,7 +115,16 @@ def main():
                 if len(log) != S_ * 20 or err.max() > 1e-4:
                     fails.append(f"{kind} S={S_} R={R}: {len(log)} events, log replay error {err.max():.2e}")
             ctx.destroy()
-            dist.barrier()
+            G.barrier()
+    return fails
+
+
+def main():
+    from mp_worker import DistGroup
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fails = body(rank, world, local, DistGroup(rank, world))
     if rank == 0:
         print("SUPER", "FAIL" if fails else "OK", fails, flush=True)
     dist.destroy_process_group()

@@ -1,6 +1,12 @@
-"""Multi-process (one rank per GPU) parity worker, launched by tests/test_multigpu.py
-through torch.distributed.run.  Rank 0 compares against the oracle and exits
-non-zero on any mismatch.
+"""Multi-rank parity worker.  Two launchers run the same body:
+  * one process per GPU (tests/test_multigpu.py::test_nvlink_parity through
+    torch.distributed.run; CUDA IPC peers + NCCL);
+  * in-process ranks on host threads (tests/test_multigpu.py::
+    test_virtual_ranks_parity; comm_local contexts, which may all share ONE GPU:
+    the same cross-rank engine protocol -- remote try-locks, cooperative
+    mailboxes, commit flags, tickets -- with local pointers, and fixed-order
+    in-process collectives instead of NCCL).
+Rank 0 compares against the oracle; any mismatch is returned / exits non-zero.
 
 Checks:
   1. engine replay of a pure-gossip schedule whose ring edges cross GPUs
@@ -22,6 +28,7 @@ import hashlib
 import math
 import os
 import sys
+import time
 
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
@@ -33,10 +40,45 @@ import synth
 import paper_1710_06952_b200 as P
 
 
-def gather_models(ctx):
+class DistGroup:
+    """torch.distributed (one process per rank)."""
+
+    def __init__(self, rank, world):
+        self.rank, self.world = rank, world
+
+    def barrier(self):
+        G.barrier()
+
+    def all_gather(self, obj):
+        out = [None] * self.world
+        dist.all_gather_object(out, obj)
+        return out
+
+    def ctx_kw(self):
+        return {}
+
+
+class ThreadRanks:
+    """In-process ranks (P.ThreadGroup): same interface."""
+
+    def __init__(self, tg, rank):
+        self.tg, self.rank, self.world = tg, rank, tg.world
+
+    def barrier(self):
+        self.tg.barrier()
+
+    def all_gather(self, obj):
+        out = [None] * self.world
+        self.tg.all_gather_object(out, obj, self.rank)
+        return out
+
+    def ctx_kw(self):
+        return {"group": self.tg}
+
+
+def gather_models(ctx, G):
     mine = {w: ctx.read_model(w) for w in ctx.local_workers()}
-    allm = [None] * ctx.world
-    dist.all_gather_object(allm, mine)
+    allm = G.all_gather(mine)
     X = np.zeros((ctx.n, ctx.d), np.float32)
     for m in allm:
         for w, x in m.items():
@@ -44,14 +86,16 @@ def gather_models(ctx):
     return X
 
 
+_T0 = time.time()
+
+
 def progress(rank, what):
-    print(f"[rank {rank}] {what}", file=sys.stderr, flush=True)
+    print(f"[rank {rank} {time.time() - _T0:7.1f}s] {what}", file=sys.stderr, flush=True)
 
 
-def main():
-    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
-    torch.cuda.set_device(local)
-    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+def body(rank, world, local, G, full_size=True):
+    """The checks; G is a DistGroup or ThreadRanks.  Returns rank 0's failures."""
+    kw = G.ctx_kw()
     fails = []
     if rank == 0:
         from oracle import oracle as O
@@ -71,16 +115,15 @@ def main():
     if rank == 0:
         Xo, _ = O.replay(O.OracleProblem(), X0, e, r, ev)
     for variant in (3, 0):
-        ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+        ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=1,
                         x0_per_worker=X0, engine_variant=variant)
         ctx.replay(ev, flags=P.REPLAY_ENGINE)
         ctx.sync()
-        dist.barrier()
+        G.barrier()
         st = ctx.stats()
-        X = gather_models(ctx)
-        cross, hbm = [None] * world, [None] * world
-        dist.all_gather_object(cross, st["local_cross_events"])
-        dist.all_gather_object(hbm, st["local_bytes"])
+        X = gather_models(ctx, G)
+        cross = G.all_gather(st["local_cross_events"])
+        hbm = G.all_gather(st["local_bytes"])
         if rank == 0:
             # every pair reads + writes two rows: 16d bytes system-wide, 8d on each GPU's HBM
             if abs(sum(hbm) - 1500 * 16.0 * d) > 1e-6 * 1500 * 16.0 * d or min(hbm) <= 0:
@@ -91,10 +134,10 @@ def main():
                 fails.append(f"expected every event to cross GPUs, got {sum(cross)}")
         if variant == 3:
             ctx.destroy()
-            dist.barrier()
+            G.barrier()
     progress(rank, "1 pure-gossip replay done")
     # 4. consensus mean (NCCL fp64)
-    out = torch.empty(d, dtype=torch.float32, device="cuda")
+    out = torch.empty(d, dtype=torch.float32, device=f"cuda:{local}")
     mk = ctx.consensus_mean(out.data_ptr())
     if rank == 0:
         xo, mko = O.consensus_mean(Xo)
@@ -104,27 +147,27 @@ def main():
         if abs(mk - mko) > 1e-9 * mko:
             fails.append(f"M_k {mk} vs {mko}")
     ctx.destroy()
-    dist.barrier()
+    G.barrier()
 
     progress(rank, "4 consensus done")
     # 2./3. quadratic: engine replay then free-running, block placement
     d = 1 << 20
     ev, _ = synth.schedule_iid(n, e, K=400, seed=8, local_prob=0.3)
-    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=0,
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=0,
                     model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
                     straggler=synth.stragglers(n), compute_ns=20_000, seed=9)
     ctx.replay(ev, flags=P.REPLAY_ENGINE)
     ctx.sync()
-    dist.barrier()
-    X = gather_models(ctx)
+    G.barrier()
+    X = gather_models(ctx, G)
     if rank == 0:
         Xo, _ = O.replay(prob_q, np.zeros((n, d), np.float32), e, r, ev)
         if not np.array_equal(X.view(np.uint32), Xo.view(np.uint32)):
             fails.append("quadratic engine replay (block placement) not bit-exact")
     ctx.run(3000)
     ctx.sync()
-    dist.barrier()
-    X2 = gather_models(ctx)
+    G.barrier()
+    X2 = gather_models(ctx, G)
     if rank == 0:
         log = ctx.read_log(400)
         evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
@@ -140,8 +183,7 @@ def main():
     ctx.dpsgd_reset(X0d)
     ctx.dpsgd(4)
     mine = {w: ctx.dpsgd_read_model(w) for w in ctx.local_workers()}
-    allm = [None] * world
-    dist.all_gather_object(allm, mine)
+    allm = G.all_gather(mine)
     if rank == 0:
         Xd = np.zeros((n, d), np.float32)
         for m in allm:
@@ -159,27 +201,27 @@ def main():
     if rank == 0:
         x = np.zeros(d, np.float32)
         for rr in range(5):
-            G = np.stack([O.gradient(prob_q, x, k=rr * n + w) for w in range(n)])
-            x = O.allreduce_update(x, G, 0.01)
+            Gm = np.stack([O.gradient(prob_q, x, k=rr * n + w) for w in range(n)])
+            x = O.allreduce_update(x, Gm, 0.01)
         if not np.allclose(xa, x, rtol=1e-5, atol=1e-6):
             fails.append(f"allreduce baseline max err {np.abs(xa - x).max()}")
     ctx.destroy()
-    dist.barrier()
+    G.barrier()
 
     progress(rank, "5/6 baselines done")
     # 8. host-driven adpsgd_step across GPUs (device try-lock + ticket, fused pass over
     #    NVLink, commit): ranks step their own workers concurrently; the log replays bitwise
     d = (1 << 14) + 20
     X0s = synth.x0_uniform(n, d, seed=27)
-    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=1,
                     model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
                     x0_per_worker=X0s, seed=13)
     for _ in range(25):
         for w in ctx.local_workers():
             ctx.step(w)
     ctx.sync()
-    dist.barrier()
-    Xs = gather_models(ctx)
+    G.barrier()
+    Xs = gather_models(ctx, G)
     if rank == 0:
         log = ctx.read_log(0)
         evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
@@ -193,11 +235,11 @@ def main():
     progress(rank, "8 steps done")
     ctx.run(200)                                  # the device ticket is settled before the collective run
     ctx.sync()
-    dist.barrier()
+    G.barrier()
     if rank == 0 and ctx.ticket() != 25 * n + 200:
         fails.append(f"ticket after steps + run: {ctx.ticket()}")
     ctx.destroy()
-    dist.barrier()
+    G.barrier()
 
     progress(rank, "8 run after steps done")
     # 7. App. A wait-free engine loop (reading R20), interleave placement: pulls,
@@ -205,14 +247,14 @@ def main():
     #    (tau = k - t_read, FLUSH_FIRST | COMPENSATE) replays bitwise
     d = (1 << 14) + 20
     X0w = synth.x0_uniform(n, d, seed=25)
-    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=1,
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=1,
                     model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
                     x0_per_worker=X0w, straggler=synth.stragglers(n, slow=3.0), compute_ns=30_000, seed=11,
                     wait_free=2)
     ctx.run(2000)
     ctx.sync()
-    dist.barrier()
-    Xw = gather_models(ctx)
+    G.barrier()
+    Xw = gather_models(ctx, G)
     if rank == 0:
         log = ctx.read_log(0)
         evs = np.stack([log["i"], log["j"], log["tau"], log["flags"].astype(np.int32)], 1)
@@ -224,22 +266,23 @@ def main():
             if not np.array_equal(Xw.view(np.uint32), Xwo.view(np.uint32)):
                 fails.append("wait-free multi-GPU log replay not bit-exact")
     ctx.destroy()
-    dist.barrier()
+    G.barrier()
 
     progress(rank, "7 wait-free done")
+    if not full_size:
+        return fails
     # 9. full-size bench workload across GPUs: digests of every row vs the oracle's replay
     d, U = 25_600_000, 32 * world
-    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=0,
+    ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=0,
                     model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
                     straggler=synth.stragglers(n), compute_ns=50_000, seed=17)
     ctx.run(U)
     ctx.sync()
-    dist.barrier()
+    G.barrier()
     mine = {w: hashlib.sha1(ctx.read_model(w).tobytes()).hexdigest() for w in ctx.local_workers()}
     cross = ctx.stats()["local_cross_events"]
-    alld, allc = [None] * world, [None] * world
-    dist.all_gather_object(alld, mine)
-    dist.all_gather_object(allc, cross)
+    alld = G.all_gather(mine)
+    allc = G.all_gather(cross)
     if rank == 0:
         dig = {w: h for m in alld for w, h in m.items()}
         log = ctx.read_log(0)
@@ -256,7 +299,15 @@ def main():
             fails.append("full-size run had no cross-GPU event")
         progress(rank, f"9 full size: {sum(allc)} cross events of {U}")
     ctx.destroy()
-    dist.barrier()
+    G.barrier()
+    return fails
+
+
+def main():
+    rank, world, local = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"]), int(os.environ["LOCAL_RANK"])
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    fails = body(rank, world, local, DistGroup(rank, world))
     if rank == 0:
         print("MULTIGPU", "FAIL" if fails else "OK", fails, flush=True)
     dist.destroy_process_group()

@@ -41,7 +41,7 @@ def test_library_exports_every_declared_symbol(lib):
 
 def test_abi_version_and_error_text(lib):
     import paper_1710_06952_b200 as P
-    assert lib.adpsgd_abi_version() == 2
+    assert lib.adpsgd_abi_version() == 3
     assert isinstance(lib.adpsgd_last_error(), bytes)
     sz = ctypes.c_int64()
     assert lib.adpsgd_peer_info_size(ctypes.byref(sz)) == 0 and sz.value > 64

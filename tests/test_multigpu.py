@@ -41,3 +41,4 @@ def test_super_learner_parity(world):
     r = subprocess.run(cmd, capture_output=True, text=True, timeout=420, cwd=ROOT)
     assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-3000:]
     assert "SUPER OK" in r.stdout
+
