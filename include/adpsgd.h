@@ -174,7 +174,7 @@ typedef struct {
  * averaging partner (must be a neighbour of the other role) or -1 (W_k = I);
  * tau is the staleness of the read, Xhat = X_{k - tau}.                         */
 typedef struct { int32_t i, j, tau; uint32_t flags; } adpsgd_event;
-#define ADPSGD_EV_NO_GRAD 1u   /* pure averaging: W_k only, no gradient update (k still advances) */
+#define ADPSGD_EV_NO_GRAD 1u   /* pure averaging: W_k only, no gradient update (takes a ticket, R23) */
 /* App. A, the wait-free runtime, reading R20:
  * FLUSH_FIRST  the communication thread flushes g into x_i BEFORE averaging
  *              (Alg. 2 order): x_i <- fl(x_i - fl(gamma g));
@@ -237,8 +237,13 @@ adpsgd_status adpsgd_connect(adpsgd_ctx* ctx, const void* nccl_id /* 128 B, NULL
 /* ------------------------------------------------------------- hot path ---- */
 
 /* Pairwise averaging alone (W_k): x_i, x_j <- fl(fl(x_i + x_j)*0.5).
- * i and j must be neighbours of different roles and both local (world 1).
- * Does NOT advance k (no gradient update).                           */
+ * i and j must be neighbours of different roles; i lives on this rank (j may
+ * be remote when world_size > 1: the passive endpoint's lock and the ticket are
+ * then taken on the device, as adpsgd_step does).  Like every pure average
+ * (NO_GRAD events of replays and runs) it takes the next ticket k and is
+ * logged with flags = ADPSGD_EV_NO_GRAD (reading R23: the ticket
+ * counts committed events; the paper's k of P:429-432 counts the events
+ * without NO_GRAD, and staleness tau is measured in ticket units).             */
 adpsgd_status adpsgd_gossip(adpsgd_ctx* ctx, int32_t i, int32_t j, adpsgd_stream s);
 
 /* One AD-PSGD worker iteration for local worker w: gradient at the

@@ -156,7 +156,7 @@ typedef struct {
  * low 16 bits (definition v3).  Every op is
  * one rounded fp32 op (no FMA): this is the workload's definition, so the
  * oracle evaluates it exactly.                                               */
-static uint32_t quad_noise_mix(uint32_t x) {
+uint32_t oracle_quad_noise_mix(uint32_t x) {
   x *= 0x7feb352du;
   x ^= x >> 15;
   x *= 0x846ca68bu;
@@ -184,7 +184,7 @@ int oracle_quadratic_grad(const oracle_problem* p, int64_t d, const float* xhat,
   for (int64_t c = 0; c < d; ++c) {
     float h, xs;
     quad_data(p, c, &h, &xs);
-    uint32_t u = quad_noise_mix((uint32_t)c ^ kk);
+    uint32_t u = oracle_quad_noise_mix((uint32_t)c ^ kk);
     float m = (float)(u >> 9) * (1.0f / 4194304.0f);    /* exact: (u>>9) * 2^-22, in [0,2) */
     float v = m - 1.0f;                                  /* exact, uniform grid in [-1,1) */
     float noise = p->noise_s * v;

@@ -59,6 +59,8 @@ def lib():
             L.oracle_philox4x32_10.restype = None
             L.oracle_lowbias32.argtypes = [C.c_uint32]
             L.oracle_lowbias32.restype = C.c_uint32
+            L.oracle_quad_noise_mix.argtypes = [C.c_uint32]
+            L.oracle_quad_noise_mix.restype = C.c_uint32
             L.oracle_quad_event_key.argtypes = [C.c_uint32, C.c_uint64]
             L.oracle_quad_event_key.restype = C.c_uint32
             L.oracle_check_graph.argtypes = [C.c_int32, C.c_int32, P, P, P]
@@ -107,6 +109,11 @@ def read_key(t_read: int, i: int) -> int:
 
 def lowbias32(x: int) -> int:
     return int(lib().oracle_lowbias32(x & 0xFFFFFFFF))
+
+
+def quad_noise_mix(x: int) -> int:
+    """The synthetic quadratic's noise word u = mix(c ^ K_k) (DESIGN.md definition v3)."""
+    return int(lib().oracle_quad_noise_mix(x & 0xFFFFFFFF))
 
 
 def check_graph(n, edges, role=None):

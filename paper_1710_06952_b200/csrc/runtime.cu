@@ -1206,15 +1206,28 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s
     CTX_CHECK(c);
     if (i < 0 || j < 0 || i >= c->n || j >= c->n || i == j) return fail(ADPSGD_E_INVALID, "i/j");
     if (!is_neighbour(c, i, j)) return fail(ADPSGD_E_NOT_NEIGHBOURS, "not an edge");
-    if (!c->is_local(i) || !c->is_local(j)) return fail(ADPSGD_E_UNSUPPORTED, "gossip needs local workers");
+    if (c->role[i] == c->role[j]) return fail(ADPSGD_E_NOT_BIPARTITE, "gossip pairs two workers of the same role");
+    // a pure average is an event of the log like any other (reading R23): it
+    // takes the next ticket k and is logged with NO_GRAD, so the event log
+    // replays every change of X; the paper's k (gradient updates) is
+    // the subsequence of events without NO_GRAD
+    if (c->world > 1) {
+      if (!c->is_local(i)) return fail(ADPSGD_E_INVALID, "adpsgd_gossip: worker i must live on this rank");
+      return step_multi(c, i, nullptr, s, nullptr, j);
+    }
     std::lock_guard<std::mutex> lk(c->mu);
+    unsigned long long k;
+    ST(host_ticket(c, &k));
     cudaStream_t st = c->use(s);
     CU(cudaStreamWaitEvent(st, c->last_evt[i], 0));
     CU(cudaStreamWaitEvent(st, c->last_evt[j], 0));
     CU(launch_event(c->row(i), c->row(j), nullptr, nullptr, c->d, c->n4, c->gamma, c->q, 0, kGradNone, st));
-    ++c->launches;
+    CU(launch_step_commit(c->gctl0, c->ctl + c->worker_local[i], c->log0, c->log_cap, (long long)k, i, j,
+                          ADPSGD_EV_NO_GRAD, 0, st));
+    c->launches += 2;
     CU(cudaEventRecord(c->last_evt[i], st));
     CU(cudaEventRecord(c->last_evt[j], st));
+    c->host_k = k + 1;
     return ADPSGD_OK;
   })
 }
@@ -1224,12 +1237,15 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s
 // device -- the lock may live on a peer GPU and other ranks step concurrently --
 // k is read back (a built-in gradient's draws are keyed by k), then gradient,
 // fused pass over NVLink, and a commit kernel that logs and unlocks.
-static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_stream s, int64_t* ticket_out) {
+// gossip_j >= 0: adpsgd_gossip(w, gossip_j) -- the pair average alone, a NO_GRAD event.
+static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_stream s, int64_t* ticket_out,
+                                int gossip_j = -1) {
   if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
   if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "adpsgd_step: worker w must live on this rank");
   std::lock_guard<std::mutex> lk(c->mu);
-  int j = -1;
-  if (c->role[w] == 0 && !c->nb[w].empty()) {
+  const bool gossip = gossip_j >= 0;
+  int j = gossip ? gossip_j : -1;
+  if (!gossip && c->role[w] == 0 && !c->nb[w].empty()) {
     uint64_t st = c->seed ^ (0x9E3779B97F4A7C15ull * (uint64_t)(w + 1)) ^ (c->step_ctr[w]++ << 20);
     const uint64_t r = splitmix64(st);
     j = c->nb[w][(size_t)((r >> 32) * c->nb[w].size() >> 32)];
@@ -1246,7 +1262,7 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
   }
   // allocate before taking the lock: nothing that may synchronise the device
   // (which would wait for a peer's lock kernel spinning on our lock) runs under it
-  if (!grad && c->model != ADPSGD_MODEL_QUADRATIC) {
+  if (!gossip && !grad && c->model != ADPSGD_MODEL_QUADRATIC) {
     if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
     if (c->model == ADPSGD_MODEL_MLP) ST(ensure_mlp_scratch(c, 1));
   }
@@ -1256,15 +1272,18 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
   const bool j_local = j >= 0 && c->is_local(j);
   CU(cudaStreamWaitEvent(st, c->last_evt[w], 0));
   if (j_local) CU(cudaStreamWaitEvent(st, c->last_evt[j], 0));
-  unsigned int* lock = &ctl_of(j >= 0 ? j : w)->lock;
+  // the passive endpoint's lock (bipartite order): the partner of an
+  // active, or the worker itself when it is passive (a local step, or a gossip
+  // call naming the passive first)
+  unsigned int* lock = &ctl_of((j >= 0 && c->role[w] == 0) ? j : w)->lock;
   CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, 20ull * 1000000000ull, st));
   unsigned long long k = 0;
   CU(cudaMemcpyAsync(&k, c->super_k, sizeof k, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   if (k == ~0ull) return fail(ADPSGD_E_TIMEOUT, "adpsgd_step: lock wait exceeded the watchdog");
-  int mode = kGradExternal;
+  int mode = gossip ? kGradNone : kGradExternal;
   const float* g = grad;
-  if (!grad) {
+  if (!gossip && !grad) {
     if (c->model == ADPSGD_MODEL_QUADRATIC) {
       mode = kGradQuadInline;
     } else {
@@ -1274,8 +1293,8 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
     }
   }
   CU(launch_event(c->row(w), j >= 0 ? row_of(j) : nullptr, g, nullptr, c->d, c->n4, c->gamma, c->q, k, mode, st));
-  CU(launch_super_commit(c->log0, c->log_cap, c->super_k, w, j, 0u, c->ctl + c->worker_local[w],
-                         &c->gctl0->committed, lock, st));
+  CU(launch_super_commit(c->log0, c->log_cap, c->super_k, w, j, gossip ? (unsigned)ADPSGD_EV_NO_GRAD : 0u,
+                         c->ctl + c->worker_local[w], &c->gctl0->committed, lock, st));
   CU(cudaEventRecord(c->last_evt[w], st));
   if (j_local) CU(cudaEventRecord(c->last_evt[j], st));
   c->launches += 3;

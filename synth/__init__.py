@@ -148,6 +148,21 @@ def x0_uniform(n: int, d: int, seed: int = 7) -> np.ndarray:
     return (m.astype(np.float64) * 2.0 ** -23 - 1.0).astype(np.float32)
 
 
+def schedule_alg1(n, edges, role, K, seed=0):
+    """Algorithm 1 iterations as an i.i.d. schedule (law c4): i_k ~ U{0..n-1};
+    an active worker averages with j_k ~ U(N(i_k)), a passive one updates alone
+    (j = -1, W_k = I) -- the event mix of the free-running engine's Alg. 1 loop.
+    Returns events[K,4] int32 (i, j, 0, 0)."""
+    rng = np.random.default_rng(seed)
+    nb = neighbours(n, edges)
+    ev = np.zeros((K, 4), np.int32)
+    for k in range(K):
+        i = int(rng.integers(n))
+        j = nb[i][int(rng.integers(len(nb[i])))] if (role[i] == 0 and nb[i]) else -1
+        ev[k] = (i, j, 0, 0)
+    return ev
+
+
 def lsq_data(S: int = 8192, d: int = 1024, seed: int = 1, noise: float = 0.01):
     """Config 1: A ~ N(0, 1/d) fp32, x_true ~ N(0,1), b = A x_true + noise*N(0,1)."""
     rng = np.random.default_rng(seed)

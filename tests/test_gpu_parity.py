@@ -7,6 +7,8 @@ same seeded inputs (-m gpu).  Bars:
     the GPU models bitwise; column sum within the c10 tolerances.
 """
 import math
+import os
+import sys
 
 import numpy as np
 import pytest
@@ -155,7 +157,13 @@ def test_config1_replay_within_1e4(P, kind):
     ok = c11_ok(Xg, Xo)
     assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum(), O.full_loss(prob, Xg.mean(0)),
                       O.full_loss(prob, Xo.mean(0)))
-    assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * 0.5
+    # progress sanity (not parity -- that is the c11 check above): least squares
+    # starts at f(0) = mean(b^2)/2 ~ 1/2 and its optimum is ~1e-4 of that (SURVEY
+    # config 1); the logistic loss starts at ln 2 and decreases far
+    # more slowly (label noise in synth.logreg_data, a flat loss far from the
+    # margin) -- so the bar is 1/10 of f(0) for lsq and 1/2 for logreg
+    frac = 0.1 if kind == "lsq" else 0.5
+    assert O.full_loss(prob, Xo.mean(0)) < O.full_loss(prob, np.zeros(d, np.float32)) * frac
     ctx.destroy()
 
 
@@ -280,9 +288,16 @@ def test_step_and_gossip_match_oracle(P):
     Xo, _ = O.replay(prob, X0, e, r, log_events(log))
     assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
     ctx.gossip(0, 1)
+    ctx.gossip(3, 0)                    # passive named first: the same pair average
     ctx.sync()
-    Xo2, _ = O.replay(O.OracleProblem(), Xo, e, r, [[0, 1, 0, 1]])
+    Xo2, _ = O.replay(O.OracleProblem(), Xo, e, r, [[0, 1, 0, 1], [3, 0, 0, 1]])
     assert np.array_equal(read_all(ctx).view(np.uint32), Xo2.view(np.uint32))
+    # reading R23: pure averages take tickets 40, 41 and are logged with NO_GRAD
+    log2 = ctx.read_log(0)
+    assert ctx.ticket() == 42 and len(log2) == 42
+    assert log_events(log2)[40:].tolist() == [[0, 1, 0, 1], [3, 0, 0, 1]]
+    Xo3, _ = O.replay(prob, X0, e, r, log_events(log2))
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo3.view(np.uint32))
     ctx.destroy()
 
 
@@ -513,3 +528,60 @@ def test_divergence_is_reported(P):
     with pytest.raises(O.OracleError) as eo:
         O.replay(prob, np.zeros((n, d), np.float32), e, r, ev)
     assert eo.value.code == 6
+
+
+def test_config3_full_size_2000_steps_vs_oracle_fixture(P):
+    """Config 3 at its own size (BASELINE configs[2]): 3072 -> 512 -> 10
+    tanh MLP, n = 8 ring, M = 128, tau ~ U{0..4}, 2000 events, tcgen05 3xTF32
+    gradients, against the ORACLE's result stored by tools/make_config3_reference.py
+    (tests/golden/config3_mlp_2000_oracle.json: seeded coordinate subset + row rms).
+    Acceptance: reading R11 (|x_gpu - x_orc| <= 1e-4 max(|x_orc|, rms)) on every
+    stored coordinate of every worker."""
+    import json
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    import make_config3_reference as R
+    with open(R.OUT_PATH) as f:
+        ref = json.load(f)
+    X, y, x0, e, r, ev, bi = R.inputs()
+    assert ref["digest_inputs"] == {"data": R.digest(X, y), "x0": R.digest(x0), "schedule": R.digest(ev, bi)}
+    ctx = P.Context(e, R.N, x0.size, role=r, T=R.T, model=P.MODEL_MLP, gamma=R.GAMMA, batch_M=R.M, data_A=X,
+                    data_y=y, mlp_dims=(R.I, R.H, R.OUT), x0=x0)
+    ctx.replay(ev, batch_idx=bi)
+    ctx.sync()
+    idx = np.array(ref["idx"], np.int64)
+    worst = 0.0
+    for w in range(R.N):
+        xg = ctx.read_model(w)[idx].astype(np.float64)
+        xo = np.array(ref["values"][w], np.float64)
+        err = np.abs(xg - xo) / np.maximum(np.abs(xo), ref["rms"][w])
+        worst = max(worst, float(err.max()))
+    assert worst <= 1e-4, worst
+    assert ref["loss_xbar"] < 0.9 * ref["loss_x0"]          # the run made progress (oracle's own)
+    ctx.destroy()
+
+
+def test_free_running_reaches_oracle_loss_threshold(P):
+    """Reading c20 (north star: free-running 'reaches the oracle's loss
+    threshold'; P:861-863 'w.r.t. epochs ... converge similar'): L* = f(x_bar)
+    after K_ref updates of a seeded i.i.d. Algorithm-1 schedule replayed by the
+    oracle; the free-running engine (worker 0 slowed 10x) must reach
+    f(x_bar) <= L* within 1.5 K_ref committed updates.  Config-4 quadratic at
+    d = 2^20, n = 16."""
+    n, d, K_ref = 16, 1 << 20, 3000
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(12)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    ev = synth.schedule_alg1(n, e, r, K_ref, seed=31)
+    Xo, _ = O.replay(prob, np.zeros((n, d), np.float32), e, r, ev)
+    L_star = O.full_loss(prob, Xo.astype(np.float64).mean(0).astype(np.float32))
+    L0 = O.full_loss(prob, np.zeros(d, np.float32))
+    assert L_star < 0.9 * L0
+    ctx = P.Context(e, n, d, role=r, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk),
+                    quad_noise_s=s, straggler=synth.stragglers(n), compute_ns=20_000, seed=5)
+    ctx.run(int(1.5 * K_ref))
+    ctx.sync()
+    xbar = read_all(ctx).astype(np.float64).mean(0).astype(np.float32)
+    L_gpu = O.full_loss(prob, xbar)
+    assert L_gpu <= L_star, (L_gpu, L_star, L0)
+    ctx.destroy()

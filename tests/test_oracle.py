@@ -38,6 +38,53 @@ def test_philox_known_answers():
         ["0xd16cfe09", "0x94fdcceb", "0x5001e420", "0x24126ea1"]
 
 
+# lowbias32's published inverse ("lowbias32_r", C. Wellons, hash-prospector):
+#   x ^= x >> 16; x *= 0x43021123; x ^= x >> 15 ^ x >> 30; x *= 0x1d69e2a5; x ^= x >> 16
+# 0x43021123 and 0x1d69e2a5 are the inverses mod 2^32 of 0x846ca68b and
+# 0x7feb352d, and x ^ x>>15 ^ x>>30 undoes the xorshift by 15.  The inverse only
+# round-trips if every constant and shift of the forward hash is the published one.
+_M = 0xFFFFFFFF
+
+
+def _xs15_inv(x):
+    return x ^ (x >> 15) ^ (x >> 30)
+
+
+def test_lowbias32_known_inverse():
+    rng = np.random.default_rng(5)
+    for x in [0, 1, 2, 0xFFFFFFFF, 0x80000000] + rng.integers(0, 2**32, 2000).tolist():
+        y = O.lowbias32(int(x))
+        y ^= y >> 16
+        y = (y * 0x43021123) & _M
+        y = _xs15_inv(y)
+        y = (y * 0x1d69e2a5) & _M
+        y ^= y >> 16
+        assert y == x
+
+
+def test_quad_noise_mix_known_inverse_and_grid():
+    """The quadratic's noise mix (DESIGN.md definition v3: u = ((x A) ^ (x A) >> 15) B
+    with lowbias32's multipliers A = 0x7feb352d, B = 0x846ca68b) inverts with the
+    published inverse multipliers; and the noise v = (u >> 9) 2^-22 - 1 it feeds is
+    the 23-bit uniform grid on [-1, 1): mean 0, variance 1/3 (so s v has the
+    variance M sigma^2 of a batch sum when s = sigma sqrt(3M), reading R2)."""
+    rng = np.random.default_rng(6)
+    for x in [0, 1, 0xFFFFFFFF] + rng.integers(0, 2**32, 2000).tolist():
+        y = (O.quad_noise_mix(int(x)) * 0x43021123) & _M
+        y = (_xs15_inv(y) * 0x1d69e2a5) & _M
+        assert y == x
+    d = 1 << 18
+    p = O.OracleProblem(O.MODEL_QUADRATIC, M=1, noise_key=0x5EED, noise_s=1.0,
+                        h=np.ones(d, np.float32), xstar=np.zeros(d, np.float32))
+    v = O.gradient(p, np.zeros(d, np.float32), k=3).astype(np.float64)   # det part 0: g = 1 * v
+    assert v.min() >= -1.0 and v.max() < 1.0
+    grid = (v + 1.0) * 2.0 ** 22
+    assert np.array_equal(grid, np.round(grid))
+    se = math.sqrt(1 / 3 / d)
+    assert abs(v.mean()) < 5 * se
+    assert abs(v.var() - 1 / 3) < 5 * math.sqrt(4 / 45 / d)
+
+
 def test_lowbias32_is_a_bijection_sample():
     """lowbias32 is a composition of invertible steps: no collisions on a block,
     and 0 is its fixed point (every step maps 0 to 0)."""
@@ -425,7 +472,7 @@ def test_mlp_gradient_matches_finite_differences():
     X, y = synth.mlp_data(S=6, n_in=I, n_out=Ocl, s=1.0, seed=1)
     p = O.OracleProblem(O.MODEL_MLP, M=6, A=X, y=y, dims=(I, H, Ocl))
     w = synth.mlp_init(I, H, Ocl, seed=2)
-    w[H * I:H * I + H] = 0.3                    # keep hidden units off the ReLU kink
+    w[H * I:H * I + H] = 0.3                    # hidden pre-activations in tanh's curved range (reading R18)
     assert w.size == O.mlp_dim(I, H, Ocl)
     g = O.gradient(p, w, idx=np.arange(6))
     fd = _fd(lambda z: O.full_loss(p, z) * 6, w, 2.0 ** -12)
