@@ -1201,6 +1201,9 @@ adpsgd_status adpsgd_connect(adpsgd_ctx* c, const void* nccl_id) {
   })
 }
 
+static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_stream s, int64_t* ticket_out,
+                                int gossip_j);
+
 adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s) {
   GUARD({
     CTX_CHECK(c);
@@ -1239,7 +1242,7 @@ adpsgd_status adpsgd_gossip(adpsgd_ctx* c, int32_t i, int32_t j, adpsgd_stream s
 // fused pass over NVLink, and a commit kernel that logs and unlocks.
 // gossip_j >= 0: adpsgd_gossip(w, gossip_j) -- the pair average alone, a NO_GRAD event.
 static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_stream s, int64_t* ticket_out,
-                                int gossip_j = -1) {
+                                int gossip_j) {
   if (!c->connected) return fail(ADPSGD_E_STATE, "not connected");
   if (!c->is_local(w)) return fail(ADPSGD_E_INVALID, "adpsgd_step: worker w must live on this rank");
   std::lock_guard<std::mutex> lk(c->mu);
@@ -1310,7 +1313,7 @@ adpsgd_status adpsgd_step(adpsgd_ctx* c, int32_t w, const float* grad, adpsgd_st
     if (w < 0 || w >= c->n) return fail(ADPSGD_E_INVALID, "worker");
     if (!grad && (c->model == ADPSGD_MODEL_NONE || c->model == ADPSGD_MODEL_EXTERNAL))
       return fail(ADPSGD_E_INVALID, "no gradient: pass grad or configure a built-in model");
-    if (c->world > 1) return step_multi(c, w, grad, s, ticket_out);
+    if (c->world > 1) return step_multi(c, w, grad, s, ticket_out, -1);
     std::lock_guard<std::mutex> lk(c->mu);
     int j = -1;
     if (c->role[w] == 0 && !c->nb[w].empty()) {
