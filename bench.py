@@ -106,6 +106,45 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
+class NvlCounters:
+    """NVML NVLink byte counters of this rank's GPU (hardware counters, not the
+    engine's algorithmic accounting): cumulative data TX / RX (field ids 138 / 139,
+    KiB) and raw TX / RX incl. protocol (140 / 141).  Read before and after a
+    timed region; None when NVML or the fields are unavailable."""
+
+    FIELDS = {"data_tx": 138, "data_rx": 139, "raw_tx": 140, "raw_rx": 141}
+
+    def __init__(self, dev):
+        self.h = None
+        try:
+            import pynvml as N
+            import torch
+            N.nvmlInit()
+            uuid = str(torch.cuda.get_device_properties(dev).uuid)
+            self.N = N
+            self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+        except Exception:
+            self.h = None
+
+    def read(self):
+        if self.h is None:
+            return None
+        try:
+            vals = self.N.nvmlDeviceGetFieldValues(self.h, list(self.FIELDS.values()))
+            out = {}
+            for (k, _), v in zip(self.FIELDS.items(), vals):
+                if v.nvmlReturn != 0:
+                    return None
+                out[k] = float(v.value.ullVal) * 1024.0          # KiB -> bytes
+            return out
+        except Exception:
+            return None
+
+    @staticmethod
+    def delta(a, b):
+        return None if (a is None or b is None) else {k: b[k] - a[k] for k in a}
+
+
 def traffic_per_launch(alg_bytes):
     """DRAM bytes per engine launch: the dram/algorithmic ratio of the committed
     ncu --set full capture (profiles/engine_traffic.json) times this launch's
@@ -126,8 +165,10 @@ def peaks():
 
 
 # --------------------------------------------------------- CPU oracle legs --
-def oracle_sample(n, d, events, seed=5):
-    """Time the oracle (as it stands) on `events` events of the same workload."""
+def oracle_sample(n, d, events, seed=5, omp=False):
+    """Time the oracle (as it stands) on `events` events of the same workload:
+    the replay core only -- a call's fixed cost (copying the n x d state in and
+    out, allocating its history) is timed with an empty schedule and subtracted."""
     import numpy as np
     import synth
     from oracle import oracle as O
@@ -137,11 +178,27 @@ def oracle_sample(n, d, events, seed=5):
     prob = O.OracleProblem(O.MODEL_QUADRATIC, M=M_BATCH, gamma=GAMMA, data_key=dk, noise_key=nk, noise_s=s)
     ev, _ = synth.schedule_iid(n, e, K=events, seed=seed, local_prob=0.0)
     X = np.zeros((n, d), np.float32)
+    O.replay(prob, X, e, r, ev[:1], omp=omp)        # page in the library / first-touch the state
     t0 = time.perf_counter()
-    O.replay(prob, X, e, r, ev)
-    dt = time.perf_counter() - t0
+    O.replay(prob, X, e, r, ev[:0], omp=omp)
+    t1 = time.perf_counter()
+    O.replay(prob, X, e, r, ev, omp=omp)
+    t2 = time.perf_counter()
+    dt = max((t2 - t1) - (t1 - t0), 1e-9)
     pairs = int((ev[:, 1] >= 0).sum())
     return pairs, dt
+
+
+def host_info():
+    """nproc and the CPU model (lscpu) of the box the CPU legs ran on."""
+    model = None
+    try:
+        for line in subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout.splitlines():
+            if line.startswith("Model name:"):
+                model = line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return {"nproc": os.cpu_count(), "cpu_model": model}
 
 
 def run_reference(a):
@@ -154,7 +211,7 @@ def run_reference(a):
     # n x d state per call, so the sample uses a ring of min(n, 8) workers to keep
     # every step bounded (n = 64 at 8 GPUs would be 6.5 GB per copy)
     n_s = min(n, 8)
-    per_step = 2
+    per_step = 4
     for _ in range(a.warmup):
         oracle_sample(n_s, a.d, per_step)
     tot_pairs, tot_t = 0, 0.0
@@ -171,7 +228,8 @@ def run_reference(a):
                        "parallelism": "none (1 CPU core)"},
             "cpu_baseline": {"value": v, "unit": "gossip-steps/s", "cores": 1, "kind": "oracle",
                              "sample": f"{per_step} pair events per step on a ring of {n_s} workers (the "
-                                       f"workload has n={n}), d={a.d}"},
+                                       f"workload has n={n}), d={a.d}; replay core (fixed per-call copy "
+                                       f"cost subtracted)", "host": host_info()},
             "e2e": {"value": v, "unit": "gossip-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line))
 
@@ -305,18 +363,21 @@ def main():
     strag = synth.stragglers(n, slow_worker=0, slow=a.straggler)
     cns = int(a.compute_us * 1000)
 
-    def make_ctx(st, nn=None, ee=None, rr=None, wait_free=0):
+    def make_ctx(st, nn=None, ee=None, rr=None, wait_free=0, compute_ns=None):
         nn = n if nn is None else nn
         ee = e if ee is None else ee
         rr = r if rr is None else rr
         return P.Context(ee, nn, d, role=rr, rank=rank, world_size=world, device=local, placement=a.placement,
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
-                         quad_noise_s=s, straggler=st, compute_ns=cns, seed=1234, log_capacity=1 << 16,
+                         quad_noise_s=s, straggler=st, compute_ns=cns if compute_ns is None else compute_ns,
+                         seed=1234, log_capacity=1 << 16,
                          engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free,
                          engine_fuse=not a.no_fuse, engine_coop=None if a.coop == 0 else a.coop > 0)
 
     stream = torch.cuda.Stream()
     out = torch.empty(d, dtype=torch.float32, device="cuda")
+    out_host = torch.empty(d, dtype=torch.float32, pin_memory=True)   # e2e: x_bar back to the host
+    nvl = NvlCounters(local)
 
     def barrier():
         if dist:
@@ -335,6 +396,22 @@ def main():
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
         dist.all_reduce(t)
         return float(t.item())
+
+    def nvl_report(delta, sec):
+        """counter-based NVLink GB/s of this GPU (data payload and raw incl. protocol), mean and
+        max over ranks; collective"""
+        ok = -maxr(-(0.0 if delta is None else 1.0)) > 0          # available on every rank
+        vals = {k: (0.0 if delta is None else delta[k] / sec / 1e9) for k in NvlCounters.FIELDS}
+        rep = {"source": "NVML field values 138-141 (NVLink data / raw TX and RX byte counters) read "
+                         "around the timed region on every rank"}
+        if delta is None or not ok:
+            rep["available"] = False
+            return rep
+        for k, v in vals.items():
+            rep[f"{k}_gbs_mean"] = sumr(v) / max(world, 1)
+            rep[f"{k}_gbs_max"] = maxr(v)
+        rep["data_per_direction_frac_of_900"] = max(rep["data_tx_gbs_mean"], rep["data_rx_gbs_mean"]) / 900.0
+        return rep
 
     def step(ctx, eng=None):
         if eng:
@@ -359,6 +436,7 @@ def main():
             t0, t1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             torch.cuda.synchronize()
             barrier()
+            nv0 = nvl.read()
             h0 = time.perf_counter()
             t0.record(stream)
             for k in range(K):
@@ -366,7 +444,9 @@ def main():
             t1.record(stream)
             torch.cuda.synchronize()
             h1 = time.perf_counter()
+            nv1 = nvl.read()
         clk.window(h0, h1)
+        timed.nvl = NvlCounters.delta(nv0, nv1)
         ctx.sync()
         barrier()
         ms = maxr(t0.elapsed_time(t1))
@@ -377,6 +457,7 @@ def main():
     # ------------------------------------------------ main leg: straggler --
     ctx = make_ctx(strag)
     ms, st0, st1, launches, clocks, eng_ms = timed(ctx, a.steps, a.warmup, engine_events=True)
+    nvl_main = timed.nvl
     pairs = sumr(st1["local_pair_events"] - st0["local_pair_events"])
     events = sumr(st1["local_events"] - st0["local_events"])
     loc_bytes = st1["local_bytes"] - st0["local_bytes"]
@@ -399,6 +480,7 @@ def main():
     for _ in range(a.steps):
         ctx.run(U)
         mk = ctx.consensus_mean(out.data_ptr(), with_mk=True)
+        out_host.copy_(out)                     # the step's result x_bar, device -> pinned host
     te = maxr(time.perf_counter() - te0)
     pairs_e = sumr(ctx.stats()["local_pair_events"] - st_e["local_pair_events"])
     n_local = len(ctx.local_workers())
@@ -445,11 +527,11 @@ def main():
         extras["adpsgd_vs_dpsgd_updates_ratio_straggler"] = upd_s / dp["straggler"]["updates_per_s"]
         # config 5 (BASELINE configs[4]): 16 workers per GPU, heterogeneous stragglers
         # s_w = 10^U[0,1] plus worker 0 at 10x, AD-PSGD vs the NCCL AllReduce-SGD baseline
-        n5 = 16 * world
+        n5 = 128 if 128 // world <= 128 and 128 % world == 0 else 16 * world   # BASELINE configs[4]: n = 128
         e5, r5 = synth.ring(n5)
         st5 = synth.stragglers(n5, seed=99, slow_worker=0, slow=10.0, hetero=True)
         c5 = make_ctx(st5, n5, e5, r5)
-        U5, reps = 16 * n5, 3
+        U5, reps = 8 * n5, 3
         c5.run(U5, stream)
         torch.cuda.synchronize()
         c5.sync()
@@ -479,7 +561,8 @@ def main():
         barrier()
         up5 = sumr(s51["local_events"] - s50["local_events"]) / sec5
         extras["config5"] = {
-            "workload": f"n={n5} (16/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, t_c={a.compute_us}us",
+            "workload": f"n={n5} ({n5 // world}/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, "
+                        f"t_c={a.compute_us}us",
             "adpsgd_updates_per_s": up5,
             "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
             "allreduce_updates_per_s": R5 * n5 / sec5ar,
@@ -524,6 +607,13 @@ def main():
             t4[f"x{slow:g}"] = three_way(make_ctx(synth.stragglers(n, slow_worker=0, slow=slow)),
                                          4 if slow < 50 else 2)
         extras["table4_updates_per_s"] = t4
+        # emulated t_c sweep: 0.1 / 1 / 10 ms per gradient spans the paper's
+        # communication-intensive and computation-intensive regimes, worker 0 slowed 10x
+        tcs = {}
+        for tc_us, rb in ((100.0, 4), (1000.0, 3), (10000.0, 2)):
+            tcs[f"t_c_{tc_us / 1000:g}ms"] = three_way(make_ctx(strag, compute_ns=int(tc_us * 1000)), rb)
+        tcs["workload"] = "config 4 workload, worker 0 x10; updates/s of AD-PSGD / AllReduce-SGD / D-PSGD"
+        extras["tc_sweep_updates_per_s"] = tcs
         # heterogeneous communication (Fig. loss-link; reading R21): worker 1's
         # link 10x slower, nominal model transfer 4d / 900 GB/s; no compute straggler
         link_ns = int(4 * d / 900e9 * 1e9)
@@ -585,14 +675,17 @@ def main():
             barrier()
             s0 = cn.stats()
             ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            nvs0 = nvl.read()
             ta.record(stream)
             for _ in range(3):
                 cn.run(8 * ns, stream)
             tb.record(stream)
             torch.cuda.synchronize()
+            nvs1 = nvl.read()
             cn.sync()
             barrier()
             secn = maxr(ta.elapsed_time(tb)) / 1e3
+            nvl_stress = nvl_report(NvlCounters.delta(nvs0, nvs1), secn)
             s1 = cn.stats()
             nvb = sumr(s1["local_nvlink_bytes"] - s0["local_nvlink_bytes"])
             npair = sumr(s1["local_pair_events"] - s0["local_pair_events"])
@@ -604,7 +697,8 @@ def main():
                 "gossip_steps_per_s": npair / secn,
                 "per_gpu_per_direction_gbs": nvb / secn / world / 1e9,
                 "frac_of_900": nvb / secn / world / 900e9,
-                "frac_of_measured_peer_copy_770": nvb / secn / world / 770e9}
+                "frac_of_measured_peer_copy_770": nvb / secn / world / 770e9,
+                "nvml_counters": nvl_stress}
         if world > 1 and world % 2 == 0:
             # super-learners (reading R22): R = 2 GPUs per super-learner (NCCL all-reduce of
             # their gradients), S = world / 2 super-learners gossiping over NVLink; one learner per GPU
@@ -673,10 +767,18 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not a.no_extras:
         pairs_c, dt_c = oracle_sample(n, d, a.cpu_events)
+        pairs_o, dt_o = oracle_sample(n, d, a.cpu_events, omp=True)
+        hi = host_info()
         cpu = {"value": pairs_c / dt_c, "unit": "gossip-steps/s", "cores": 1, "kind": "oracle",
-               "sample": f"{a.cpu_events} iid events (ring n={n}, d={d}) of the oracle's Alg. 1 replay"}
+               "sample": f"{a.cpu_events} iid events (ring n={n}, d={d}) of the oracle's Alg. 1 replay; replay "
+                         f"core (the fixed per-call copy of the n x d state timed with an empty schedule and "
+                         f"subtracted)", "host": hi,
+               "openmp_all_cores": {"value": pairs_o / dt_o, "unit": "gossip-steps/s", "cores": hi["nproc"],
+                                    "kind": "oracle built with -fopenmp (per-coordinate loops; bit-identical, "
+                                            "tests/test_oracle.py)"}}
 
     traffic_bytes, traffic_src = traffic_per_launch(loc_bytes / a.steps)
+    nvl_main_rep = nvl_report(nvl_main, sec) if world > 1 else {"available": False, "note": "one GPU"}
     line = {
         "metric": "gossip-steps/s", "value": gossip_s, "unit": "gossip-steps/s", "n_gpus": world,
         "steps": a.steps, "warmup": a.warmup, "ms_per_step": ms / a.steps, "higher_is_better": True,
@@ -693,23 +795,35 @@ def main():
                    nvl_bytes / sec / max(world, 1) / 1e9, "frac_of_900": nvl_bytes / sec / max(world, 1) / 900e9,
                    "frac_of_measured_peer_copy_770": nvl_bytes / sec / max(world, 1) / 770e9,
                    "note": "this workload's block placement: one ring edge per GPU boundary crosses NVLink; "
-                           "the all-cross figure is under all_cross (extras.nvlink_stress)"},
+                           "the all-cross figure is under all_cross (extras.nvlink_stress)",
+                   "nvml_counters": nvl_main_rep},
         "roofline": {"kernel": "k_engine", "bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic_bytes, "traffic_source": traffic_src,
                      "per_launch_algorithmic_bytes": loc_bytes / a.steps, "avg_launch_ms": eng_ms,
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "clocks": clocks,
         "e2e": {"value": pairs_e / te, "unit": "gossip-steps/s",
-                "h2d_bytes_per_step": 136 * n_local * world, "d2h_bytes_per_step": 16 * world,
-                "note": "public API (Context.run + consensus_mean with M_k read back), host wall clock"},
+                "h2d_bytes_per_step": 136 * n_local * world, "d2h_bytes_per_step": (16 + 4 * d) * world,
+                "note": "public API (Context.run + consensus_mean with M_k read back), x_bar copied to pinned "
+                        "host memory every step, host wall clock, max over ranks"},
         "gpu_launches": launches,
         "update_counts_rank0": cnts,
     }
     line.update(extras)
+    if "wait_free_appA" in extras:
+        # the App. A runtime (real gradient buffer, real staleness tau = k - t_read) beside the
+        # Alg. 1 loop's tau = 0 fused figure above
+        line["realistic_staleness"] = {
+            "wait_free_updates_per_s": extras["wait_free_appA"]["plain"]["updates_per_s"],
+            "wait_free_compensated_updates_per_s": extras["wait_free_appA"]["compensated"]["updates_per_s"],
+            "alg1_fused_updates_per_s": upd_s,
+            "note": "App. A loop (P:1235-1314, reading R20): gradients computed at a pulled model into a "
+                    "buffer and flushed later (tau > 0 logged); the headline runs Alg. 1 with tau = 0"}
     if "nvlink_stress" in extras:           # the fused kernel's NVLink fraction when every pair crosses GPUs
         ns = extras["nvlink_stress"]
         line["nvlink"]["all_cross"] = {"per_gpu_per_direction_gbs": ns["per_gpu_per_direction_gbs"],
-                                       "frac_of_900": ns["frac_of_900"], "workload": ns["workload"]}
+                                       "frac_of_900": ns["frac_of_900"], "workload": ns["workload"],
+                                       "nvml_counters": ns["nvml_counters"]}
     if cpu:
         line["cpu_baseline"] = cpu
     if rank == 0:

@@ -30,6 +30,19 @@
 #include <string.h>
 #include <math.h>
 
+/* Coordinates are independent in every per-coordinate loop below (each c is
+ * written once from its own inputs), so the optional OpenMP build
+ * (liboracle_omp.so, bench.py's all-cores CPU baseline)
+ * is bit-identical to the serial one (tests/test_oracle.py checks it).  The
+ * default build ignores the pragmas.                                          */
+#ifdef _OPENMP
+#define ORC_OMP_FOR _Pragma("omp parallel for schedule(static)")
+#define ORC_OMP_FOR_BAD _Pragma("omp parallel for schedule(static) reduction(|:bad)")
+#else
+#define ORC_OMP_FOR
+#define ORC_OMP_FOR_BAD
+#endif
+
 int oracle_consensus_mean(int32_t n, int64_t d, const float* X, const double* p, float* out,
                           double* mk);
 
@@ -181,6 +194,7 @@ int oracle_quadratic_grad(const oracle_problem* p, int64_t d, const float* xhat,
                           float* g) {
   uint32_t kk = oracle_quad_event_key(p->noise_key, k);
   float Mf = (float)p->M;
+  ORC_OMP_FOR
   for (int64_t c = 0; c < d; ++c) {
     float h, xs;
     quad_data(p, c, &h, &xs);
@@ -479,16 +493,20 @@ int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
     if (Xn != Xk) memcpy(Xn, Xk, sizeof(float) * (size_t)nd);
     float* xi = Xn + (int64_t)i * d;
     if (do_grad && flush_first) {       /* Alg. 2: flush g first */
+      int bad = 0;
+      ORC_OMP_FOR_BAD
       for (int64_t c = 0; c < d; ++c) {
         float step = p->gamma * g[c];
         xi[c] = xi[c] - step;
-        if (!isfinite(xi[c])) st = ORC_E_DIVERGED;
+        if (!isfinite(xi[c])) bad = 1;
       }
+      if (bad) st = ORC_E_DIVERGED;
       if (st != ORC_OK) break;
       do_grad = 0;
     }
     if (j >= 0) {                       /* X_{k+1/2} = X_k W_k */
       float* xj = Xn + (int64_t)j * d;
+      ORC_OMP_FOR
       for (int64_t c = 0; c < d; ++c) {
         float s = xi[c] + xj[c];
         float m = s * 0.5f;
@@ -496,11 +514,14 @@ int oracle_replay(const oracle_problem* p, int32_t n, int64_t d, float* X,
       }
     }
     if (do_grad) {                      /* x_{k+1}^{i_k} = x_{k+1/2}^{i_k} - gamma g */
+      int bad = 0;
+      ORC_OMP_FOR_BAD
       for (int64_t c = 0; c < d; ++c) {
         float step = p->gamma * g[c];
         xi[c] = xi[c] - step;
-        if (!isfinite(xi[c])) st = ORC_E_DIVERGED;
+        if (!isfinite(xi[c])) bad = 1;
       }
+      if (bad) st = ORC_E_DIVERGED;
       if (st != ORC_OK) break;
     }
     if (mk_trace) {

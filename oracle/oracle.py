@@ -31,13 +31,19 @@ class OracleError(RuntimeError):
         self.code = code
 
 
-def build(force: bool = False) -> str:
-    """Compile the oracle shared library (plain gcc, no GPU)."""
-    if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
+_LIB_OMP = os.path.join(_HERE, "liboracle_omp.so")
+
+
+def build(force: bool = False, omp: bool = False) -> str:
+    """Compile the oracle shared library (plain gcc, no GPU).  omp=True: the same
+    source with -fopenmp (per-coordinate loops over all cores, bit-identical)."""
+    out = _LIB_OMP if omp else _LIB
+    if force or not os.path.exists(out) or os.path.getmtime(out) < os.path.getmtime(_SRC):
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-ffp-contract=off", "-fno-fast-math",
-                               "-fPIC", "-shared", "-Wall", "-o", _LIB + ".tmp", _SRC, "-lm"])
-        os.replace(_LIB + ".tmp", _LIB)
-    return _LIB
+                               "-fPIC", "-shared", "-Wall"] + (["-fopenmp"] if omp else []) +
+                              ["-o", out + ".tmp", _SRC, "-lm"])
+        os.replace(out + ".tmp", out)
+    return out
 
 
 class Problem(C.Structure):
@@ -49,11 +55,15 @@ class Problem(C.Structure):
                 ("batch_key", C.c_uint32 * 2)]
 
 
-def lib():
-    global _lib
+_lib_omp = None
+
+
+def lib(omp: bool = False):
+    """The serial oracle (default), or its OpenMP build (bench.py's all-cores CPU leg)."""
+    global _lib, _lib_omp
     with _lock:
-        if _lib is None:
-            L = C.CDLL(build())
+        if (_lib_omp if omp else _lib) is None:
+            L = C.CDLL(build(omp=omp))
             P = C.c_void_p
             L.oracle_philox4x32_10.argtypes = [P, P, P]
             L.oracle_philox4x32_10.restype = None
@@ -80,8 +90,11 @@ def lib():
             L.oracle_super_gradient.argtypes = [C.POINTER(Problem), C.c_int64, P, C.c_int32, C.c_int64, C.c_int32, P]
             L.oracle_super_replay.argtypes = [C.POINTER(Problem), C.c_int32, C.c_int64, P, C.c_int32, P, P, P,
                                               C.c_int64, C.c_int32]
-            _lib = L
-    return _lib
+            if omp:
+                _lib_omp = L
+            else:
+                _lib = L
+    return _lib_omp if omp else _lib
 
 
 def _p(a):
@@ -170,8 +183,9 @@ def full_loss(prob: OracleProblem, x) -> float:
 
 
 def replay(prob: OracleProblem, X, edges, role, events, batch_idx=None, T=0, clamp_tau=False,
-           k0=0, mk_trace=False):
-    """Run Alg. 1 over an explicit event schedule; returns (X_K, mk or None)."""
+           k0=0, mk_trace=False, omp=False):
+    """Run Alg. 1 over an explicit event schedule; returns (X_K, mk or None).
+    omp=True runs the OpenMP build (bit-identical; bench.py's all-cores leg)."""
     X = np.ascontiguousarray(np.array(X, np.float32, copy=True))
     n, d = X.shape
     e = np.ascontiguousarray(np.asarray(edges, np.int32).reshape(-1, 2))
@@ -179,7 +193,7 @@ def replay(prob: OracleProblem, X, edges, role, events, batch_idx=None, T=0, cla
     ev = np.ascontiguousarray(np.asarray(events, np.int32).reshape(-1, 4))
     bi = None if batch_idx is None else np.ascontiguousarray(np.asarray(batch_idx, np.int32))
     mk = np.zeros(ev.shape[0] + 1, np.float64) if mk_trace else None
-    _check(lib().oracle_replay(prob.ref, n, d, _p(X), e.shape[0], _p(e), _p(r), _p(ev), ev.shape[0],
+    _check(lib(omp).oracle_replay(prob.ref, n, d, _p(X), e.shape[0], _p(e), _p(r), _p(ev), ev.shape[0],
                                _p(bi), T, int(clamp_tau), k0, _p(mk)))
     return X, mk
 

@@ -660,3 +660,17 @@ def test_super_gradient_any_model_and_distinct_batches():
     A2, b2 = synth.lsq_data(S=S, d=d, seed=3)
     p2 = O.OracleProblem(O.MODEL_LSQ, M=M, gamma=0.1, A=A2, b=b2, batch_key=(3, 4))
     assert not np.array_equal(O.super_gradient(p2, x, s=0, c=7, R=1), O.super_gradient(p2, x, s=1, c=7, R=1))
+
+
+def test_openmp_build_is_bit_identical():
+    """The all-cores CPU baseline (liboracle_omp.so) runs the
+    same per-coordinate loops in parallel: identical results to the serial oracle."""
+    n, d = 4, 100_003
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(3)
+    p = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=0.5)
+    ev, _ = synth.schedule_iid(n, e, K=40, T=2, seed=9, local_prob=0.3)
+    X0 = synth.x0_uniform(n, d, seed=4)
+    Xs, _ = O.replay(p, X0, e, r, ev, T=2)
+    Xp, _ = O.replay(p, X0, e, r, ev, T=2, omp=True)
+    assert np.array_equal(Xs.view(np.uint32), Xp.view(np.uint32))
