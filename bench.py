@@ -108,36 +108,58 @@ class ClockSampler:
 
 class NvlCounters:
     """NVML NVLink byte counters of this rank's GPU (hardware counters, not the
-    engine's algorithmic accounting): cumulative data TX / RX (field ids 138 / 139,
-    KiB) and raw TX / RX incl. protocol (140 / 141).  Read before and after a
-    timed region; None when NVML or the fields are unavailable."""
+    engine's algorithmic accounting), read before and after a timed region.
+    Scheme "throughput": fields 138 / 139 (data TX / RX) and 140 / 141 (raw TX /
+    RX incl. protocol), cumulative KiB over all links; scheme "per_link": fields
+    202 / 204 (XMIT / RCV bytes) summed over every link.  The first scheme the
+    driver supports is used; None when NVML has neither."""
 
     FIELDS = {"data_tx": 138, "data_rx": 139, "raw_tx": 140, "raw_rx": 141}
+    LINK_FIELDS = {"data_tx": 202, "data_rx": 204}
+    MAX_LINKS = 18
 
     def __init__(self, dev):
-        self.h = None
+        self.h, self.scheme, self.err = None, None, None
         try:
             import pynvml as N
             import torch
             N.nvmlInit()
-            uuid = str(torch.cuda.get_device_properties(dev).uuid)
             self.N = N
-            self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
-        except Exception:
-            self.h = None
+            try:
+                uuid = str(torch.cuda.get_device_properties(dev).uuid)
+                self.h = N.nvmlDeviceGetHandleByUUID(uuid if uuid.startswith("GPU-") else "GPU-" + uuid)
+            except Exception:
+                self.h = N.nvmlDeviceGetHandleByIndex(dev)
+            for scheme in ("throughput", "per_link"):
+                self.scheme = scheme
+                if self.read() is not None:
+                    break
+                self.scheme = None
+        except Exception as ex:
+            self.h, self.err = None, repr(ex)
+
+    def _fields(self):
+        if self.scheme == "throughput":
+            return [(k, (f, 0)) for k, f in self.FIELDS.items()]
+        return [(k, (f, l)) for k, f in self.LINK_FIELDS.items() for l in range(self.MAX_LINKS)]
 
     def read(self):
-        if self.h is None:
+        if self.h is None or self.scheme is None:
             return None
         try:
-            vals = self.N.nvmlDeviceGetFieldValues(self.h, list(self.FIELDS.values()))
+            fl = self._fields()
+            vals = self.N.nvmlDeviceGetFieldValues(self.h, [f for _, f in fl])
             out = {}
-            for (k, _), v in zip(self.FIELDS.items(), vals):
+            for (k, _), v in zip(fl, vals):
                 if v.nvmlReturn != 0:
+                    if self.scheme == "per_link":
+                        continue                       # a link that is absent
+                    self.err = f"field {k}: nvmlReturn {v.nvmlReturn}"
                     return None
-                out[k] = float(v.value.ullVal) * 1024.0          # KiB -> bytes
-            return out
-        except Exception:
+                out[k] = out.get(k, 0.0) + float(v.value.ullVal) * (1024.0 if self.scheme == "throughput" else 1.0)
+            return out if out else None
+        except Exception as ex:
+            self.err = repr(ex)
             return None
 
     @staticmethod
@@ -401,12 +423,13 @@ def main():
         """counter-based NVLink GB/s of this GPU (data payload and raw incl. protocol), mean and
         max over ranks; collective"""
         ok = -maxr(-(0.0 if delta is None else 1.0)) > 0          # available on every rank
-        vals = {k: (0.0 if delta is None else delta[k] / sec / 1e9) for k in NvlCounters.FIELDS}
-        rep = {"source": "NVML field values 138-141 (NVLink data / raw TX and RX byte counters) read "
-                         "around the timed region on every rank"}
+        rep = {"source": f"NVML NVLink byte counters ({nvl.scheme} scheme, see NvlCounters) read around the "
+                         "timed region on every rank"}
         if delta is None or not ok:
             rep["available"] = False
+            rep["error"] = nvl.err
             return rep
+        vals = {k: v / sec / 1e9 for k, v in delta.items()}
         for k, v in vals.items():
             rep[f"{k}_gbs_mean"] = sumr(v) / max(world, 1)
             rep[f"{k}_gbs_max"] = maxr(v)

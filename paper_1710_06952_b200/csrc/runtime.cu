@@ -1018,11 +1018,11 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
     const int occ = engine_max_ctas_per_sm(c->engine_threads, c->engine_variant);
     const int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
-    c->engine_grid = cps * sms;
+    const int full = cps * sms;
     // in-process ranks may share one device: by default each takes 1/world of it
     // so that every rank's persistent engine is resident at once
-    if (c->comm_local && c->world > 1) c->engine_grid = std::max(1, c->engine_grid / c->world);
-    if (cfg->engine_grid > 0) c->engine_grid = std::min(c->engine_grid, (int)cfg->engine_grid);
+    c->engine_grid = cfg->engine_grid > 0 ? std::min(full, (int)cfg->engine_grid)
+                                          : ((c->comm_local && c->world > 1) ? std::max(1, full / c->world) : full);
     if (c->engine_grid > kMaxGrid) c->engine_grid = kMaxGrid;
   }
   c->peer_models[c->rank] = c->models;

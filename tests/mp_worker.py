@@ -47,7 +47,7 @@ class DistGroup:
         self.rank, self.world = rank, world
 
     def barrier(self):
-        G.barrier()
+        dist.barrier()
 
     def all_gather(self, obj):
         out = [None] * self.world
