@@ -269,8 +269,10 @@ adpsgd_status adpsgd_step(adpsgd_ctx* ctx, int32_t w, const float* grad, adpsgd_
  *  sampling (idx = (u32*S)>>32, u32 = Philox4x32-10(key=seed, ctr=(lo32(k), m, BATCH, hi32(k)))).
  * flags: 0 = auto, ADPSGD_REPLAY_HOST = stream-ordered per-event kernels (all
  * models, any tau <= T; world 1), ADPSGD_REPLAY_ENGINE = the persistent NVLink
- * engine with device epoch flags (models NONE/QUADRATIC, tau = 0; any world;
- * collective: every rank passes the same schedule).                            */
+ * engine with device epoch flags (models NONE/QUADRATIC, any tau <= T: a stale
+ * read is an op of the worker's sequence computing the gradient at X_{k-tau}
+ * into one of its T + 1 read rows, see adpsgd_plan_replay; no COMPENSATE
+ * events; any world; collective: every rank passes the same schedule).         */
 #define ADPSGD_REPLAY_HOST 1u
 #define ADPSGD_REPLAY_ENGINE 2u
 adpsgd_status adpsgd_replay(adpsgd_ctx* ctx, const adpsgd_event* schedule, int64_t n_events,
@@ -358,14 +360,19 @@ adpsgd_status adpsgd_launch_count(adpsgd_ctx* ctx, int64_t* out);
 adpsgd_status adpsgd_plan_placement(int32_t n, int32_t world_size, int32_t placement,
                                     const int32_t* worker_rank_in, int32_t* worker_rank_out,
                                     int32_t* local_index_out);
-/* The engine-replay plan of `rank`: the events whose updating worker i lives on
- * `rank`, grouped by local worker, each as int64[6] {k, i, j, flags, e_i, e_j}
- * where e_i / e_j are the epochs (counts of earlier schedule events touching
- * i / j, starting from `epochs`) the device waits for.  `epochs` (n entries) is
+/* The engine-replay plan of `rank`: the ops whose worker i lives on `rank`,
+ * grouped by local worker in execution order, each as int64[8]
+ * {k, i, j, flags, e_i, e_j, kind, row}.  kind 0 = an event (k = its index);
+ * kind 2 = a stale read (stale_reads != 0 and tau > 0): the gradient of
+ * event f at X_{f - tau} computed into worker i's read row `row` (f's m-th such
+ * event of i uses row m mod (T + 1)), placed before the first event >= f - tau
+ * touching i; its k is the gradient's random-draw key.  An event with row >= 0
+ * applies that row.  e_i / e_j are the epochs (counts of earlier ops of i / j,
+ * starting from `epochs`) the device waits for; `epochs` (n entries) is
  * advanced in place exactly as on every rank.  out may be NULL to query n_out. */
 adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t rank, const adpsgd_event* schedule,
-                                 int64_t K, int64_t k0, uint32_t* epochs, int64_t* out, int64_t cap,
-                                 int64_t* n_out);
+                                 int64_t K, int64_t k0, int32_t T, int32_t stale_reads, uint32_t* epochs,
+                                 int64_t* out, int64_t cap, int64_t* n_out);
 
 /* Diagnostics: the MLP's tensor-core GEMM on its own.
  * C[M x N] = A[M x K] . B[N x K]^T, fp32 row-major DEVICE pointers on the current

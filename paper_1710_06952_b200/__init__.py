@@ -106,7 +106,7 @@ def lib():
             "adpsgd_reset_stats": ([P], I32), "adpsgd_launch_count": ([P, P], I32),
             "adpsgd_gemm_tf32x3": ([P, P, P, I32, I32, I32, I32], I32),
             "adpsgd_plan_placement": ([I32, I32, I32, P, P, P], I32),
-            "adpsgd_plan_replay": ([I32, P, I32, P, I64, I64, P, P, I64, P], I32),
+            "adpsgd_plan_replay": ([I32, P, I32, P, I64, I64, I32, I32, P, P, I64, P], I32),
             "adpsgd_dpsgd": ([P, I64, P], I32), "adpsgd_dpsgd_reset": ([P, P], I32),
             "adpsgd_dpsgd_read_model": ([P, I32, P], I32),
             "adpsgd_gemm_tf32x3_bench": ([I32, I32, I32, I32, I32, I32, P], I32),
@@ -147,20 +147,21 @@ def plan_placement(n, world_size, placement=0, worker_rank=None):
     return wr, wl
 
 
-def plan_replay(worker_rank, rank, events, k0=0, epochs=None):
-    """Host-only: this rank's engine-replay plan, rows (k, i, j, flags, e_i, e_j);
-    returns (plan, advanced epoch mirror)."""
+def plan_replay(worker_rank, rank, events, k0=0, epochs=None, T=0, stale_reads=False):
+    """Host-only: this rank's engine-replay plan, rows (k, i, j, flags, e_i, e_j,
+    kind, row) -- kind 2 rows are stale reads (see adpsgd.h); returns (plan,
+    advanced epoch mirror)."""
     wr = _arr(worker_rank, np.int32)
     n = wr.size
     ev = _arr(np.asarray(events).reshape(-1, 4), np.int32)
     ep = np.zeros(n, np.uint32) if epochs is None else np.array(epochs, np.uint32)
     m = C.c_int64()
-    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, _ptr(ep), None, 0, C.byref(m)),
-         "plan_replay")
-    out = np.zeros((m.value, 6), np.int64)
+    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, T, int(stale_reads), _ptr(ep), None,
+                                  0, C.byref(m)), "plan_replay")
+    out = np.zeros((m.value, 8), np.int64)
     ep2 = np.zeros(n, np.uint32) if epochs is None else np.array(epochs, np.uint32)
-    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, _ptr(ep2), _ptr(out), m.value,
-                                  C.byref(m)), "plan_replay")
+    _chk(lib().adpsgd_plan_replay(n, _ptr(wr), rank, _ptr(ev), ev.shape[0], k0, T, int(stale_reads), _ptr(ep2),
+                                  _ptr(out), m.value, C.byref(m)), "plan_replay")
     return out, ep2
 
 

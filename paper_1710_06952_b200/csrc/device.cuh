@@ -23,11 +23,12 @@ struct alignas(128) WorkerCtl {
   unsigned int epoch;              // committed events touching this worker (replay order)
   unsigned long long updates;      // committed gradient updates made by this worker (p_i)
   unsigned long long gossips;      // pair averages initiated by / applied to this worker
-  // push request (cross-GPU pair events, two-sided NVLink protocol): the GPU
-  // computing an event asks this worker's home GPU to push the row to it
-  unsigned int req_tag;            // (request seq << 2) | state, written remotely (release.sys)
-  int req_consumer;                // worker whose landing buffer receives the row
-  unsigned int req_tag16;          // consumer's event seq (low 16 bits) for the counters
+  // cooperative cross-GPU event posted in this worker's mailbox (guest_tag):
+  // this GPU's share of its tiles is claimed from guest_next, and at most
+  // guest_nwork CTAs of this GPU join it (both reset by the poster)
+  unsigned int guest_next;
+  unsigned int guest_nwork;
+  unsigned int guest_eseq;         // the initiator slot's event sequence (its pin word's tag)
   // App. A wait-free runtime (home GPU only; persists across adpsgd_run calls):
   // the computation thread's state and the shared gradient buffer g
   unsigned int wf_state;           // 0 = pull next, 1 = computing (until wf_ready_ns)
@@ -49,7 +50,7 @@ struct alignas(128) WorkerCtl {
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
 
-constexpr int kMaxGrid = 1024;     // per-CTA push counters per landing buffer
+constexpr int kMaxGrid = 1024;     // engine CTAs per GPU (upper bound)
 
 // One per rank; rank 0's `ticket` is the system-wide virtual counter k.
 struct alignas(128) GlobalCtl {
@@ -80,14 +81,13 @@ struct Slot;                       // engine slot (internal.h)
 struct WorkerDesc {
   float* x;                        // model row, d_pad floats
   WorkerCtl* ctl;
-  float* land;                     // landing row (partner rows pushed here), null if world 1
-  unsigned int* pcnt;              // kMaxGrid per-CTA push counters of the landing row
   int rank;                        // home rank
   int role;                        // 0 active, 1 passive
   int nb_off, nb_cnt;              // CSR neighbour range
   float straggle;                  // slowdown factor s_w >= 1
   int local;                       // index among this rank's workers, -1 if remote
   float* gb;                       // App. A: two gradient rows (2 * d_pad), local workers only
+  float* gr;                       // engine replay with stale reads: T + 1 read-time gradient rows
   float link;                      // link slowdown L_w >= 1 (emulated slow network, R21)
   Slot* slot;                      // the worker's engine slot (home GPU's control arena; peer-mapped)
 };
@@ -305,22 +305,48 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
 }
 
-// Per-CTA staging pipeline state.  `consumed` advances identically in every
-// thread.  full[s] completes once per use of stage s (TMA bytes landed);
-// empty[s] completes once per use when every warp has copied the stage to
-// registers (one arrival per warp), so no CTA-wide barrier sits in the loop.
-template <int kTile4, int kStages, bool kWarpEmpty = true>
+// Dynamic tile claiming.  An event's float4 range is cut into tiles of kTile4
+// float4; this GPU's share is the tile list t(c) = c * stride + off for c in
+// [0, n) (stride 2 / off 0 or 1 for the halves of a cooperative cross-GPU
+// event, else stride 1).  Thread 0 of a CTA takes chunks of kChunk consecutive
+// c from the shared counter *ctr, so every CTA that has joined an event keeps
+// streaming its tiles until none is left -- no CTA waits for a fixed share,
+// and a CTA stalled on NVLink never holds back the tiles of a local event.
+template <int kChunk>
+struct TileClaim {
+  unsigned int* ctr;
+  unsigned int n, stride, off;
+  unsigned int cur, end;
+  bool out;
+  __device__ __forceinline__ void init(unsigned int* c, unsigned int n_, unsigned int stride_, unsigned int off_) {
+    ctr = c; n = n_; stride = stride_; off = off_; cur = end = 0; out = false;
+  }
+  __device__ __forceinline__ int next() {           // thread 0 only; -1 once exhausted
+    if (cur >= end) {
+      if (out) return -1;
+      const unsigned int b = atomicAdd(ctr, (unsigned int)kChunk);
+      if (b >= n) { out = true; return -1; }
+      cur = b;
+      end = b + kChunk < n ? b + kChunk : n;
+    }
+    return (int)(cur++ * stride + off);
+  }
+};
+
+// Per-CTA staging pipeline: kStages tiles of x_i / x_j in flight, filled by
+// cp.async.bulk (TMA bulk copies, local HBM or a peer GPU alike) completing on
+// an mbarrier (complete_tx).  `consumed` (tile uses so far) advances
+// identically in every thread and sets each stage's mbarrier parity.
+template <int kTile4, int kStages>
 struct Stager {
   float4* buf;      // [kStages][2][kTile4]
-  uint64_t* bar;    // [kStages] full
-  uint64_t* empty;  // [kStages] empty
+  uint64_t* bar;    // [kStages] full barriers
+  int* stile;       // [kStages] tile held by each stage, -1 = none (shared memory)
   uint32_t consumed;
 
-  // tile use g goes into stage g % kStages once use g - kStages has been drained
   __device__ __forceinline__ void issue(uint32_t g, const float4* xi4, const float4* xj4, long long base,
                                         long long hi) {
     const uint32_t s = g % kStages;
-    if (kWarpEmpty && g >= kStages) mbar_wait(empty + s, ((g / kStages) - 1u) & 1u);
     const long long cnt = (hi - base) < kTile4 ? (hi - base) : kTile4;
     const uint32_t bytes = (uint32_t)cnt * 16u;
     mbar_arrive_tx(bar + s, xj4 ? 2u * bytes : bytes);
@@ -328,55 +354,30 @@ struct Stager {
     if (xj4) bulk_g2s(buf + (size_t)s * 2 * kTile4 + kTile4, xj4 + base, bytes, bar + s);
   }
 
-  // One event over the float4 range [0, hi): this CTA takes tiles first,
-  // first + step, first + 2*step, ... (interleaved across the grid, so all
-  // CTAs sweep the rows together -- measured ~5% more HBM throughput than
-  // contiguous per-CTA slices, tools/membench.cu).
-  static __device__ __forceinline__ long long tiles_of(long long first, long long step, long long hi) {
-    const long long tot = (hi + kTile4 - 1) / kTile4;
-    return tot > first ? (tot - first + step - 1) / step : 0;
-  }
-
-  template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
-  __device__ __forceinline__ void run(float4* xi4, float4* xj4, long long first, long long step,
-                                      long long hi, long long d, float gamma, const QuadParams& q,
-                                      uint32_t kk, const float4* g4 = nullptr, uint32_t kkj = 0u) {
-    run_range<kPair, kGrad, kFF, kPreJ>(xi4, xj4, xj4, first, step, hi, 0, tiles_of(first, step, hi), d, gamma,
-                                        q, kk, g4, kkj);
-  }
-
-  // Tiles [t0, t1) of this CTA's list; the partner row is read from xj_src and
-  // the average written to xj_dst (equal for an in-place pair; for a cross-GPU
-  // event xj_src is the local landing row and xj_dst the peer's model row).
-  // kGradExternal reads the gradient row g4 directly (L2), issued before the
-  // stage wait so it overlaps the bulk copies.
-  template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
-  __device__ __forceinline__ void run_range(float4* xi4, const float4* xj_src, float4* xj_dst, long long first,
-                                            long long step, long long hi, long long t0, long long t1,
-                                            long long d, float gamma, const QuadParams& q, uint32_t kk,
-                                            const float4* g4 = nullptr, uint32_t kkj = 0u) {
-    const long long n_t = t1 - t0;
-    if (n_t <= 0) return;
+  // Claim-driven loop shared by events and pulls: thread 0 claims a tile per
+  // stage use and issues its copies kStages uses ahead; every thread reads the
+  // stage's tile from stile[] (written before a CTA barrier the readers pass).
+  // body(tile, a[], b[]) consumes one staged tile.  Returns the tiles done.
+  template <int kClaimChunk, class Body>
+  __device__ __forceinline__ unsigned int drive(TileClaim<kClaimChunk>& cl, const float4* s0, const float4* s1,
+                                                long long hi, Body&& body) {
     if (threadIdx.x == 0) {
       fence_proxy_async();
-      for (long long t = 0; t < n_t && t < kStages; ++t)
-        issue(consumed + (uint32_t)t, xi4, kPair ? xj_src : nullptr, (first + (t0 + t) * step) * kTile4, hi);
-    }
-    for (long long t = 0; t < n_t; ++t) {
-      const uint32_t g = consumed + (uint32_t)t;
-      const uint32_t s = g % kStages;
-      const long long base = (first + (t0 + t) * step) * kTile4;
-      constexpr int kPer = kTile4 / 512;
-      float4 gx[kPer];
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        gx[u] = make_float4(0.f, 0.f, 0.f, 0.f);
-        if (kGrad == kGradExternal) {
-          const long long idx = base + u * 512 + (int)threadIdx.x;
-          if (idx < hi) gx[u] = ld_cg4(g4 + idx);
-        }
+      for (int t = 0; t < kStages; ++t) {
+        const int tile = cl.next();
+        stile[(consumed + t) % kStages] = tile;
+        if (tile >= 0) issue(consumed + t, s0, s1, (long long)tile * kTile4, hi);
       }
+    }
+    __syncthreads();
+    unsigned int done = 0;
+    for (uint32_t g = consumed;; ++g) {
+      const uint32_t s = g % kStages;
+      const int tile = stile[s];
+      if (tile < 0) break;
+      body.prefetch((long long)tile * kTile4);
       mbar_wait(bar + s, (g / kStages) & 1u);
+      constexpr int kPer = kTile4 / 512;
       const float4* sa = buf + (size_t)s * 2 * kTile4;
       const float4* sb = sa + kTile4;
       float4 a[kPer], b[kPer];
@@ -384,120 +385,76 @@ struct Stager {
       for (int u = 0; u < kPer; ++u) {
         const int off = u * 512 + (int)threadIdx.x;
         a[u] = sa[off];
-        b[u] = kPair ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
+        b[u] = s1 ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (kWarpEmpty) {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);   // this warp is done with stage s
-      } else {
-        __syncthreads();                                        // stage s read by every thread
+      __syncthreads();                                  // stage s drained, stile[s] free
+      if (threadIdx.x == 0) {
+        const int nt = cl.next();
+        stile[s] = nt;
+        if (nt >= 0) issue(g + kStages, s0, s1, (long long)nt * kTile4, hi);
       }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const long long idx = base + u * 512 + (int)threadIdx.x;
-        if (idx < hi) {
-          update4<kPair, kGrad, kFF, kPreJ>(a[u], b[u], gx[u], make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4),
-                                            d, gamma, q, kk, kkj);
-          if (kPair) st_cg4(xj_dst + idx, b[u]);
-          st_cg4(xi4 + idx, a[u]);
-        }
-      }
-      if (threadIdx.x == 0 && t + kStages < n_t)
-        issue(g + kStages, xi4, kPair ? xj_src : nullptr, (first + (t0 + t + kStages) * step) * kTile4, hi);
+      body.template consume<kPer>((long long)tile * kTile4, a, b);
+      ++done;
     }
-    consumed += (uint32_t)n_t;
+    consumed += done;
+    return done;
   }
+};
 
-  // App. A pull (computation thread): gout = gradient at the
-  // pulled model x, compensated by the buffered gradient gp when gp != null.
-  // x and gp are staged like x_i / x_j of a pair event; x is not written.
-  __device__ __forceinline__ void pull(const float4* x4, const float4* gp4, float4* gout, long long first,
-                                       long long step, long long hi, long long d, float gamma, const QuadParams& q,
-                                       uint32_t kk) {
-    const long long n_t = tiles_of(first, step, hi);
-    if (n_t <= 0) return;
-    const bool comp = gp4 != nullptr;
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      for (long long t = 0; t < n_t && t < kStages; ++t)
-        issue(consumed + (uint32_t)t, x4, gp4, (first + t * step) * kTile4, hi);
-    }
-    for (long long t = 0; t < n_t; ++t) {
-      const uint32_t g = consumed + (uint32_t)t;
-      const uint32_t s = g % kStages;
-      mbar_wait(bar + s, (g / kStages) & 1u);
-      const float4* sa = buf + (size_t)s * 2 * kTile4;
-      const float4* sb = sa + kTile4;
-      const long long base = (first + t * step) * kTile4;
-      constexpr int kPer = kTile4 / 512;
-      float4 a[kPer], b[kPer];
+// One event's update on staged tiles (Alg. 1 steps 4-6 / App. A order);
+// kP float4 per thread per tile (kTile4 / 512).
+template <int kP, bool kPair, int kGrad, bool kFF, bool kPreJ>
+struct EventBody {
+  float4* xi4;
+  float4* xj4;
+  const float4* g4;
+  long long hi, d;
+  float gamma;
+  QuadParams q;
+  uint32_t kk, kkj;
+  float4 gx[kP];
+  __device__ __forceinline__ void prefetch(long long base) {   // external gradient (L2), before the wait
+    if (kGrad == kGradExternal) {
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const int off = u * 512 + (int)threadIdx.x;
-        a[u] = sa[off];
-        b[u] = comp ? sb[off] : make_float4(0.f, 0.f, 0.f, 0.f);
-      }
-      if (kWarpEmpty) {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
-      } else {
-        __syncthreads();
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
+      for (int u = 0; u < kP; ++u) {
         const long long idx = base + u * 512 + (int)threadIdx.x;
-        if (idx < hi) st_cg4(gout + idx, pull4(a[u], b[u], comp, (uint32_t)(idx * 4), d, gamma, q, kk));
+        gx[u] = idx < hi ? ld_cg4(g4 + idx) : make_float4(0.f, 0.f, 0.f, 0.f);
       }
-      if (threadIdx.x == 0 && t + kStages < n_t)
-        issue(g + kStages, x4, gp4, (first + (t + kStages) * step) * kTile4, hi);
     }
-    consumed += (uint32_t)n_t;
   }
+  template <int kPer>
+  __device__ __forceinline__ void consume(long long base, float4* a, float4* b) {
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+      const long long idx = base + u * 512 + (int)threadIdx.x;
+      if (idx < hi) {
+        update4<kPair, kGrad, kFF, kPreJ>(a[u], b[u], kGrad == kGradExternal ? gx[u] : make_float4(0.f, 0.f, 0.f, 0.f),
+                                          make_float4(0.f, 0.f, 0.f, 0.f), (uint32_t)(idx * 4), d, gamma, q, kk, kkj);
+        if (kPair) st_cg4(xj4 + idx, b[u]);
+        st_cg4(xi4 + idx, a[u]);
+      }
+    }
+  }
+};
 
-  // Push side of a cross-GPU event: copy this CTA's tiles of the local row src
-  // into the consumer's landing row dst (a peer address: NVLink writes only) and
-  // publish progress as cnt = (tag16 << 16) | tiles_done, release at system scope
-  // every kPublish tiles.  Never waits on another GPU.
-  template <int kPublish = 8>
-  __device__ __forceinline__ void push(const float4* src, float4* dst, unsigned int* cnt, unsigned int tag16,
-                                       long long first, long long step, long long hi) {
-    const long long n_t = tiles_of(first, step, hi);
-    if (n_t <= 0) return;
-    if (threadIdx.x == 0) {
-      fence_proxy_async();
-      for (long long t = 0; t < n_t && t < kStages; ++t)
-        issue(consumed + (uint32_t)t, src, nullptr, (first + t * step) * kTile4, hi);
-    }
-    for (long long t = 0; t < n_t; ++t) {
-      const uint32_t g = consumed + (uint32_t)t;
-      const uint32_t s = g % kStages;
-      mbar_wait(bar + s, (g / kStages) & 1u);
-      const float4* sa = buf + (size_t)s * 2 * kTile4;
-      const long long base = (first + t * step) * kTile4;
-      constexpr int kPer = kTile4 / 512;
-      float4 a[kPer];
+// A gradient read (App. A pull, or the read-time gradient of an
+// engine-replayed stale read): gout = gradient at the staged x,
+// compensated by the staged gp when comp.
+struct ReadBody {
+  float4* gout;
+  long long hi, d;
+  float gamma;
+  QuadParams q;
+  uint32_t kk;
+  bool comp;
+  __device__ __forceinline__ void prefetch(long long) {}
+  template <int kPer>
+  __device__ __forceinline__ void consume(long long base, float4* a, float4* b) {
 #pragma unroll
-      for (int u = 0; u < kPer; ++u) a[u] = sa[u * 512 + (int)threadIdx.x];
-      if (kWarpEmpty) {
-        __syncwarp();
-        if ((threadIdx.x & 31) == 0) mbar_arrive(empty + s);
-      } else {
-        __syncthreads();
-      }
-#pragma unroll
-      for (int u = 0; u < kPer; ++u) {
-        const long long idx = base + u * 512 + (int)threadIdx.x;
-        if (idx < hi) st_cg4(dst + idx, a[u]);
-      }
-      if (threadIdx.x == 0 && t + kStages < n_t)
-        issue(g + kStages, src, nullptr, (first + (t + kStages) * step) * kTile4, hi);
-      if ((t + 1) % kPublish == 0 || t + 1 == n_t) {
-        __threadfence_system();                   // every thread's peer stores are performed
-        __syncthreads();
-        if (threadIdx.x == 0) st_release_sys(cnt, (tag16 << 16) | (unsigned int)(t + 1));
-      }
+    for (int u = 0; u < kPer; ++u) {
+      const long long idx = base + u * 512 + (int)threadIdx.x;
+      if (idx < hi) st_cg4(gout + idx, pull4(a[u], b[u], comp, (uint32_t)(idx * 4), d, gamma, q, kk));
     }
-    consumed += (uint32_t)n_t;
   }
 };
 

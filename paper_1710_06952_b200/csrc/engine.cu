@@ -1,6 +1,6 @@
-// engine.cu -- the persistent AD-PSGD engine: one cooperative kernel per GPU
-// runs every local worker's loop of the wait-free runtime (App. A)
-// on the device, with no host round trip per event.
+// engine.cu -- the persistent AD-PSGD engine: one persistent kernel per GPU
+// runs every local worker's loop of the asynchronous runtime on the device,
+// with no host round trip per event.
 //
 // Per local worker w, in free-running mode (mode 0):
 //   1. compute phase: emulated gradient time s_w * t_c (timer; no SM spinning)
@@ -11,26 +11,29 @@
 //      (P:458-479).  A failed try-lock leaves the worker pending; no CTA
 //      ever blocks on it.
 //   3. take ticket k (CAS on rank 0's counter, bounded by the run's target):
-//      the virtual counter of P:429-432, taken while holding the lock so the
-//      ticket order is the serialisation order (log replay).
-//   4. fused pass over d, split across ALL CTAs of the grid (interleaved tiles):
-//      m = fl(fl(x_w + x_j)*0.5); x_j <- m; x_w <- fl(m - fl(gamma g)),
-//      g = quadratic gradient at the pre-average x_w (tau = 0) -- Alg. 1 steps
-//      4-6, reading R1.
-//   5. the CTA finishing the last slice commits: log {k,i,j,0}, counters,
+//      the virtual counter of P:429-432 (reading R23), taken while holding the
+//      lock so the ticket order is the serialisation order (log replay).
+//   4. fused pass over d: m = fl(fl(x_w + x_j)*0.5); x_j <- m;
+//      x_w <- fl(m - fl(gamma g)), g = the quadratic gradient at the pre-average
+//      x_w (tau = 0) -- Alg. 1 steps 4-6, reading R1.
+//   5. the CTA whose leave finishes the event commits: log {k,i,j,0}, counters,
 //      release fence (sys), unlock, schedule the next compute phase.
-// Replay mode (mode 1): the event list of each local worker is consumed in
-// order; event k starts when epoch[i] == e_i(k) and epoch[j] == e_j(k) (device
-// epoch flags, system scope), and commits by bumping both epochs.
+// Replay mode (mode 1): the op list of each local worker is consumed in order;
+// an op starts when epoch[i] == e_i and epoch[j] == e_j (device epoch flags,
+// system scope) and bumps both epochs at commit.  A stale read (tau > 0,
+// X_hat = X_{k - tau}) is its own op, placed in worker i's sequence
+// where X_{k - tau} holds: it computes the gradient into one of the worker's
+// T + 1 read rows, which the event applies later.
 //
-// Cross-GPU pairs (world > 1), two-sided: the GPU computing the event posts a
-// push request on the partner's home GPU, whose engine copies x_j tile by tile
-// into the computing GPU's landing row (NVLink writes) and publishes per-CTA
-// progress counters; the computing CTAs consume tiles as they land (never
-// blocking: they return to the scheduler when nothing has landed) and write the
-// average back into x_j (NVLink writes).  NVLink then carries writes only, in
-// both directions: tools/membench measured 672 GB/s per direction for
-// bidirectional pushes vs 476 GB/s when one GPU both reads and writes its peer.
+// Work distribution: an event's float4 range is cut into tiles of kTile4; the
+// CTAs that join an event claim tile chunks from its counter until none is
+// left (TileClaim), so a CTA held up on NVLink never delays a local event's
+// tiles.  Joining pins the event (Slot::pin counts unfinished tiles plus
+// joined CTAs under the event's sequence tag), so it cannot commit -- and its
+// slot cannot be reused -- while a CTA still reads its fields; the CTA whose
+// leave brings the pin to zero commits.  A cross-GPU event is joined by at most
+// grid / kCrossDiv CTAs per GPU (it is NVLink-bound); with cooperative events
+// the partner GPU claims the odd tiles (its half) from its own mailbox counter.
 #include "internal.h"
 
 namespace adp {
@@ -38,42 +41,39 @@ namespace adp {
 namespace {
 
 constexpr int kEngineThreads = 512;
-constexpr int kEngineUnroll = 2;
 constexpr int kExit = -2;
-constexpr int kPickPush = 1 << 20;      // pick codes >= kPickPush: push request of local worker
-constexpr int kPickGuest = kPickPush - 1; // a peer's cooperative event posted in a local mailbox
+constexpr int kPickGuest = 1 << 20;     // a peer's cooperative event posted in a local mailbox
+constexpr int kTile4 = 1536;            // float4 per stream per stage (24 KB); round-1 A/B: 1536x2 stages
+                                        // 0.869-0.871 of the HBM peak vs 1024x3 0.863-0.867, 512x6 0.82
+constexpr int kStages = 2;
+constexpr int kClaimChunk = 2;          // tiles per claim
+constexpr int kCrossDiv = 4;            // CTAs per GPU on one cross-GPU event: grid / 4 (round-1 A/B at
+                                        // N=2: 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k steps/s)
+constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
+using EngineStager = Stager<kTile4, kStages>;
+using Claim = TileClaim<kClaimChunk>;
+constexpr int kPer = kTile4 / 512;
 
-struct SmemSlot {                  // tid 0 copies the running event here for the CTA
+struct SmemSlot {                  // tid 0 copies the joined event here for the CTA
   float* xi;
   float* xj;
-  float* land;
-  long long k;
   int grad;
   int pair;
-  int cross;                       // partner row lives on another GPU (P2P stores)
-  long long t0, t1;                // tile sub-range (two-sided cross consume)
-  // push request
-  const float* src;
-  float* dst;
-  unsigned int* cnt;
-  unsigned int tag16;
-  // App. A: flush-first order, pulls, buffered gradients
-  int ff;
+  int cross;                       // partner row lives on another GPU (peer loads / stores)
+  int ff;                          // App. A order (flush first)
   int kind;
   unsigned long long key;
   const float* g;
   float* gout;
   int absorb;                      // fused passive local step (event k-1) before the pair
-  // tile split and arrival: own events use (blockIdx, grid) or, when
-  // cooperative, (blockIdx, 2 grid); a guest (a peer's cooperative event) uses
-  // (grid + blockIdx, 2 grid) and arrives on the initiator's slot
-  long long first, step;
-  int ncta;                        // CTAs that arrive on the event's counter
-  int coop;
-  int guest;
-  int gl;                          // local worker whose mailbox carried the guest event
-  unsigned int* gdone;             // initiator's slot->done (peer)
-  unsigned int* gready;            // initiator's slot->commit_ready (peer)
+  // this CTA's claim on the event: tile c of its share is c * stride + off
+  unsigned int* ctr;
+  unsigned int n, stride, off;
+  unsigned long long* pin;         // the initiator slot's pin word (peer memory for a guest)
+  int guest;                       // a peer's cooperative event (our half)
+  int slot;                        // local slot (own events) or mailbox index (guest)
+  unsigned int seq;                // the slot's / mailbox's sequence
+  unsigned int* gready;            // initiator's slot->commit_ready (peer; guest events)
 };
 
 __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st) { return (seq << 2) | st; }
@@ -81,6 +81,28 @@ __device__ __forceinline__ unsigned int tag_of(unsigned int seq, unsigned int st
 __device__ void latch_error(const EngineParams& p, unsigned int code) {
   atomicCAS(&p.gctl->error, 0u, code);
   atomicExch(&p.gctl->abort_flag, 1u);
+}
+
+__device__ __forceinline__ unsigned int event_tiles(const EngineParams& p) {
+  return (unsigned int)((p.n4 + kTile4 - 1) / kTile4);
+}
+
+// Join an event: +1 on its pin unless the event is over or another one holds
+// the slot (sequence tag).  System scope: a partner GPU's CTAs pin it too.
+__device__ __forceinline__ bool pin_join(unsigned long long* pin, unsigned int seq) {
+  unsigned long long w = ld_relaxed_sys64(pin);
+  while (true) {
+    if ((unsigned int)(w >> 32) != seq || (w & 0xffffffffull) == 0ull) return false;
+    const unsigned long long old = atomicCAS_system(pin, w, w + 1ull);
+    if (old == w) return true;
+    w = old;
+  }
+}
+// Leave it, crediting the tiles this CTA finished; true if this leave ends it.
+__device__ __forceinline__ bool pin_leave(unsigned long long* pin, unsigned int tiles) {
+  const unsigned long long dec = (unsigned long long)tiles + 1ull;
+  const unsigned long long old = atomicAdd_system(pin, 0ull - dec);
+  return (old & 0xffffffffull) == dec;
 }
 
 // tickets k, k+1, ..: up to `want` consecutive values of rank 0's counter below
@@ -99,37 +121,34 @@ __device__ __forceinline__ bool take_ticket(const EngineParams& p, unsigned long
   return take_tickets(p, k, 1) == 1;
 }
 
-__device__ void publish_running(Slot* sl, unsigned int seq) {
-  __threadfence();                                   // fields before the tag
+// Make the slot's event (fields already written) visible as running: fresh
+// claim counter, pin = (new seq, all tiles), then the tag.
+__device__ void publish_running(const EngineParams& p, Slot* sl, unsigned int seq) {
+  const unsigned int T = event_tiles(p);
+  sl->next = 0u;
+  sl->nwork = 0u;
+  sl->ntiles = T;
+  sl->commit_ready = 0u;
+  *(volatile unsigned long long*)&sl->pin = ((unsigned long long)(seq + 1u) << 32) | T;
+  __threadfence_system();                            // fields before the tag (a guest reads them)
   st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
 }
 
 // Cooperative cross-GPU event: after publishing event seq+1 in worker w's slot,
-// post it in partner j's guest mailbox (j's home GPU) so that GPU's CTAs take
-// half of the tiles -- both GPUs then drive NVLink (reads of the other row and
-// writes of the results in both directions) instead of one.
-// The mailbox has its own sequence (a partner serves events of several
-// initiators, whose slot sequences may coincide); the poster holds the partner
-// exclusively (its lock or its epoch), so read-increment is race-free.
-__device__ void post_guest(const EngineParams& p, Slot* sl, int w, int j) {
+// post it in partner j's guest mailbox (j's home GPU) so that GPU's CTAs claim
+// the odd tiles -- both GPUs then drive NVLink (reads of the other row and
+// writes of the results in both directions) instead of one.  The mailbox has
+// its own sequence (a partner serves events of several initiators); the poster
+// holds the partner exclusively (its lock or its epoch), so read-increment is
+// race-free.
+__device__ void post_guest(Slot* sl, const EngineParams& p, int w, int j, unsigned int eseq) {
   WorkerCtl* cj = p.workers[j].ctl;                   // peer memory
-  __threadfence_system();                             // the slot's fields, system-wide
   *(volatile int*)&cj->guest_i = w;
+  *(volatile unsigned int*)&cj->guest_next = 0u;
+  *(volatile unsigned int*)&cj->guest_nwork = 0u;
+  *(volatile unsigned int*)&cj->guest_eseq = eseq;
+  __threadfence_system();
   st_release_sys(&cj->guest_tag, tag_of(sl->gseq, kStateRunning));
-}
-
-// cross-GPU event (two-sided): ask j's home GPU to push x_j into our landing row
-__device__ void post_push_request(const EngineParams& p, Slot* sl, int w, int j, unsigned int seq) {
-  const WorkerDesc& dw = p.workers[w];
-  const unsigned int tag16 = (seq + 1) & 0xffffu;    // the seq this event is published with
-  sl->tag16 = tag16;
-  sl->land = dw.land;
-  sl->pcnt = dw.pcnt;
-  WorkerCtl* cj = p.workers[j].ctl;                   // peer memory
-  const unsigned int rq = ld_acquire_sys(&cj->req_tag) >> 2;
-  *(volatile int*)&cj->req_consumer = w;
-  *(volatile unsigned int*)&cj->req_tag16 = tag16;
-  st_release_sys(&cj->req_tag, ((rq + 1u) << 2) | kStateRunning);
 }
 
 // App. A wait-free runtime, reading R20.  A worker runs two
@@ -182,8 +201,7 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
     sl->gout = dw.gb + (long long)(cw->wf_buf ^ 1u) * dpad;
     sl->ctl_i = dw.ctl; sl->ctl_j = nullptr; sl->lock = lock; sl->cross = 0;
     sl->t0 = now;
-    sl->done = 0;
-    publish_running(sl, seq);
+    publish_running(p, sl, seq);
     return true;
   }
   const bool flush = cw->wf_pub != 0u;                 // communication thread
@@ -217,18 +235,18 @@ __device__ __noinline__ bool start_wait_free(const EngineParams& p, Slot* sl, un
   sl->tau = flush ? (int)(k - cw->wf_tread_pub) : 0;
   sl->flags = flush ? (2u | (cw->wf_comp_pub ? 4u : 0u)) : 1u;
   sl->g = flush ? dw.gb + (long long)cw->wf_buf * dpad : nullptr;
+  sl->gout = nullptr;
   sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
   sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
   sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
   if (j >= 0) { sl->pending_j = -2; sl->nb_ctr += 1; }
   sl->t0 = now;
-  sl->done = 0;
-  publish_running(sl, seq);
+  publish_running(p, sl, seq);
   return true;
 }
 
-// Called by tid 0 of some CTA that found no slice to do.  Returns true if it
-// started or finished a worker (progress).
+// Called by tid 0 of some CTA that found no tile to work on.  Returns true if
+// it started or finished a worker (progress).
 __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned int tag, unsigned long long now) {
   Slot* sl = p.slots + s;
   const unsigned int seq = tag >> 2;
@@ -276,21 +294,32 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
       return false;
     }
     __threadfence_system();                                 // acquire their data
+    const long long dpad = p.n4 * 4;
     sl->i = w; sl->j = e.j; sl->tau = 0; sl->flags = e.flags; sl->k = e.k;
-    sl->kind = kKindEvent; sl->g = nullptr; sl->absorb = -1;
-    sl->key = (e.flags & 2u) ? read_key((unsigned long long)e.k, w) : (unsigned long long)e.k;   // R20
+    sl->absorb = -1; sl->lock = nullptr;
     sl->xi = dw.x; sl->xj = e.j >= 0 ? p.workers[e.j].x : nullptr;
-    sl->ctl_i = dw.ctl; sl->ctl_j = cj; sl->lock = nullptr;
-    sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
-    if (sl->cross && p.two_sided) post_push_request(p, sl, w, e.j, seq);
-    sl->coop = sl->cross && p.coop;
-    sl->commit_ready = 0u;
+    sl->ctl_i = dw.ctl; sl->ctl_j = cj;
+    sl->key = (e.flags & 2u) ? read_key((unsigned long long)e.k, w) : (unsigned long long)e.k;   // R20
+    if (e.kind == kKindRead) {                              // stale read: g at X_{k - tau}
+      sl->kind = kKindRead;
+      sl->key = (unsigned long long)e.k;                    // e.k holds the read's key (plan_replay)
+      sl->g = nullptr;
+      sl->gout = dw.gr + (long long)e.grow * dpad;
+      sl->xj = nullptr; sl->ctl_j = nullptr; sl->j = -1;
+      sl->cross = 0; sl->coop = 0;
+    } else {
+      sl->kind = kKindEvent;
+      sl->g = e.grow >= 0 ? dw.gr + (long long)e.grow * dpad : nullptr;   // read earlier by a kKindRead op
+      sl->gout = nullptr;
+      sl->cross = e.j >= 0 && p.workers[e.j].rank != p.my_rank;
+      // a guest cannot read a gradient row (not peer-mapped): such events stay one-sided
+      sl->coop = sl->cross && p.coop && !sl->g;
+    }
     if (sl->coop) sl->gseq = (ld_acquire_sys(&p.workers[e.j].ctl->guest_tag) >> 2) + 1u;
     sl->ev_cur = cur + 1;
     sl->t0 = now;
-    sl->done = 0;
-    publish_running(sl, seq);
-    if (sl->coop) post_guest(p, sl, w, e.j);
+    publish_running(p, sl, seq);
+    if (sl->coop) post_guest(sl, p, w, e.j, seq + 1);
     return true;
   }
   // ------------------------------------------------------- free-running ----
@@ -358,27 +387,24 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
   if (absorb >= 0) ++k;                                     // the pair is the second event
   sl->absorb = absorb;
   sl->i = w; sl->j = j; sl->tau = 0; sl->flags = p.model == 0 ? 1u : 0u; sl->k = (long long)k;
-  sl->kind = kKindEvent; sl->key = k; sl->g = nullptr;
+  sl->kind = kKindEvent; sl->key = k; sl->g = nullptr; sl->gout = nullptr;
   sl->xi = dw.x; sl->xj = j >= 0 ? p.workers[j].x : nullptr;
   sl->ctl_i = dw.ctl; sl->ctl_j = j >= 0 ? p.workers[j].ctl : nullptr; sl->lock = lock;
   sl->cross = j >= 0 && p.workers[j].rank != p.my_rank;
-  if (sl->cross && p.two_sided) post_push_request(p, sl, w, j, seq);
   sl->coop = sl->cross && p.coop;
-  sl->commit_ready = 0u;
   if (sl->coop) sl->gseq = (ld_acquire_sys(&p.workers[j].ctl->guest_tag) >> 2) + 1u;
   sl->pending_j = -2;
   sl->nb_ctr += 1;
   sl->t0 = now;
-  sl->done = 0;
-  publish_running(sl, seq);
-  if (sl->coop) post_guest(p, sl, w, j);
+  publish_running(p, sl, seq);
+  if (sl->coop) post_guest(sl, p, w, j, seq + 1);
   return true;
 }
 
-// Called by tid 0 of the CTA that finished the last slice of slot s.
+// Called by tid 0 of the CTA whose leave finished the event of slot s.
 __device__ __noinline__ void commit(const EngineParams& p, int s) {
   Slot* sl = p.slots + s;
-  __threadfence_system();                 // every slice's stores (fenced by their CTAs) first
+  __threadfence_system();                 // every tile's stores (fenced by their CTAs) first
   const unsigned long long now = globaltimer();
   const double d4 = 4.0 * (double)p.d;
   if (sl->kind == kKindPull) {            // App. A: g' computed; its compute phase starts now
@@ -388,6 +414,15 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     atomicAdd(&p.gctl->st_bytes, (sl->g ? 3.0 : 2.0) * d4);
     atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
     if (sl->lock) { __threadfence_system(); atomicExch_system(sl->lock, 0u); }
+    const unsigned int seq = sl->tag >> 2;
+    st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
+    return;
+  }
+  if (sl->kind == kKindRead) {            // replay stale read done: the worker's next op may run
+    atomicAdd(&p.gctl->st_bytes, 2.0 * d4);
+    atomicAdd(&p.gctl->st_busy_ns, now - sl->t0);
+    __threadfence_system();
+    atomicAdd_system(&sl->ctl_i->epoch, 1u);
     const unsigned int seq = sl->tag >> 2;
     st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
     return;
@@ -418,7 +453,7 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
     st_release_gpu(&sj->tag, tag_of(sj->tag >> 2, kStateIdle));
   }
   // stats: algorithmic bytes: pair 16d, local 8d; NVLink 8d per cross
-  // pair; a flushed App. A buffer adds its 4d read; a fused passive step adds
+  // pair; an applied gradient row adds its 4d read; a fused passive step adds
   // nothing (its row is already read and written by the pair)
   atomicAdd(&p.gctl->st_events, 1ull);
   if (j >= 0) atomicAdd(&p.gctl->st_pair, 1ull);
@@ -469,251 +504,134 @@ __device__ __noinline__ void commit(const EngineParams& p, int s) {
   st_release_gpu(&sl->tag, tag_of(seq, kStateIdle));
 }
 
-// tile x stages, fixed-mix A/B (tools/ab_engine.py, mixed / local-only GB/s):
-// 512x4 5356/4774, 1024x3 5488/5129, 1536x2 5589/5109, 2048x2 5491/5010 (2048x2
-// needs 128 KB: one CTA per SM).  Whole bench (tools/ab_build.py + bench.py
-// --no-extras, 3 runs each): 1536x2 0.869-0.871 of the HBM peak, 1024x3
-// 0.863-0.867, 512x6 0.819-0.824.
-#ifndef ADPSGD_TILE4
-#define ADPSGD_TILE4 1536
-#endif
-#ifndef ADPSGD_STAGES
-#define ADPSGD_STAGES 2
-#endif
-constexpr int kTile4 = ADPSGD_TILE4;     // float4 per stream per stage (24 KB)
-constexpr int kStages = ADPSGD_STAGES;
-constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + 2 * kStages * sizeof(uint64_t);
-
-// engine variants: 0 = bulk-copy staged, CTA barrier per tile (default);
-// 1 = register slices (no staging, one-sided cross access); 2 = bulk-copy
-// staged, per-warp empty mbarriers.  tools/ab_engine.py on a fixed 512-event
-// mix at d = 25.6M: 5404 / 4996 / 5324 GB/s (variant 0 / 1 / 2).
-template <int kVar>
-using EngineStager = Stager<kTile4, kStages, kVar == 2>;
-
-template <int kVar, bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
-__device__ __forceinline__ void slice(const EngineParams& p, const SmemSlot& e, EngineStager<kVar>& stg) {
-  const uint32_t kk = quad_event_key_h(p.q.noise_key, e.key);
-  const uint32_t kkj = kPreJ ? quad_event_key_h(p.q.noise_key, e.key - 1ull) : 0u;   // the passive's event k-1
-  float4* xi4 = reinterpret_cast<float4*>(e.xi);
-  float4* xj4 = reinterpret_cast<float4*>(e.xj);
-  const float4* g4 = reinterpret_cast<const float4*>(e.g);
-  if (kVar != 1) {
-    if (e.cross && p.two_sided)             // consume landed tiles [t0, t1); average back to x_j
-      stg.template run_range<kPair, kGrad, kFF>(xi4, reinterpret_cast<const float4*>(e.land), xj4, blockIdx.x,
-                                                gridDim.x, p.n4, e.t0, e.t1, p.d, p.gamma, p.q, kk, g4);
-    else
-      stg.template run<kPair, kGrad, kFF, kPreJ>(xi4, xj4, e.first, e.step, p.n4, p.d, p.gamma, p.q, kk, g4, kkj);
-  } else {
-    const long long per = (p.n4 + gridDim.x - 1) / gridDim.x;
-    const long long lo = (long long)blockIdx.x * per;
-    const long long hi = lo + per < p.n4 ? lo + per : p.n4;
-    event_range<kPair, kGrad, kEngineUnroll, kFF>(xi4, xj4, g4, nullptr, lo, hi, threadIdx.x, blockDim.x, p.d,
-                                                  p.gamma, p.q, kk);
-  }
+// The staged pass of one joined event over the tiles this CTA claims.
+template <bool kPair, int kGrad, bool kFF = false, bool kPreJ = false>
+__device__ __forceinline__ unsigned int event_pass(const EngineParams& p, const SmemSlot& e, EngineStager& stg,
+                                                   Claim& cl) {
+  EventBody<kPer, kPair, kGrad, kFF, kPreJ> body;
+  body.xi4 = reinterpret_cast<float4*>(e.xi);
+  body.xj4 = reinterpret_cast<float4*>(e.xj);
+  body.g4 = reinterpret_cast<const float4*>(e.g);
+  body.hi = p.n4;
+  body.d = p.d;
+  body.gamma = p.gamma;
+  body.q = p.q;
+  body.kk = quad_event_key_h(p.q.noise_key, e.key);
+  body.kkj = kPreJ ? quad_event_key_h(p.q.noise_key, e.key - 1ull) : 0u;   // the passive's event k-1
+  return stg.drive(cl, body.xi4, kPair ? body.xj4 : nullptr, p.n4, body);
 }
 
-template <int kVar>
 __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_constant__ EngineParams p) {
   extern __shared__ __align__(128) unsigned char dyn_smem[];
-  __shared__ unsigned int done_seq[kMaxLocal];   // last event seq this CTA finished, per slot
-  __shared__ unsigned int push_seq[kMaxLocal];   // last push request seq this CTA served, per worker
-  __shared__ unsigned int cons_seq[kMaxLocal];   // event seq cons_cnt refers to
-  __shared__ unsigned int cons_cnt[kMaxLocal];   // tiles of a cross event consumed so far
-  __shared__ unsigned int gdone_seq[kMaxLocal];  // last guest event seq this CTA finished, per mailbox
+  __shared__ unsigned int done_seq[kMaxLocal];   // last event seq this CTA is done with, per slot
+  __shared__ unsigned int gdone_seq[kMaxLocal];  // last guest event seq this CTA is done with, per mailbox
   __shared__ int s_pick;
-  __shared__ unsigned int s_seq;
+  __shared__ int s_stile[kStages];
   __shared__ SmemSlot s_ev;
-  EngineStager<kVar> stg;
+  EngineStager stg;
   stg.buf = reinterpret_cast<float4*>(dyn_smem);
   stg.bar = reinterpret_cast<uint64_t*>(dyn_smem + (size_t)kStages * 2 * kTile4 * sizeof(float4));
-  stg.empty = stg.bar + kStages;
+  stg.stile = s_stile;
   stg.consumed = 0;
-  if (kVar != 1 && threadIdx.x == 0) {
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(stg.bar + s, 1);
-      mbar_init(stg.empty + s, kEngineThreads / 32);
-    }
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < kStages; ++s) mbar_init(stg.bar + s, 1);
     mbar_fence_init();
   }
   for (int s = threadIdx.x; s < kMaxLocal; s += blockDim.x) {
     done_seq[s] = 0u;
-    cons_seq[s] = 0u;
-    cons_cnt[s] = 0u;
     gdone_seq[s] = 0u;
-    push_seq[s] = 0xffffffffu;
   }
   __syncthreads();
-  if (p.two_sided)                           // push requests this CTA served in earlier launches
-    for (int l = threadIdx.x; l < p.n_local; l += blockDim.x) push_seq[l] = p.served[l * kMaxGrid + blockIdx.x];
-  __syncthreads();
   const int L = p.n_local;
-#ifdef ADPSGD_ROT0
-  const int rot = 0;                         // A/B: every CTA prefers the same running event
-#else
   const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
-#endif
-  const long long my_tiles = EngineStager<kVar>::tiles_of(blockIdx.x, gridDim.x, p.n4);
-  // An event of fewer tiles than CTAs (small d) is taken by `part` CTAs only,
-  // rotated by the slot index so that concurrent small events use disjoint CTAs;
-  // the others neither pick it up nor arrive on its counter.
-#ifndef ADPSGD_MIN_TILES_PER_CTA
-#define ADPSGD_MIN_TILES_PER_CTA 4   // config 2 A/B (d = 2^20): 1 -> 79k, 2 -> 91k, 4 -> 96k, 8 -> 92k replay events/s
-#endif
-  const int tiles_ev = (int)((p.n4 + kTile4 - 1) / kTile4);
-  const int want = (tiles_ev + ADPSGD_MIN_TILES_PER_CTA - 1) / ADPSGD_MIN_TILES_PER_CTA;
-  const int part = (kVar == 1 || want >= (int)gridDim.x) ? (int)gridDim.x : (want > 0 ? want : 1);
-  // A cross-GPU event is bound by NVLink (~1/8 of HBM), so it is given a
-  // fraction of the CTAs (rotated by slot, like small events): the rest keep
-  // streaming local events from HBM meanwhile instead of every CTA stalling on
-  // its share of the remote tiles.  Both GPUs of a cooperative event use the same
-  // fraction (same grid), so the arrival count is 2 * xpart.
-#ifndef ADPSGD_CROSS_RESERVE
-#define ADPSGD_CROSS_RESERVE 0   // A/B (tools/ab_reserve.sh): 1 -> N=2 13.5k vs 14.5k, N=4 26.5k vs 28.4k (dropped)
-#endif
-  constexpr bool kReserve = ADPSGD_CROSS_RESERVE != 0;
-#ifndef ADPSGD_CROSS_DIV
-#define ADPSGD_CROSS_DIV 4   // N=2 A/B (bench --no-extras, coop auto): 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k gossip-steps/s
-#endif
-  const int xpart = kVar == 1 ? (int)gridDim.x
-                    : max(1, min(part, (int)gridDim.x / (ADPSGD_CROSS_DIV > 1 ? ADPSGD_CROSS_DIV : 1)));
+  const unsigned int T = event_tiles(p);
+  const unsigned int xpart = max(1u, gridDim.x / (unsigned)kCrossDiv);
+  Claim cl;                                     // thread 0's claim on the joined event
   unsigned long long last_progress = globaltimer();
   while (true) {
     if (threadIdx.x == 0) {
       int pick = -1;
       if (ld_acquire_gpu(&p.gctl->abort_flag)) pick = kExit;
-      // 1. push requests from other GPUs (they unblock remote consumers; never wait)
-      if (p.two_sided)
-        for (int t = 0; t < L && pick == -1; ++t) {
-          const int l = (t + rot) % L;
-          WorkerCtl* c = p.workers[p.local_ids[l]].ctl;
-          const unsigned int tag = ld_acquire_sys(&c->req_tag);
-          if ((tag & 3u) == kStateRunning && (tag >> 2) != push_seq[l]) {
-            const int ci = *(volatile int*)&c->req_consumer;
-            s_ev.src = p.workers[p.local_ids[l]].x;
-            s_ev.dst = p.workers[ci].land;
-            s_ev.cnt = p.workers[ci].pcnt + blockIdx.x;
-            s_ev.tag16 = *(volatile unsigned int*)&c->req_tag16;
-            s_seq = tag >> 2;
-            pick = kPickPush + l;
-          }
-        }
-      auto scan_guests = [&]() {
-        // 2b. cooperative events of peer GPUs posted in our workers' mailboxes
-        if (p.coop)
-          for (int t = 0; t < L && pick == -1; ++t) {
-            const int l = (t + rot) % L;
-            const int wl = p.local_ids[l];
-            WorkerCtl* cl = p.workers[wl].ctl;
-            const unsigned int gt = ld_acquire_sys(&cl->guest_tag);
-            if ((gt & 3u) != kStateRunning || (gt >> 2) == gdone_seq[l]) continue;
-            int grb = (int)blockIdx.x;
-            if (xpart < (int)gridDim.x) {
-              const int base = kReserve && p.reserve ? (int)gridDim.x - xpart
-                                                     : (int)(((unsigned int)l * (unsigned int)xpart) % gridDim.x);
-              grb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
-              if (grb >= xpart) { gdone_seq[l] = gt >> 2; continue; }  // not one of this event's CTAs
-            }
-            const int gi = *(volatile int*)&cl->guest_i;
-            Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
-            const unsigned int fl = *(volatile unsigned int*)&sa->flags;
-            s_ev.xi = p.workers[gi].x;
-            s_ev.xj = p.workers[wl].x;
-            s_ev.k = *(volatile long long*)&sa->k;
-            s_ev.key = *(volatile unsigned long long*)&sa->key;
-            s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
-            s_ev.ff = (fl & 2u) ? 1 : 0;
-            s_ev.kind = kKindEvent;
-            s_ev.g = nullptr;
-            s_ev.gout = nullptr;
-            s_ev.absorb = 0;
-            s_ev.pair = 1;
-            s_ev.cross = 1;
-            s_ev.t0 = s_ev.t1 = 0;
-            s_ev.coop = 1;
-            s_ev.first = (long long)xpart + grb;
-            s_ev.step = 2ll * xpart;
-            s_ev.ncta = 2 * xpart;
-            s_ev.guest = 1;
-            s_ev.gl = l;
-            s_ev.gdone = &sa->done;
-            s_ev.gready = &sa->commit_ready;
-            s_seq = gt >> 2;
-            pick = kPickGuest;
-          }
-      };
-#ifdef ADPSGD_GUEST_FIRST
-      scan_guests();
-#endif
-      // 2. running events with work for this CTA
+      // 1. running events of local workers with tiles left to claim
       for (int t = 0; t < L && pick == -1; ++t) {
         const int s = (t + rot) % L;
-        const unsigned int tag = ld_acquire_gpu(&p.slots[s].tag);
-        if (p.coop && (tag & 3u) == kStateRunning && *(volatile int*)&p.slots[s].coop) {
-          const unsigned int g = *(volatile unsigned int*)&p.slots[s].gseq;
-          if (ld_acquire_sys(&p.slots[s].commit_ready) == g && atomicCAS(&p.slots[s].commit_ready, g, 0u) == g) {
-            commit(p, s);                                   // last arrival was on the partner GPU
+        Slot* sl = p.slots + s;
+        const unsigned int tag = ld_acquire_gpu(&sl->tag);
+        if (p.coop && (tag & 3u) == kStateRunning && *(volatile int*)&sl->coop) {
+          const unsigned int g = *(volatile unsigned int*)&sl->gseq;
+          if (ld_acquire_sys(&sl->commit_ready) == g && atomicCAS(&sl->commit_ready, g, 0u) == g) {
+            commit(p, s);                                   // the last leave was on the partner GPU
             continue;
           }
         }
-        if ((tag & 3u) != kStateRunning || (tag >> 2) == done_seq[s]) continue;
-        Slot* sl = p.slots + s;
-        int rb = (int)blockIdx.x;
-        const int cross = *(volatile int*)&sl->cross;
+        const unsigned int seq = tag >> 2;
+        if ((tag & 3u) != kStateRunning || seq == done_seq[s]) continue;
         const int coop = *(volatile int*)&sl->coop;
-        // CTAs that take this event: all, `part` (small d) or `xpart` (cross-GPU, one-sided or cooperative)
-        int evp = (cross && !p.two_sided) ? xpart : ((!coop && !(p.two_sided && cross)) ? part : (int)gridDim.x);
-        int base = (int)(((unsigned int)s * (unsigned int)evp) % gridDim.x);
-        if (kReserve && p.reserve && xpart < (int)gridDim.x) {
-          // cross events keep to the last xpart CTAs and large local events to the
-          // others, so a CTA busy on NVLink never holds up a local event's arrival
-          if (cross) base = (int)gridDim.x - xpart;
-          else if (evp == (int)gridDim.x) { evp = (int)gridDim.x - xpart; base = 0; }
-        }
-        if (evp < (int)gridDim.x) {
-          rb = (int)((blockIdx.x + gridDim.x - base) % gridDim.x);
-          if (rb >= evp) { done_seq[s] = tag >> 2; continue; }    // not one of this event's CTAs
-        }
-        long long t0 = 0, t1 = 0;
-        if (cross && p.two_sided && kVar != 1) {
-          if (cons_seq[s] != (tag >> 2)) { cons_seq[s] = tag >> 2; cons_cnt[s] = 0u; }
-          const unsigned int tag16 = *(volatile unsigned int*)&sl->tag16;
-          unsigned int avail = 0;
-          if (my_tiles > 0) {
-            const unsigned int v = ld_acquire_sys(*(unsigned int* volatile*)&sl->pcnt + blockIdx.x);
-            avail = (v >> 16) == tag16 ? (v & 0xffffu) : 0u;
-            if (avail <= cons_cnt[s]) continue;              // nothing landed yet: look elsewhere
-          }
-          t0 = cons_cnt[s];
-          t1 = avail;
-          s_ev.land = *(float* volatile*)&sl->land;
-        }
-        pick = s;
-        s_seq = tag >> 2;
+        const unsigned int share = coop ? (T + 1u) / 2u : T;
+        if (*(volatile unsigned int*)&sl->next >= share) { done_seq[s] = seq; continue; }
+        if (*(volatile int*)&sl->cross && atomicAdd(&sl->nwork, 1u) >= xpart) { done_seq[s] = seq; continue; }
+        if (!pin_join(&sl->pin, seq)) { done_seq[s] = seq; continue; }
+        // pinned: the fields are stable until we leave
         s_ev.xi = *(float* volatile*)&sl->xi;
         s_ev.xj = *(float* volatile*)&sl->xj;
-        s_ev.k = *(volatile long long*)&sl->k;
         const unsigned int fl = *(volatile unsigned int*)&sl->flags;
+        s_ev.kind = *(volatile int*)&sl->kind;
         s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
         s_ev.ff = (fl & 2u) ? 1 : 0;
-        s_ev.kind = *(volatile int*)&sl->kind;
         s_ev.key = *(volatile unsigned long long*)&sl->key;
         s_ev.g = *(float* volatile*)&sl->g;
         s_ev.gout = *(float* volatile*)&sl->gout;
         s_ev.absorb = *(volatile int*)&sl->absorb >= 0 ? 1 : 0;
         s_ev.pair = s_ev.xj != nullptr;
-        s_ev.cross = cross;
-        s_ev.t0 = t0;
-        s_ev.t1 = t1;
-        s_ev.coop = coop;
-        s_ev.first = rb;
-        s_ev.step = coop ? 2ll * evp : (long long)evp;
-        s_ev.ncta = coop ? 2 * evp : evp;
+        s_ev.cross = *(volatile int*)&sl->cross;
+        s_ev.ctr = &sl->next;
+        s_ev.n = share;
+        s_ev.stride = coop ? 2u : 1u;
+        s_ev.off = 0u;
+        s_ev.pin = &sl->pin;
         s_ev.guest = 0;
+        s_ev.slot = s;
+        s_ev.seq = seq;
+        pick = s;
       }
-#ifndef ADPSGD_GUEST_FIRST
-      scan_guests();
-#endif
+      // 2. cooperative events of peer GPUs posted in our workers' mailboxes
+      if (p.coop)
+        for (int t = 0; t < L && pick == -1; ++t) {
+          const int l = (t + rot) % L;
+          const int wl = p.local_ids[l];
+          WorkerCtl* mb = p.workers[wl].ctl;
+          const unsigned int gt = ld_acquire_sys(&mb->guest_tag);
+          const unsigned int gseq = gt >> 2;
+          if ((gt & 3u) != kStateRunning || gseq == gdone_seq[l]) continue;
+          const unsigned int share = T / 2u;
+          if (*(volatile unsigned int*)&mb->guest_next >= share) { gdone_seq[l] = gseq; continue; }
+          if (atomicAdd(&mb->guest_nwork, 1u) >= xpart) { gdone_seq[l] = gseq; continue; }
+          const int gi = *(volatile int*)&mb->guest_i;
+          Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
+          if (!pin_join(&sa->pin, *(volatile unsigned int*)&mb->guest_eseq)) { gdone_seq[l] = gseq; continue; }
+          const unsigned int fl = *(volatile unsigned int*)&sa->flags;
+          s_ev.xi = p.workers[gi].x;
+          s_ev.xj = p.workers[wl].x;
+          s_ev.key = *(volatile unsigned long long*)&sa->key;
+          s_ev.grad = (!(fl & 1u) && p.model != 0) ? 1 : 0;
+          s_ev.ff = (fl & 2u) ? 1 : 0;
+          s_ev.kind = kKindEvent;
+          s_ev.g = nullptr;
+          s_ev.gout = nullptr;
+          s_ev.absorb = 0;
+          s_ev.pair = 1;
+          s_ev.cross = 1;
+          s_ev.ctr = &mb->guest_next;
+          s_ev.n = share;
+          s_ev.stride = 2u;
+          s_ev.off = 1u;
+          s_ev.pin = &sa->pin;
+          s_ev.guest = 1;
+          s_ev.slot = l;
+          s_ev.seq = gseq;
+          s_ev.gready = &sa->commit_ready;
+          pick = kPickGuest;
+        }
       // 3. scheduler duty
       if (pick == -1) {
         const unsigned long long now = globaltimer();
@@ -726,71 +644,63 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           if (st == kStateFinished) ++n_fin;
           else if (st == kStateIdle) progress |= try_start(p, s, tag, now);
         }
-        // local work done; with cross-GPU partners stay to serve push requests
-        // until every event of the run is committed system-wide
-        if (n_fin == L && (!(p.two_sided || p.coop) || ld_relaxed_sys64(&p.gctl0->committed) >= p.target))
-          pick = kExit;
+        // local work done; with cooperative partners stay to serve their
+        // events until every event of the run is committed system-wide
+        if (n_fin == L && (!p.coop || ld_relaxed_sys64(&p.gctl0->committed) >= p.target)) pick = kExit;
         if (progress) last_progress = now;
         else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
-      } else {
+      } else if (pick != kExit) {
         last_progress = globaltimer();
+        cl.init(s_ev.ctr, s_ev.n, s_ev.stride, s_ev.off);
       }
       s_pick = pick;
     }
     __syncthreads();
     const int pick = s_pick;
     if (pick == kExit) break;
-    if (pick >= kPickPush) {
+    if (pick >= 0) {                 // a joined event (own slot or, kPickGuest, a peer's half)
       const SmemSlot& e = s_ev;      // stable until the trailing barrier
-      if (kVar != 1)
-        stg.push(reinterpret_cast<const float4*>(e.src), reinterpret_cast<float4*>(e.dst), e.cnt, e.tag16,
-                 blockIdx.x, gridDim.x, p.n4);
-      __syncthreads();
-      if (threadIdx.x == 0) push_seq[pick - kPickPush] = s_seq;
-    } else if (pick >= 0) {
-      const SmemSlot& e = s_ev;      // stable until the trailing barrier
-      if (e.kind == kKindPull) {
-        if (kVar != 1)
-          stg.pull(reinterpret_cast<const float4*>(e.xi), reinterpret_cast<const float4*>(e.g),
-                   reinterpret_cast<float4*>(e.gout), e.first, e.step, p.n4, p.d, p.gamma, p.q,
-                   quad_event_key_h(p.q.noise_key, e.key));
-      } else if (kVar != 1 && e.g) {        // App. A flush of the buffered gradient (staged variants)
-        if (e.pair) slice<kVar, true, kGradExternal, true>(p, e, stg);
-        else slice<kVar, false, kGradExternal>(p, e, stg);
+      unsigned int tiles = 0;
+      if (e.kind != kKindEvent) {    // App. A pull / replay stale read: gradient at x_i into gout
+        ReadBody body;
+        body.gout = reinterpret_cast<float4*>(e.gout);
+        body.hi = p.n4;
+        body.d = p.d;
+        body.gamma = p.gamma;
+        body.q = p.q;
+        body.kk = quad_event_key_h(p.q.noise_key, e.key);
+        body.comp = e.g != nullptr;
+        tiles = stg.drive(cl, reinterpret_cast<const float4*>(e.xi), reinterpret_cast<const float4*>(e.g), p.n4,
+                          body);
+      } else if (e.g) {              // a gradient row: App. A flush (FF) or a replayed stale read (Alg. 1)
+        if (e.pair) tiles = e.ff ? event_pass<true, kGradExternal, true>(p, e, stg, cl)
+                                 : event_pass<true, kGradExternal>(p, e, stg, cl);
+        else tiles = event_pass<false, kGradExternal>(p, e, stg, cl);
       } else if (e.pair) {
         if (e.grad) {
-          if (kVar != 1 && e.ff) slice<kVar, true, kGradQuadInline, true>(p, e, stg);
-          else if (kVar != 1 && e.absorb) slice<kVar, true, kGradQuadInline, false, true>(p, e, stg);
-          else slice<kVar, true, kGradQuadInline>(p, e, stg);
+          if (e.ff) tiles = event_pass<true, kGradQuadInline, true>(p, e, stg, cl);
+          else if (e.absorb) tiles = event_pass<true, kGradQuadInline, false, true>(p, e, stg, cl);
+          else tiles = event_pass<true, kGradQuadInline>(p, e, stg, cl);
         } else {
-          slice<kVar, true, kGradNone>(p, e, stg);
+          tiles = event_pass<true, kGradNone>(p, e, stg, cl);
         }
       } else if (e.grad) {
-        slice<kVar, false, kGradQuadInline>(p, e, stg);
+        tiles = event_pass<false, kGradQuadInline>(p, e, stg, cl);
+      } else {                       // a partner-less NO_GRAD event: W = I, nothing to stream
+        if (threadIdx.x == 0) while (cl.next() >= 0) ++tiles;
       }
       __syncthreads();
       if (threadIdx.x == 0) {
-        bool finished = true;
-        if (e.cross && p.two_sided && kVar != 1) {
-          cons_cnt[pick] = (unsigned int)e.t1;
-          finished = e.t1 >= my_tiles;
-        }
-        if (finished && e.guest) {          // our half of a peer's cooperative event
-          gdone_seq[e.gl] = s_seq;
-          __threadfence_system();
-          if (atomicAdd_system(e.gdone, 1u) == (unsigned int)e.ncta - 1u) st_release_sys(e.gready, s_seq);
-        } else if (finished) {
-          done_seq[pick] = s_seq;
-          // this CTA's slice is visible before its arrival; P2P stores need the
-          // system-scope fence, local ones only gpu scope (the committing CTA
-          // issues fence.sys before the cross-GPU release, which is cumulative)
-          if (e.cross) __threadfence_system();
-          else __threadfence();
-          if (e.coop) {
-            if (atomicAdd_system(&p.slots[pick].done, 1u) == (unsigned int)e.ncta - 1u) commit(p, pick);
-          } else if (atomicAdd(&p.slots[pick].done, 1u) == (unsigned int)e.ncta - 1u) {
-            commit(p, pick);
-          }
+        // this CTA's tiles are visible before its leave; peer stores need the
+        // system-scope fence, local ones gpu scope (the committing CTA issues
+        // fence.sys before the cross-GPU release, which is cumulative)
+        if (e.cross) __threadfence_system();
+        else __threadfence();
+        if (e.guest) gdone_seq[e.slot] = e.seq;
+        else done_seq[e.slot] = e.seq;
+        if (pin_leave(e.pin, tiles)) {
+          if (e.guest) st_release_sys(e.gready, e.seq);   // the initiator's scheduler commits
+          else commit(p, e.slot);
         }
       }
     } else if (threadIdx.x == 0) {
@@ -798,26 +708,14 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
     }
     __syncthreads();
   }
-  if (p.two_sided)
-    for (int l = threadIdx.x; l < p.n_local; l += blockDim.x) p.served[l * kMaxGrid + blockIdx.x] = push_seq[l];
-}
-
-const void* engine_fn(int variant, size_t* smem) {
-  switch (variant) {
-    case 1: *smem = 0; return (const void*)k_engine<1>;
-    case 2: *smem = kTmaSmem; return (const void*)k_engine<2>;
-    default: *smem = kTmaSmem; return (const void*)k_engine<0>;
-  }
 }
 
 }  // namespace
 
-int engine_max_ctas_per_sm(int threads, int variant) {
+int engine_max_ctas_per_sm(int threads) {
   int n = 0;
-  size_t smem = 0;
-  const void* fn = engine_fn(variant, &smem);
-  if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, fn, threads, smem);
+  cudaFuncSetAttribute((const void*)k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&n, (const void*)k_engine, threads, kTmaSmem);
   return n;
 }
 
@@ -825,13 +723,12 @@ cudaError_t launch_engine(const EngineParams& p, int grid, int threads, bool coo
   EngineParams pp = p;
   void* args[] = {&pp};
   if (threads != kEngineThreads || grid > kMaxGrid) return cudaErrorInvalidValue;
-  size_t smem = 0;
-  const void* fn = engine_fn(p.variant, &smem);
-  if (smem) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (cooperative) return cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), args, smem, s);
-  return cudaLaunchKernel(fn, dim3(grid), dim3(threads), args, smem, s);
+  cudaFuncSetAttribute((const void*)k_engine, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kTmaSmem);
+  if (cooperative) return cudaLaunchCooperativeKernel((const void*)k_engine, dim3(grid), dim3(threads), args,
+                                                      kTmaSmem, s);
+  return cudaLaunchKernel((const void*)k_engine, dim3(grid), dim3(threads), args, kTmaSmem, s);
 }
 
-const void* engine_module_anchor() { return (const void*)k_engine<0>; }
+const void* engine_module_anchor() { return (const void*)k_engine; }
 
 }  // namespace adp

@@ -10,9 +10,13 @@
 namespace adp {
 
 // --------------------------------------------------------------- engine ----
-struct Slot {                      // per local worker, in local device memory
+struct Slot {                      // per local worker, in the peer-mapped control arena
   unsigned int tag;                // (seq << 2) | state
-  unsigned int done;               // CTAs finished with the current event
+  unsigned int next;               // tile claim counter of this GPU's share of the running event
+  unsigned long long pin;          // (event seq << 32) | (unfinished tiles + CTAs joined): the CTA
+                                   // whose leave brings it to 0 commits the event
+  unsigned int nwork;              // CTAs of this GPU that joined (cross events are capped)
+  unsigned int ntiles;             // tiles of the event (both GPUs' shares for a coop event)
   int i, j;
   int tau;
   unsigned int flags;
@@ -28,29 +32,29 @@ struct Slot {                      // per local worker, in local device memory
   int pending_j;                   // chosen partner awaiting its lock; -2 none
   long long ev_cur, ev_end;        // replay cursor into ReplayEv list
   int cross;                       // partner lives on another rank
-  unsigned int tag16;              // push-counter tag of this event (cross, two-sided)
-  float* land;                     // local landing row the partner pushes x_j into (cross)
-  unsigned int* pcnt;              // per-CTA push counters of that landing row (cross)
-  // App. A (wait_free) and flush-first replay events
-  int kind;                        // 0 = event (ticketed), 1 = pull (computation thread, no ticket)
-  unsigned long long key;          // random-draw key of an inline / pulled gradient
-  float* g;                        // event: buffered gradient to flush; pull: g_p to compensate with
-  float* gout;                     // pull: gradient row written
+  // App. A (wait_free) and flush-first events; replay reads (stale reads)
+  int kind;                        // kKindEvent (ticketed), kKindPull (App. A computation thread),
+                                   // kKindRead (replay: gradient at X_{k - tau} into a row)
+  unsigned long long key;          // random-draw key of an inline / pulled / read gradient
+  float* g;                        // event: gradient row to apply; pull: g_p to compensate with
+  float* gout;                     // pull / read: gradient row written
   // slow-link emulation (R21): the passive's lock is released at unlock_at
   unsigned int* held_lock;
   unsigned long long unlock_at;
   int absorb;                      // slot of a passive whose local step (event k-1) is fused into this pair, -1 none
-  int coop;                        // cross event processed by both GPUs (2 x grid CTAs arrive on `done`)
-  unsigned int commit_ready;       // mailbox seq of a coop event whose last arrival was on the partner GPU
+  int coop;                        // cross event processed by both GPUs (the partner claims the odd tiles)
+  unsigned int commit_ready;       // mailbox seq of a coop event whose last leave was on the partner GPU
   unsigned int gseq;               // the partner mailbox's sequence for this coop event
 };
-constexpr int kKindEvent = 0, kKindPull = 1;
+constexpr int kKindEvent = 0, kKindPull = 1, kKindRead = 2;
 
-struct ReplayEv {                  // one schedule event owned by this rank (i local)
-  long long k;
-  int j;
+struct ReplayEv {                  // one op of a local worker's replay list, in order
+  long long k;                     // event index (kKindRead: the event whose gradient is read)
+  int j;                           // partner or -1
   unsigned int flags;
-  unsigned int e_i, e_j;           // required epochs of i and j before the event
+  unsigned int e_i, e_j;           // required epochs of i and j before the op
+  int kind;                        // kKindEvent or kKindRead
+  int grow;                        // gradient row of a stale-read event (-1: inline, tau = 0)
 };
 
 struct EngineParams {
@@ -76,19 +80,15 @@ struct EngineParams {
   long long compute_ns;
   uint2 seed;
   unsigned long long watchdog_ns;
-  int variant;                     // 0 = bulk-copy (TMA) staged slices, 1 = register slices
-  int two_sided;                   // cross-GPU events via partner push (write-only NVLink)
-  unsigned int* served;            // [n_local][kMaxGrid] last push request served per CTA (persistent)
   int wait_free;                   // free-running loop: 0 Alg. 1, 1 App. A, 2 App. A + compensation
   long long link_ns;               // nominal model-transfer time of a 1x link (R21)
   int fuse;                        // fuse a due passive local step into the pair that holds its lock
   unsigned long long fuse_wait_ns; // a due passive stays absorbable this long before stepping alone
   int coop;                        // cooperative cross-GPU events (both GPUs process the tiles)
-  int reserve;                     // world > 1: cross events on a fixed CTA range, local events on the rest
 };
 
 cudaError_t launch_engine(const EngineParams& p, int grid, int threads, bool cooperative, cudaStream_t s);
-int engine_max_ctas_per_sm(int threads, int variant);
+int engine_max_ctas_per_sm(int threads);
 
 // ---------------------------------------------------- standalone kernels ----
 // Pair/local update with external, inline-quadratic, snapshot-quadratic or no gradient.

@@ -65,12 +65,12 @@ struct PeerBlob {
   uint32_t magic, version;
   int32_t rank, n_local;
   int64_t d_pad;
-  int64_t gctl_offset, log_offset, log_cap, pcnt_offset, slots_offset;
-  int32_t has_land, engine_grid;
-  cudaIpcMemHandle_t models, ctl, land;
+  int64_t gctl_offset, log_offset, log_cap, slots_offset;
+  int32_t engine_grid, pad0;
+  cudaIpcMemHandle_t models, ctl;
   // in-process ranks (cfg.comm_local): raw device addresses, valid in this process
   int32_t local, device;
-  uint64_t pid, models_ptr, ctl_ptr, land_ptr;
+  uint64_t pid, models_ptr, ctl_ptr;
 };
 
 uint64_t splitmix64(uint64_t& s) {
@@ -93,7 +93,7 @@ struct adpsgd_ctx {
   uint64_t seed = 0;
   QuadParams q{};
   long long compute_ns = 0;
-  int engine_cps = 0, engine_threads = 512, engine_variant = 0;
+  int engine_cps = 0, engine_threads = 512;
   int wait_free = 0;                 // App. A runtime for adpsgd_run (reading R20)
   int engine_fuse = 1;               // fuse due passive steps into pair passes
   int engine_coop = 0;               // cooperative cross-GPU events: 0 auto, 1 on, -1 off
@@ -116,11 +116,9 @@ struct adpsgd_ctx {
   cudaStream_t stream = nullptr;
   float* models = nullptr;
   char* ctl_arena = nullptr;
-  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0, pcnt_offset = 0, slots_offset = 0;
-  float* land = nullptr;             // landing rows [n_local][d_pad] (world > 1)
-  unsigned int* served = nullptr;    // [n_local][kMaxGrid] push requests served per CTA
-  std::vector<float*> peer_land;
-  std::vector<size_t> peer_pcnt_off;
+  size_t ctl_bytes = 0, gctl_offset = 0, log_offset = 0, slots_offset = 0;
+  float* rrows = nullptr;            // engine replay stale reads: [n_local][T+1][d_pad] gradient rows
+  int rrows_n = 0;
   std::vector<size_t> peer_slots_off;
   int engine_grid = 0;
   WorkerCtl* ctl = nullptr;
@@ -290,9 +288,6 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
       x.x = c->peer_models[r] ? c->peer_models[r] + l * c->d_pad : nullptr;
       x.ctl = c->peer_ctl[r] ? reinterpret_cast<WorkerCtl*>(c->peer_ctl[r]) + l : nullptr;
     }
-    x.land = c->peer_land[r] ? c->peer_land[r] + l * c->d_pad : nullptr;
-    x.pcnt = c->peer_ctl[r] ? reinterpret_cast<unsigned int*>(c->peer_ctl[r] + c->peer_pcnt_off[r]) + l * kMaxGrid
-                            : nullptr;
     x.rank = r;
     x.role = c->role[w];
     x.nb_off = c->nb_off[w];
@@ -300,6 +295,7 @@ adpsgd_status upload_workers(adpsgd_ctx* c) {
     x.straggle = c->straggle[w];
     x.local = r == c->rank ? c->worker_local[w] : -1;
     x.gb = (r == c->rank && c->wf_g) ? c->wf_g + l * 2 * c->d_pad : nullptr;
+    x.gr = (r == c->rank && c->rrows) ? c->rrows + l * (long long)c->rrows_n * c->d_pad : nullptr;
     x.link = c->link[w];
     x.slot = c->peer_ctl[r] ? reinterpret_cast<Slot*>(c->peer_ctl[r] + c->peer_slots_off[r]) + l : nullptr;
   }
@@ -638,22 +634,12 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   p.compute_ns = c->compute_ns;
   p.seed = make_uint2((uint32_t)(c->seed ^ 0x5bd1e995u), (uint32_t)(c->seed >> 32) ^ c->run_counter);
   p.watchdog_ns = 60ull * 1000000000ull;
-  p.variant = c->engine_variant;
-  // variant 3 = variant 0 with the two-sided push protocol for cross-GPU pairs.
-  // tools/ab_nvlink.py (2 B200, every event cross-GPU): one-sided 604/616 GB/s
-  // per GPU per direction vs two-sided 587/579 (pure gossip / quadratic), so
-  // one-sided peer access is the default.
-  p.two_sided = (c->world > 1 && p.variant == 3 && c->land) ? 1 : 0;
-  if (p.variant == 3) p.variant = 0;
-  p.served = c->served;
   p.wait_free = mode == 0 ? c->wait_free : 0;
   p.link_ns = c->link_ns;
   p.fuse = c->engine_fuse;
   p.fuse_wait_ns = (unsigned long long)c->fuse_wait_ns;
-  // cooperative cross-GPU events: the partner GPU's CTAs take half of the tiles
-  // (same grid on every rank, checked at import); not with the register-slice
-  // variant, the two-sided protocol, or the wait-free loop (its gradient rows
-  // are not peer-mapped)
+  // cooperative cross-GPU events: the partner GPU's CTAs claim half of the tiles;
+  // not in the wait-free loop (its gradient rows are not peer-mapped)
   bool coop = c->engine_coop > 0;
   if (c->engine_coop == 0 && c->world > 1) {
     // auto: on at two GPUs (measured: N=2 all-cross 455 -> 624 GB/s free-running,
@@ -676,10 +662,9 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
     const bool few_cross = 2 * (size_t)cross <= c->edges.size() / 2;
     coop = c->world == 2 || few_cross || (mode == 0 && mx > 2 * mn);
   }
-  p.coop = (c->world > 1 && coop && p.variant != 1 && !p.two_sided && !(mode == 0 && c->wait_free)) ? 1 : 0;
-  p.reserve = (c->world > 1 && p.variant != 1 && !p.two_sided) ? 1 : 0;
+  p.coop = (c->world > 1 && coop && !(mode == 0 && c->wait_free)) ? 1 : 0;
   // the grid is fixed at init (and checked equal across ranks at import: the
-  // cooperative and two-sided protocols pair CTA b of both GPUs tile by tile)
+  // per-GPU cap on a cross event's CTAs is grid / 4 on both sides)
   if (c->engine_grid < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
   // processes: a cooperative launch guarantees co-residency of the grid; in-process
@@ -726,22 +711,51 @@ adpsgd_status compute_placement(int n, int world, int placement, const int32_t* 
   return ADPSGD_OK;
 }
 
-// Engine-replay plan: event k waits until epoch[i] == e_i(k) and epoch[j] ==
-// e_j(k), the numbers of earlier schedule events touching i and j (so every
-// worker sees the schedule's order).  Every rank runs this on the same schedule
-// and the same epoch mirror, and keeps the events whose updating worker is local.
+// Engine-replay plan.  Every worker w has a sequence of ops: the schedule's
+// events touching w (as i or j) and the stale reads of w's own gradient events
+// (tau > 0: the gradient at X_{k - tau}, is computed by a read op placed
+// in w's sequence right before the first event >= k - tau that touches w, into
+// one of w's T + 1 read rows -- w's m-th stale event uses row m mod (T + 1),
+// which no later read can overwrite before the event ran, since that read's
+// point is after it).  An op waits until epoch[i] (and epoch[j] for a pair)
+// equals the number of earlier ops in that worker's sequence, and bumps them
+// when it commits, so every worker sees the schedule's order.  Every rank runs
+// this on the same schedule and epoch mirror and keeps the ops whose worker i
+// is local.  A read op's k holds its gradient's random-draw key.
 void plan_replay(const std::vector<int>& wr, const std::vector<int>& wl, int rank, int n_local,
-                 const adpsgd_event* ev, int64_t K, unsigned long long k0, std::vector<unsigned int>& ep,
-                 std::vector<std::vector<ReplayEv>>& per) {
+                 const adpsgd_event* ev, int64_t K, unsigned long long k0, int T, bool stale_reads,
+                 std::vector<unsigned int>& ep, std::vector<std::vector<ReplayEv>>& per) {
   per.assign(n_local, {});
+  const int n = (int)ep.size();
+  std::vector<std::vector<int64_t>> reads_at(stale_reads ? K : 0);   // stale events read before event e
+  if (stale_reads)
+    for (int64_t e = 0; e < K; ++e)
+      if (ev[e].tau > 0 && !(ev[e].flags & ADPSGD_EV_NO_GRAD)) reads_at[e - ev[e].tau].push_back(e);
+  std::vector<int> row(n, 0);
+  std::vector<int> row_of(stale_reads ? K : 0, -1);
   for (int64_t e = 0; e < K; ++e) {
+    if (stale_reads)
+      for (int64_t f : reads_at[e]) {
+        const int i = ev[f].i;
+        row_of[f] = row[i]++ % (T + 1);
+        ReplayEv r{};
+        r.kind = kKindRead;
+        r.k = (long long)((ev[f].flags & ADPSGD_EV_FLUSH_FIRST) ? read_key(k0 + e, i) : k0 + f);
+        r.j = -1;
+        r.flags = ev[f].flags;
+        r.e_i = ep[i]++;
+        r.grow = row_of[f];
+        if (wr[i] == rank) per[wl[i]].push_back(r);
+      }
     const int i = ev[e].i, j = ev[e].j;
     ReplayEv r{};
+    r.kind = kKindEvent;
     r.k = (long long)(k0 + e);
     r.j = j;
     r.flags = ev[e].flags;
     r.e_i = ep[i];
     r.e_j = j >= 0 ? ep[j] : 0;
+    r.grow = stale_reads ? row_of[e] : -1;
     ep[i]++;
     if (j >= 0) ep[j]++;
     if (wr[i] == rank) per[wl[i]].push_back(r);
@@ -753,10 +767,23 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   if (c->model != ADPSGD_MODEL_NONE && c->model != ADPSGD_MODEL_QUADRATIC)
     return fail(ADPSGD_E_UNSUPPORTED, "engine replay supports models NONE and QUADRATIC");
   ST(validate_events(c, ev, K, false));
+  bool stale = false;
   for (int64_t e = 0; e < K; ++e) {
-    if (ev[e].tau != 0) return fail(ADPSGD_E_UNSUPPORTED, "engine replay needs tau = 0 (use HOST)");
-    if ((ev[e].flags & ADPSGD_EV_FLUSH_FIRST) && c->engine_variant == 1)
-      return fail(ADPSGD_E_UNSUPPORTED, "FLUSH_FIRST events need a staged engine variant (0, 2, 3)");
+    // with tau = 0 the previous gradient is always applied before the read: COMPENSATE is a no-op
+    if ((ev[e].flags & ADPSGD_EV_COMPENSATE) && ev[e].tau > 0)
+      return fail(ADPSGD_E_UNSUPPORTED, "engine replay does not run stale COMPENSATE events (use HOST)");
+    stale |= ev[e].tau > 0 && !(ev[e].flags & ADPSGD_EV_NO_GRAD) && c->model == ADPSGD_MODEL_QUADRATIC;
+  }
+  // read rows for stale reads (T + 1 per local worker), allocated before any
+  // engine of this call runs (the peers' engines never touch them)
+  if (stale && c->rrows_n < c->T + 1 && c->n_local) {
+    CU(cudaDeviceSynchronize());
+    if (c->rrows) cudaFree(c->rrows);
+    c->rrows = nullptr;
+    CU(cudaMalloc(&c->rrows, sizeof(float) * c->d_pad * (size_t)(c->T + 1) * c->n_local));
+    CU(cudaMemset(c->rrows, 0, sizeof(float) * c->d_pad * (size_t)(c->T + 1) * c->n_local));
+    c->rrows_n = c->T + 1;
+    ST(upload_workers(c));
   }
   // k and the epochs are tracked identically on every rank (they only change
   // through collective calls whose effect is known: a replay advances k by K
@@ -765,7 +792,7 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
   ST(settle_ticket(c));
   const unsigned long long k0 = c->host_k;
   std::vector<std::vector<ReplayEv>> per;
-  plan_replay(c->worker_rank, c->worker_local, c->rank, c->n_local, ev, K, k0, c->epochs, per);
+  plan_replay(c->worker_rank, c->worker_local, c->rank, c->n_local, ev, K, k0, c->T, stale, c->epochs, per);
   c->h_rev.clear();
   ST(reset_slots(c, s));
   for (int l = 0; l < c->n_local; ++l) {
@@ -797,14 +824,13 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
     if ((int)r == c->rank) continue;
     if (c->peer_models[r]) cudaIpcCloseMemHandle(c->peer_models[r]);
     if (c->peer_ctl[r]) cudaIpcCloseMemHandle(c->peer_ctl[r]);
-    if (r < c->peer_land.size() && c->peer_land[r]) cudaIpcCloseMemHandle(c->peer_land[r]);
   }
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
   for (auto e : c->evring) if (e) cudaEventDestroy(e);
   for (auto st : c->pool) if (st) cudaStreamDestroy(st);
   void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids,
                   c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
-                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->land, c->served,
+                  c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->rrows,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
                   c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar, c->agree64};
   for (void* b : bufs) if (b) cudaFree(b);
@@ -882,8 +908,10 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   c->compute_ns = cfg->compute_ns;
   c->engine_cps = cfg->engine_ctas_per_sm;
   c->engine_threads = 512;
-  c->engine_variant = cfg->engine_variant;
-  if (c->engine_variant < 0 || c->engine_variant > 3) return fail(ADPSGD_E_INVALID, "engine_variant");
+  // engine_variant: the round-1 A/B variants (register slices, per-warp barriers,
+  // two-sided push protocol) were measured slower and removed; 0 is the engine
+  if (cfg->engine_variant != 0) return fail(ADPSGD_E_UNSUPPORTED, "engine_variant must be 0 (the A/B variants "
+                                                                  "1-3 were removed)");
   if (cfg->log_capacity > 0) c->log_cap = cfg->log_capacity;
   if (c->model < ADPSGD_MODEL_NONE || c->model > ADPSGD_MODEL_MLP) return fail(ADPSGD_E_INVALID, "model");
   c->wait_free = cfg->wait_free;
@@ -898,8 +926,6 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   if (c->wait_free < 0 || c->wait_free > 2) return fail(ADPSGD_E_INVALID, "wait_free must be 0, 1 or 2");
   if (c->wait_free && c->model != ADPSGD_MODEL_QUADRATIC)
     return fail(ADPSGD_E_UNSUPPORTED, "the wait-free (App. A) engine loop supports the QUADRATIC model");
-  if (c->wait_free && (c->engine_variant == 1 || c->engine_variant == 3))
-    return fail(ADPSGD_E_UNSUPPORTED, "the wait-free engine loop needs engine_variant 0 or 2");
   ST(check_graph(c.get(), g));
   // placement
   ST(compute_placement(c->n, c->world, cfg->placement, cfg->worker_rank, c->worker_rank, c->worker_local));
@@ -962,8 +988,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   // control arena (peer-mapped): WorkerCtl[n_local] | GlobalCtl | push counters [n_local][kMaxGrid] |
   // engine Slots[n_local] | (rank 0) log
   c->gctl_offset = sizeof(WorkerCtl) * std::max(1, c->n_local);
-  c->pcnt_offset = c->gctl_offset + sizeof(GlobalCtl);
-  c->slots_offset = c->pcnt_offset + sizeof(unsigned int) * kMaxGrid * std::max(1, c->n_local);
+  c->slots_offset = (c->gctl_offset + sizeof(GlobalCtl) + 127) / 128 * 128;
   c->log_offset = (c->slots_offset + sizeof(Slot) * std::max(1, c->n_local) + 255) / 256 * 256;
   c->ctl_bytes = c->log_offset + (c->rank == 0 ? sizeof(LogEntry) * c->log_cap : 0);
   CU(cudaMalloc(&c->ctl_arena, c->ctl_bytes));
@@ -1004,19 +1029,12 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   CU(cudaMalloc(&c->mk_acc, sizeof(double)));
   c->peer_models.assign(c->world, nullptr);
   c->peer_ctl.assign(c->world, nullptr);
-  c->peer_land.assign(c->world, nullptr);
-  c->peer_pcnt_off.assign(c->world, 0);
   c->peer_slots_off.assign(c->world, 0);
   c->peer_imported.assign(c->world, false);
-  if (c->world > 1 && c->n_local) {          // two-sided NVLink protocol state
-    CU(cudaMalloc(&c->land, sizeof(float) * c->d_pad * c->n_local));
-    CU(cudaMalloc(&c->served, sizeof(unsigned int) * kMaxGrid * c->n_local));
-    CU(cudaMemset(c->served, 0, sizeof(unsigned int) * kMaxGrid * c->n_local));
-  }
   {
     int sms = 0;
     CU(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, c->device));
-    const int occ = engine_max_ctas_per_sm(c->engine_threads, c->engine_variant);
+    const int occ = engine_max_ctas_per_sm(c->engine_threads);
     const int cps = c->engine_cps > 0 ? std::min(c->engine_cps, occ) : std::min(2, occ);
     const int full = cps * sms;
     // in-process ranks may share one device: by default each takes 1/world of it
@@ -1027,8 +1045,6 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   }
   c->peer_models[c->rank] = c->models;
   c->peer_ctl[c->rank] = c->ctl_arena;
-  c->peer_land[c->rank] = c->land;
-  c->peer_pcnt_off[c->rank] = c->pcnt_offset;
   c->peer_slots_off[c->rank] = c->slots_offset;
   c->peer_imported[c->rank] = true;
   c->last_evt.assign(c->n, nullptr);
@@ -1091,19 +1107,15 @@ adpsgd_status adpsgd_export_peer_info(adpsgd_ctx* c, void* buf, int64_t cap, int
     b.gctl_offset = (int64_t)c->gctl_offset;
     b.log_offset = (int64_t)c->log_offset;
     b.log_cap = c->log_cap;
-    b.pcnt_offset = (int64_t)c->pcnt_offset;
     b.slots_offset = (int64_t)c->slots_offset;
     b.engine_grid = c->engine_grid;
     CU(cudaIpcGetMemHandle(&b.models, c->models));
     CU(cudaIpcGetMemHandle(&b.ctl, c->ctl_arena));
-    b.has_land = c->land ? 1 : 0;
-    if (c->land) CU(cudaIpcGetMemHandle(&b.land, c->land));
     b.local = c->comm_local ? 1 : 0;
     b.device = c->device;
     b.pid = (uint64_t)getpid();
     b.models_ptr = (uint64_t)(uintptr_t)c->models;
     b.ctl_ptr = (uint64_t)(uintptr_t)c->ctl_arena;
-    b.land_ptr = (uint64_t)(uintptr_t)c->land;
     memcpy(buf, &b, sizeof b);
     if (n_out) *n_out = (int64_t)sizeof b;
     return ADPSGD_OK;
@@ -1135,8 +1147,6 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
       }
       c->peer_models[rank] = reinterpret_cast<float*>((uintptr_t)b.models_ptr);
       c->peer_ctl[rank] = reinterpret_cast<char*>((uintptr_t)b.ctl_ptr);
-      c->peer_land[rank] = b.has_land ? reinterpret_cast<float*>((uintptr_t)b.land_ptr) : nullptr;
-      c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
       c->peer_slots_off[rank] = (size_t)b.slots_offset;
       c->peer_imported[rank] = true;
       if (rank == 0) {
@@ -1157,15 +1167,7 @@ adpsgd_status adpsgd_import_peer_info(adpsgd_ctx* c, int32_t rank, const void* b
       return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer control: ") + cudaGetErrorString(e));
     c->peer_models[rank] = static_cast<float*>(pm);
     c->peer_ctl[rank] = static_cast<char*>(pc);
-    c->peer_pcnt_off[rank] = (size_t)b.pcnt_offset;
     c->peer_slots_off[rank] = (size_t)b.slots_offset;
-    if (b.has_land) {
-      void* pl = nullptr;
-      e = cudaIpcOpenMemHandle(&pl, b.land, cudaIpcMemLazyEnablePeerAccess);
-      if (e != cudaSuccess)
-        return fail(ADPSGD_E_UNSUPPORTED, std::string("cannot map peer landing rows: ") + cudaGetErrorString(e));
-      c->peer_land[rank] = static_cast<float*>(pl);
-    }
     c->peer_imported[rank] = true;
     if (rank == 0) {
       c->gctl0 = reinterpret_cast<GlobalCtl*>(c->peer_ctl[0] + b.gctl_offset);
@@ -1877,10 +1879,10 @@ adpsgd_status adpsgd_plan_placement(int32_t n, int32_t world_size, int32_t place
 }
 
 adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t rank, const adpsgd_event* schedule,
-                                 int64_t K, int64_t k0, uint32_t* epochs, int64_t* out, int64_t cap,
-                                 int64_t* n_out) {
+                                 int64_t K, int64_t k0, int32_t T, int32_t stale_reads, uint32_t* epochs,
+                                 int64_t* out, int64_t cap, int64_t* n_out) {
   GUARD({
-    if (n < 1 || !worker_rank || !epochs || K < 0 || (K > 0 && !schedule) || k0 < 0 || !n_out)
+    if (n < 1 || !worker_rank || !epochs || K < 0 || (K > 0 && !schedule) || k0 < 0 || !n_out || T < 0)
       return fail(ADPSGD_E_INVALID, "plan_replay args");
     std::vector<int> wr(worker_rank, worker_rank + n), wl(n, 0);
     int world = 0;
@@ -1890,13 +1892,16 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
       if (wr[w] < 0) return fail(ADPSGD_E_INVALID, "worker_rank");
       wl[w] = cnt[wr[w]]++;
     }
-    for (int64_t e = 0; e < K; ++e)
+    for (int64_t e = 0; e < K; ++e) {
       if (schedule[e].i < 0 || schedule[e].i >= n || schedule[e].j < -1 || schedule[e].j >= n)
         return fail(ADPSGD_E_INVALID, "event index");
+      if (schedule[e].tau < 0 || schedule[e].tau > T || schedule[e].tau > e)
+        return fail(ADPSGD_E_STALENESS, "tau exceeds min(k, T)");
+    }
     const int n_local = rank >= 0 && rank < (int)cnt.size() ? cnt[rank] : 0;
     std::vector<unsigned int> ep(epochs, epochs + n);
     std::vector<std::vector<ReplayEv>> per;
-    plan_replay(wr, wl, rank, n_local, schedule, K, (unsigned long long)k0, ep, per);
+    plan_replay(wr, wl, rank, n_local, schedule, K, (unsigned long long)k0, T, stale_reads != 0, ep, per);
     int64_t m = 0;
     for (auto& lst : per) m += (int64_t)lst.size();
     if (out && cap < m) return fail(ADPSGD_E_INVALID, "output capacity");
@@ -1906,8 +1911,9 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
         int w = 0;
         while (!(wr[w] == rank && wl[w] == l)) ++w;
         for (const ReplayEv& r : per[l]) {
-          int64_t* o = out + 6 * t++;
+          int64_t* o = out + 8 * t++;
           o[0] = r.k; o[1] = w; o[2] = r.j; o[3] = r.flags; o[4] = r.e_i; o[5] = r.e_j;
+          o[6] = r.kind; o[7] = r.grow;
         }
       }
     for (int w = 0; w < n; ++w) epochs[w] = ep[w];

@@ -108,15 +108,15 @@ def body(rank, world, local, G, full_size=True):
         prob_q = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
 
     # 1. pure gossip replay over NVLink (interleave: every edge crosses GPUs),
-    #    two-sided push protocol (variant 3) and the one-sided default (variant 0)
+    #    one-sided (cooperative events off) and with the auto policy
     d = 1 << 20
     X0 = synth.x0_uniform(n, d, seed=21)
     ev, _ = synth.schedule_iid(n, e, K=1500, seed=4, no_grad=True)
     if rank == 0:
         Xo, _ = O.replay(O.OracleProblem(), X0, e, r, ev)
-    for variant in (3, 0):
+    for variant in (-1, 0):          # cooperative events off (one-sided) / auto
         ctx = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=1,
-                        x0_per_worker=X0, engine_variant=variant)
+                        x0_per_worker=X0, engine_coop=False if variant == -1 else None)
         ctx.replay(ev, flags=P.REPLAY_ENGINE)
         ctx.sync()
         G.barrier()
@@ -132,7 +132,7 @@ def body(rank, world, local, G, full_size=True):
                 fails.append(f"pure-gossip engine replay over NVLink not bit-exact (variant {variant})")
             if sum(cross) != 1500:
                 fails.append(f"expected every event to cross GPUs, got {sum(cross)}")
-        if variant == 3:
+        if variant == -1:
             ctx.destroy()
             G.barrier()
     progress(rank, "1 pure-gossip replay done")
@@ -178,6 +178,25 @@ def body(rank, world, local, G, full_size=True):
             bad = np.where((X2 != Xo2).any(1))[0]
             fails.append(f"free-running multi-GPU log replay not bit-exact (workers {bad.tolist()})")
     progress(rank, "2/3 quadratic replay + free-running done")
+    # 2b. engine replay with stale reads tau ~ U{0..3} across ranks: each
+    #     stale gradient is a read op at X_{k - tau} of the worker's sequence
+    T = 3
+    ev_s, _ = synth.schedule_iid(n, e, K=300, T=T, seed=12, local_prob=0.25)
+    X0s = synth.x0_uniform(n, d, seed=29)
+    cs = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, **kw, placement=0, T=T,
+                   model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32, quad_keys=(dk, nk), quad_noise_s=s,
+                   x0_per_worker=X0s, seed=9)
+    cs.replay(ev_s, flags=P.REPLAY_ENGINE)
+    cs.sync()
+    G.barrier()
+    Xs_ = gather_models(cs, G)
+    if rank == 0:
+        Xso, _ = O.replay(prob_q, X0s, e, r, ev_s, T=T)
+        if not np.array_equal(Xs_.view(np.uint32), Xso.view(np.uint32)):
+            fails.append("multi-rank engine replay with stale reads not bit-exact")
+    cs.destroy()
+    G.barrier()
+    progress(rank, "2b stale-read engine replay done")
     # 6. D-PSGD baseline: halo exchange of neighbour rows by NCCL send/recv
     X0d = synth.x0_uniform(n, d, seed=23)
     ctx.dpsgd_reset(X0d)

@@ -115,6 +115,32 @@ def test_quadratic_replay_bit_exact_with_staleness(P, d, n, K, T):
     ctx.destroy()
 
 
+@pytest.mark.parametrize("d,n,K,T,ff", [(100003, 8, 400, 3, False), (1 << 20, 16, 600, 4, False),
+                                        (4099, 4, 300, 2, True)])
+def test_engine_replay_with_stale_reads_bit_exact(P, d, n, K, T, ff):
+    """The persistent engine replays tau ~ U{0..T} (X_hat = X_{k - tau}):
+    each stale gradient is a read op of the worker's op sequence at X_{k - tau}
+    (adpsgd_plan_replay) -- bit-exact vs the oracle's Alg. 1 (and App. A
+    flush-first events when ff, reading R20)."""
+    e, r = synth.ring(n)
+    dk, nk = synth.quad_keys(6)
+    s = float(np.float32(0.1 * math.sqrt(3 * 32)))
+    ev, _ = synth.schedule_iid(n, e, K=K, T=T, seed=19, local_prob=0.2)
+    ev[::9, 3] = 1                                        # some pure averages in between
+    if ff:
+        ev[(ev[:, 3] & 1) == 0, 3] |= P.EV_FLUSH_FIRST
+    X0 = synth.x0_uniform(n, d, seed=5)
+    ctx = P.Context(e, n, d, role=r, T=T, model=P.MODEL_QUADRATIC, gamma=0.01, batch_M=32,
+                    quad_keys=(dk, nk), quad_noise_s=s, x0_per_worker=X0)
+    ctx.replay(ev, flags=P.REPLAY_ENGINE)
+    ctx.sync()
+    prob = O.OracleProblem(O.MODEL_QUADRATIC, M=32, gamma=0.01, data_key=dk, noise_key=nk, noise_s=s)
+    Xo, _ = O.replay(prob, X0, e, r, ev, T=T)
+    assert np.array_equal(read_all(ctx).view(np.uint32), Xo.view(np.uint32))
+    assert ctx.ticket() == K
+    ctx.destroy()
+
+
 def test_quadratic_engine_replay_full_size(P):
     """BASELINE size d = 25.6M, n = 8, tau = 0, through the persistent engine
     (the launch configuration bench.py times): bit-exact vs the oracle."""

@@ -82,7 +82,8 @@ def test_replay_plans_partition_schedule_and_epochs_are_exact(results):
             assert all(wr[x[1]] == r for x in allp[r][1])            # owned by the updating worker's rank
             assert allp[r][2] == allp[0][2]                            # identical epoch mirrors
         # brute force: e_i, e_j = number of earlier events touching i, j
-        for (k, i, j, fl, ei, ej) in rows:
+        for (k, i, j, fl, ei, ej, kind, grow) in rows:
+            assert kind == 0 and grow == -1
             prev = ev[:k - 1000]
             assert ei == int(((prev[:, 0] == i) | (prev[:, 1] == i)).sum())
             if j >= 0:
@@ -99,3 +100,52 @@ def test_peer_blob_exchange(results):
         blobs, nid = results[r]["blobs"]
         assert blobs == [bytes([q]) * 64 for q in range(WORLD)]
         assert nid == b"ID" * 64
+
+
+def test_replay_plan_stale_reads_are_placed_at_their_read_points():
+    """Engine replay with tau > 0 (X_hat_k = X_{k - tau}): each stale
+    gradient event f of worker i gets a read op in i's op sequence after every
+    event < f - tau touching i and before every event >= f - tau touching i, in
+    read row m mod (T + 1) for i's m-th such event; e_i / e_j of every op equal
+    its position in the worker's sequence (brute force over the schedule)."""
+    import paper_1710_06952_b200 as P
+    n, T, K = 8, 3, 400
+    e, _ = synth.ring(n)
+    ev, _ = synth.schedule_iid(n, e, K=K, T=T, seed=17, local_prob=0.25)
+    ev[::7, 3] = 1                                   # some pure averages (no read)
+    wr = np.array([w % 2 for w in range(n)], np.int32)
+    rows = np.concatenate([P.plan_replay(wr, r, ev, k0=50, T=T, stale_reads=True)[0] for r in range(2)])
+    events = rows[rows[:, 6] == 0]
+    reads = rows[rows[:, 6] == 2]
+    assert sorted(events[:, 0].tolist()) == list(range(50, 50 + K))
+    stale = [f for f in range(K) if ev[f, 2] > 0 and not (ev[f, 3] & 1)]
+    assert len(reads) == len(stale)
+    # reconstruct every worker's op sequence in global order and check positions
+    seq = {w: [] for w in range(n)}
+    for f in range(K):
+        for g in [g for g in stale if g - ev[g, 2] == f]:
+            seq[ev[g, 0]].append(("r", g))
+        seq[ev[f, 0]].append(("e", f))
+        if ev[f, 1] >= 0:
+            seq[ev[f, 1]].append(("e", f))
+    pos = {w: {op: p for p, op in enumerate(s)} for w, s in seq.items()}
+    m = np.zeros(n, np.int64)
+    row_of = {}
+    for f in range(K):                               # rows in order of the reads (= m-th stale event)
+        for g in [g for g in stale if g - ev[g, 2] == f]:
+            i = ev[g, 0]
+            row_of[g] = m[i] % (T + 1)
+            m[i] += 1
+    for (k, i, j, fl, ei, ej, kind, grow) in events:
+        f = k - 50
+        assert ei == pos[i][("e", f)]
+        if j >= 0:
+            assert ej == pos[j][("e", f)]
+        assert grow == (row_of[f] if f in row_of else -1)
+    by_row = {}
+    for (k, i, j, fl, ei, ej, kind, grow) in reads:
+        assert j == -1
+        cand = [g for g in stale if ev[g, 0] == i and pos[i][("r", g)] == ei]
+        assert len(cand) == 1
+        g = cand[0]
+        assert grow == row_of[g] and k == 50 + g   # Alg. 1 events: the key is the event's k
