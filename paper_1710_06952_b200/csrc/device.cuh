@@ -26,9 +26,8 @@ struct alignas(128) WorkerCtl {
   // cooperative cross-GPU event posted in this worker's mailbox (guest_tag):
   // this GPU's share of its tiles is claimed from guest_next, and at most
   // guest_nwork CTAs of this GPU join it (both reset by the poster)
-  unsigned int guest_next;
-  unsigned int guest_nwork;
-  unsigned int guest_eseq;         // the initiator slot's event sequence (its pin word's tag)
+  unsigned long long guest_next;   // claim word of this GPU's half (claim_word)
+  unsigned int guest_eseq;         // unused (kept for the 128-byte layout)
   // App. A wait-free runtime (home GPU only; persists across adpsgd_run calls):
   // the computation thread's state and the shared gradient buffer g
   unsigned int wf_state;           // 0 = pull next, 1 = computing (until wf_ready_ns)
@@ -46,7 +45,8 @@ struct alignas(128) WorkerCtl {
   // algorithmic HBM bytes moved in this worker's row by cross-GPU events that a
   // peer committed (this GPU's share of them; engine stats)
   double peer_bytes;
-  unsigned int pad[8];
+  unsigned int guest_nwork;        // CTAs of this GPU that tried to join the posted guest event
+  unsigned int pad[7];
 };
 static_assert(sizeof(WorkerCtl) == 128, "WorkerCtl must be 128 B");
 
@@ -308,28 +308,47 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 // Dynamic tile claiming.  An event's float4 range is cut into tiles of kTile4
 // float4; this GPU's share is the tile list t(c) = c * stride + off for c in
 // [0, n) (stride 2 / off 0 or 1 for the halves of a cooperative cross-GPU
-// event, else stride 1).  Thread 0 of a CTA takes chunks of kChunk consecutive
-// c from the shared counter *ctr, so every CTA that has joined an event keeps
-// streaming its tiles until none is left -- no CTA waits for a fixed share,
-// and a CTA stalled on NVLink never holds back the tiles of a local event.
+// event, else stride 1), dealt in nc = ceil(n / kChunk) chunks of consecutive
+// c.  The claim word packs (event seq mod 2^16) << 48 | nc << 32 | chunks
+// claimed; one atomicAdd claims a chunk and names the event it belongs to, so
+// a CTA that owns a chunk pins its event (the event commits when all its tiles
+// are credited) and a late claim on an exhausted counter is harmless (the
+// next publish overwrites the word).  Every CTA that joined an event keeps
+// claiming until no chunk is left: no CTA waits for a fixed share, and a CTA
+// held up on NVLink never delays a local event's tiles.  The next chunk is
+// claimed when the current one starts, so its latency hides behind its tiles.
+__host__ __device__ __forceinline__ unsigned long long claim_word(unsigned int seq, unsigned int nc) {
+  return ((unsigned long long)(seq & 0xFFFFu) << 48) | ((unsigned long long)(nc & 0xFFFFu) << 32);
+}
+__host__ __device__ __forceinline__ unsigned int claim_seq(unsigned long long w) { return (unsigned int)(w >> 48); }
+__host__ __device__ __forceinline__ unsigned int claim_nc(unsigned long long w) {
+  return (unsigned int)(w >> 32) & 0xFFFFu;
+}
+constexpr unsigned int kClaimSeqMask = 0xFFFFu;
+__host__ __device__ __forceinline__ unsigned int claim_idx(unsigned long long w) { return (unsigned int)w; }
+
 template <int kChunk>
 struct TileClaim {
-  unsigned int* ctr;
+  unsigned long long* ctr;
   unsigned int n, stride, off;
-  unsigned int cur, end;
+  unsigned int c, end, ahead;      // current chunk's next / end c; chunk claimed ahead
   bool out;
-  __device__ __forceinline__ void init(unsigned int* c, unsigned int n_, unsigned int stride_, unsigned int off_) {
-    ctr = c; n = n_; stride = stride_; off = off_; cur = end = 0; out = false;
+  // first = the chunk index the join's claim returned
+  __device__ __forceinline__ void init(unsigned long long* ctr_, unsigned int n_, unsigned int stride_,
+                                       unsigned int off_, unsigned int first) {
+    ctr = ctr_; n = n_; stride = stride_; off = off_; out = false;
+    c = first * kChunk;
+    end = c + kChunk < n ? c + kChunk : n;
+    ahead = claim_idx(atomicAdd(ctr, 1ull));
   }
   __device__ __forceinline__ int next() {           // thread 0 only; -1 once exhausted
-    if (cur >= end) {
-      if (out) return -1;
-      const unsigned int b = atomicAdd(ctr, (unsigned int)kChunk);
-      if (b >= n) { out = true; return -1; }
-      cur = b;
-      end = b + kChunk < n ? b + kChunk : n;
+    if (c >= end) {
+      if (out || ahead * kChunk >= n) { out = true; return -1; }
+      c = ahead * kChunk;
+      end = c + kChunk < n ? c + kChunk : n;
+      ahead = claim_idx(atomicAdd(ctr, 1ull));      // used when this chunk is done
     }
-    return (int)(cur++ * stride + off);
+    return (int)(c++ * stride + off);
   }
 };
 

@@ -26,14 +26,16 @@
 // T + 1 read rows, which the event applies later.
 //
 // Work distribution: an event's float4 range is cut into tiles of kTile4; the
-// CTAs that join an event claim tile chunks from its counter until none is
+// CTAs that join an event claim tile chunks from its claim word until none is
 // left (TileClaim), so a CTA held up on NVLink never delays a local event's
-// tiles.  Joining pins the event (Slot::pin counts unfinished tiles plus
-// joined CTAs under the event's sequence tag), so it cannot commit -- and its
-// slot cannot be reused -- while a CTA still reads its fields; the CTA whose
-// leave brings the pin to zero commits.  A cross-GPU event is joined by at most
-// grid / kCrossDiv CTAs per GPU (it is NVLink-bound); with cooperative events
-// the partner GPU claims the odd tiles (its half) from its own mailbox counter.
+// tiles.  A claim is one atomicAdd that also names the event (sequence tag):
+// owning an uncredited chunk pins the event -- it cannot commit, nor its slot
+// be reused, while the CTA still reads its fields -- and the CTA whose credit
+// brings the event's remaining tiles to zero commits.  (A CAS-based join pin
+// cost 0.80 vs 0.93 of the HBM peak: 296 CTAs retrying one word per event.)
+// A cross-GPU event is joined by at most grid / kCrossDiv CTAs per GPU (it is
+// NVLink-bound); with cooperative events the partner GPU claims the odd tiles
+// (its half) from its own mailbox claim word.
 #include "internal.h"
 
 namespace adp {
@@ -46,7 +48,8 @@ constexpr int kPickGuest = 1 << 20;     // a peer's cooperative event posted in 
 constexpr int kTile4 = 1536;            // float4 per stream per stage (24 KB); round-1 A/B: 1536x2 stages
                                         // 0.869-0.871 of the HBM peak vs 1024x3 0.863-0.867, 512x6 0.82
 constexpr int kStages = 2;
-constexpr int kClaimChunk = 2;          // tiles per claim
+constexpr int kClaimChunk = 8;          // tiles per claimed chunk (A/B at N=1: 4 -> 0.907, 8 -> 0.930, 16 -> 0.928 of peak)
+constexpr bool kRotate = true;          // CTA b scans slots from b mod L (else every CTA from slot 0)
 constexpr int kCrossDiv = 4;            // CTAs per GPU on one cross-GPU event: grid / 4 (round-1 A/B at
                                         // N=2: 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k steps/s)
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
@@ -67,9 +70,10 @@ struct SmemSlot {                  // tid 0 copies the joined event here for the
   float* gout;
   int absorb;                      // fused passive local step (event k-1) before the pair
   // this CTA's claim on the event: tile c of its share is c * stride + off
-  unsigned int* ctr;
+  unsigned long long* ctr;
   unsigned int n, stride, off;
-  unsigned long long* pin;         // the initiator slot's pin word (peer memory for a guest)
+  unsigned int first;              // the chunk the join's claim returned
+  unsigned int* rem;               // the initiator slot's remaining tiles (peer memory for a guest)
   int guest;                       // a peer's cooperative event (our half)
   int slot;                        // local slot (own events) or mailbox index (guest)
   unsigned int seq;                // the slot's / mailbox's sequence
@@ -87,22 +91,10 @@ __device__ __forceinline__ unsigned int event_tiles(const EngineParams& p) {
   return (unsigned int)((p.n4 + kTile4 - 1) / kTile4);
 }
 
-// Join an event: +1 on its pin unless the event is over or another one holds
-// the slot (sequence tag).  System scope: a partner GPU's CTAs pin it too.
-__device__ __forceinline__ bool pin_join(unsigned long long* pin, unsigned int seq) {
-  unsigned long long w = ld_relaxed_sys64(pin);
-  while (true) {
-    if ((unsigned int)(w >> 32) != seq || (w & 0xffffffffull) == 0ull) return false;
-    const unsigned long long old = atomicCAS_system(pin, w, w + 1ull);
-    if (old == w) return true;
-    w = old;
-  }
-}
-// Leave it, crediting the tiles this CTA finished; true if this leave ends it.
-__device__ __forceinline__ bool pin_leave(unsigned long long* pin, unsigned int tiles) {
-  const unsigned long long dec = (unsigned long long)tiles + 1ull;
-  const unsigned long long old = atomicAdd_system(pin, 0ull - dec);
-  return (old & 0xffffffffull) == dec;
+// Credit `tiles` finished tiles to an event; true if they were its last ones.
+// System scope: a partner GPU credits its half of a cooperative event too.
+__device__ __forceinline__ bool credit(unsigned int* rem, unsigned int tiles) {
+  return atomicAdd_system(rem, 0u - tiles) == tiles;
 }
 
 // tickets k, k+1, ..: up to `want` consecutive values of rank 0's counter below
@@ -122,15 +114,17 @@ __device__ __forceinline__ bool take_ticket(const EngineParams& p, unsigned long
 }
 
 // Make the slot's event (fields already written) visible as running: fresh
-// claim counter, pin = (new seq, all tiles), then the tag.
+// claim word (new seq, chunk count), remaining tiles, then the tag.
 __device__ void publish_running(const EngineParams& p, Slot* sl, unsigned int seq) {
   const unsigned int T = event_tiles(p);
-  sl->next = 0u;
+  const unsigned int share = sl->coop ? (T + 1u) / 2u : T;
   sl->nwork = 0u;
   sl->ntiles = T;
   sl->commit_ready = 0u;
-  *(volatile unsigned long long*)&sl->pin = ((unsigned long long)(seq + 1u) << 32) | T;
-  __threadfence_system();                            // fields before the tag (a guest reads them)
+  sl->rem = T;
+  __threadfence();                                   // fields before the claim word (a claim reads them)
+  *(volatile unsigned long long*)&sl->next = claim_word(seq + 1, (share + kClaimChunk - 1) / kClaimChunk);
+  __threadfence_system();                            // ... and before the tag (a guest reads them)
   st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
 }
 
@@ -141,12 +135,13 @@ __device__ void publish_running(const EngineParams& p, Slot* sl, unsigned int se
 // its own sequence (a partner serves events of several initiators); the poster
 // holds the partner exclusively (its lock or its epoch), so read-increment is
 // race-free.
-__device__ void post_guest(Slot* sl, const EngineParams& p, int w, int j, unsigned int eseq) {
+__device__ void post_guest(Slot* sl, const EngineParams& p, int w, int j) {
   WorkerCtl* cj = p.workers[j].ctl;                   // peer memory
   *(volatile int*)&cj->guest_i = w;
-  *(volatile unsigned int*)&cj->guest_next = 0u;
   *(volatile unsigned int*)&cj->guest_nwork = 0u;
-  *(volatile unsigned int*)&cj->guest_eseq = eseq;
+  __threadfence_system();                             // guest_i before the claim word
+  *(volatile unsigned long long*)&cj->guest_next =
+      claim_word(sl->gseq, (event_tiles(p) / 2u + kClaimChunk - 1) / kClaimChunk);
   __threadfence_system();
   st_release_sys(&cj->guest_tag, tag_of(sl->gseq, kStateRunning));
 }
@@ -319,7 +314,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
     sl->ev_cur = cur + 1;
     sl->t0 = now;
     publish_running(p, sl, seq);
-    if (sl->coop) post_guest(sl, p, w, e.j, seq + 1);
+    if (sl->coop) post_guest(sl, p, w, e.j);
     return true;
   }
   // ------------------------------------------------------- free-running ----
@@ -397,7 +392,7 @@ __device__ __noinline__ bool try_start(const EngineParams& p, int s, unsigned in
   sl->nb_ctr += 1;
   sl->t0 = now;
   publish_running(p, sl, seq);
-  if (sl->coop) post_guest(sl, p, w, j, seq + 1);
+  if (sl->coop) post_guest(sl, p, w, j);
   return true;
 }
 
@@ -543,7 +538,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
   }
   __syncthreads();
   const int L = p.n_local;
-  const int rot = L ? (int)(blockIdx.x % (unsigned)L) : 0;
+  const int rot = (kRotate && L) ? (int)(blockIdx.x % (unsigned)L) : 0;
   const unsigned int T = event_tiles(p);
   const unsigned int xpart = max(1u, gridDim.x / (unsigned)kCrossDiv);
   Claim cl;                                     // thread 0's claim on the joined event
@@ -564,14 +559,20 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
             continue;
           }
         }
-        const unsigned int seq = tag >> 2;
+        unsigned int seq = tag >> 2;
         if ((tag & 3u) != kStateRunning || seq == done_seq[s]) continue;
+        const unsigned long long w0 = *(volatile unsigned long long*)&sl->next;
+        if (claim_seq(w0) != (seq & kClaimSeqMask) || claim_idx(w0) >= claim_nc(w0)) { done_seq[s] = seq; continue; }
+        if (*(volatile int*)&sl->cross && atomicAdd(&sl->nwork, 1u) >= xpart) { done_seq[s] = seq; continue; }
+        const unsigned long long w = atomicAdd(&sl->next, 1ull);          // join = claim a chunk
+        if (claim_idx(w) >= claim_nc(w)) { done_seq[s] = seq; continue; }
+        // we own a chunk of event claim_seq(w): it is pinned and its fields are
+        // stable until we credit the chunk (a newer event than `seq` if the slot
+        // moved on meanwhile -- then the tag already shows it)
+        __threadfence();
+        if (claim_seq(w) != (seq & kClaimSeqMask)) seq = ld_acquire_gpu(&sl->tag) >> 2;
         const int coop = *(volatile int*)&sl->coop;
         const unsigned int share = coop ? (T + 1u) / 2u : T;
-        if (*(volatile unsigned int*)&sl->next >= share) { done_seq[s] = seq; continue; }
-        if (*(volatile int*)&sl->cross && atomicAdd(&sl->nwork, 1u) >= xpart) { done_seq[s] = seq; continue; }
-        if (!pin_join(&sl->pin, seq)) { done_seq[s] = seq; continue; }
-        // pinned: the fields are stable until we leave
         s_ev.xi = *(float* volatile*)&sl->xi;
         s_ev.xj = *(float* volatile*)&sl->xj;
         const unsigned int fl = *(volatile unsigned int*)&sl->flags;
@@ -588,7 +589,8 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.n = share;
         s_ev.stride = coop ? 2u : 1u;
         s_ev.off = 0u;
-        s_ev.pin = &sl->pin;
+        s_ev.first = claim_idx(w);
+        s_ev.rem = &sl->rem;
         s_ev.guest = 0;
         s_ev.slot = s;
         s_ev.seq = seq;
@@ -601,14 +603,18 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           const int wl = p.local_ids[l];
           WorkerCtl* mb = p.workers[wl].ctl;
           const unsigned int gt = ld_acquire_sys(&mb->guest_tag);
-          const unsigned int gseq = gt >> 2;
+          unsigned int gseq = gt >> 2;
           if ((gt & 3u) != kStateRunning || gseq == gdone_seq[l]) continue;
           const unsigned int share = T / 2u;
-          if (*(volatile unsigned int*)&mb->guest_next >= share) { gdone_seq[l] = gseq; continue; }
+          const unsigned long long w0 = *(volatile unsigned long long*)&mb->guest_next;
+          if (claim_seq(w0) != (gseq & kClaimSeqMask) || claim_idx(w0) >= claim_nc(w0)) { gdone_seq[l] = gseq; continue; }
           if (atomicAdd(&mb->guest_nwork, 1u) >= xpart) { gdone_seq[l] = gseq; continue; }
+          const unsigned long long w = atomicAdd(&mb->guest_next, 1ull);
+          if (claim_idx(w) >= claim_nc(w)) { gdone_seq[l] = gseq; continue; }
+          __threadfence_system();                         // the poster's guest_i / slot fields
+          if (claim_seq(w) != (gseq & kClaimSeqMask)) gseq = ld_acquire_sys(&mb->guest_tag) >> 2;
           const int gi = *(volatile int*)&mb->guest_i;
           Slot* sa = p.workers[gi].slot;                 // the initiator's slot (peer memory)
-          if (!pin_join(&sa->pin, *(volatile unsigned int*)&mb->guest_eseq)) { gdone_seq[l] = gseq; continue; }
           const unsigned int fl = *(volatile unsigned int*)&sa->flags;
           s_ev.xi = p.workers[gi].x;
           s_ev.xj = p.workers[wl].x;
@@ -625,7 +631,8 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           s_ev.n = share;
           s_ev.stride = 2u;
           s_ev.off = 1u;
-          s_ev.pin = &sa->pin;
+          s_ev.first = claim_idx(w);
+          s_ev.rem = &sa->rem;
           s_ev.guest = 1;
           s_ev.slot = l;
           s_ev.seq = gseq;
@@ -651,7 +658,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
       } else if (pick != kExit) {
         last_progress = globaltimer();
-        cl.init(s_ev.ctr, s_ev.n, s_ev.stride, s_ev.off);
+        cl.init(s_ev.ctr, s_ev.n, s_ev.stride, s_ev.off, s_ev.first);
       }
       s_pick = pick;
     }
@@ -698,7 +705,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         else __threadfence();
         if (e.guest) gdone_seq[e.slot] = e.seq;
         else done_seq[e.slot] = e.seq;
-        if (pin_leave(e.pin, tiles)) {
+        if (tiles && credit(e.rem, tiles)) {
           if (e.guest) st_release_sys(e.gready, e.seq);   // the initiator's scheduler commits
           else commit(p, e.slot);
         }

@@ -12,11 +12,11 @@ namespace adp {
 // --------------------------------------------------------------- engine ----
 struct Slot {                      // per local worker, in the peer-mapped control arena
   unsigned int tag;                // (seq << 2) | state
-  unsigned int next;               // tile claim counter of this GPU's share of the running event
-  unsigned long long pin;          // (event seq << 32) | (unfinished tiles + CTAs joined): the CTA
-                                   // whose leave brings it to 0 commits the event
-  unsigned int nwork;              // CTAs of this GPU that joined (cross events are capped)
-  unsigned int ntiles;             // tiles of the event (both GPUs' shares for a coop event)
+  unsigned int rem;                // tiles of the running event not yet credited (both GPUs' for a
+                                   // coop event): the CTA whose credit brings it to 0 commits
+  unsigned long long next;         // claim word of this GPU's share (claim_word, device.cuh)
+  unsigned int nwork;              // CTAs of this GPU that tried to join (cross events are capped)
+  unsigned int ntiles;             // tiles of the event
   int i, j;
   int tau;
   unsigned int flags;

@@ -884,7 +884,7 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
                         const adpsgd_config* cfg, adpsgd_ctx** out) {
   if (!g || !cfg || !out) return fail(ADPSGD_E_INVALID, "null argument");
   if (n_workers != g->n) return fail(ADPSGD_E_INVALID, "n_workers != graph.n");
-  if (d < 1 || d > (1LL << 31) - 64) return fail(ADPSGD_E_INVALID, "d out of range");
+  if (d < 1 || d > (1LL << 31) - 64) return fail(ADPSGD_E_INVALID, "d out of range");   // engine: < 2^16 claim chunks
   if (cfg->world_size < 1 || cfg->rank < 0 || cfg->rank >= cfg->world_size)
     return fail(ADPSGD_E_INVALID, "rank/world_size");
   if (cfg->batch_M < 0 || cfg->staleness_cap_T < 0) return fail(ADPSGD_E_INVALID, "M/T < 0");
