@@ -376,18 +376,19 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
 
 /* Diagnostics: the MLP's tensor-core GEMM on its own.
  * C[M x N] = A[M x K] . B[N x K]^T, fp32 row-major DEVICE pointers on the current
- * device, computed as 3xTF32 (hi*hi + hi*lo + lo*hi) with tcgen05.mma into TMEM,
- * split-K over `splits` CTAs per tile (partials summed in a fixed order).
- * Requires M % 128 == 0, N % 128 == 0, K % (32 * splits) == 0.  Synchronous.   */
+ * device, computed as 3xTF32 (hi*hi + hi*lo + lo*hi, the split done in shared
+ * memory) with tcgen05.mma into TMEM, split-K over `splits` CTAs per tile
+ * (partials summed in a fixed order).  Requires M % 128 == 0, N % 64 == 0,
+ * K % (32 * splits) == 0.  Synchronous.                                        */
 adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
                                  int32_t splits);
 
 /* Diagnostics: device time of that GEMM alone (tcgen05 utilisation
  * of the MLP GEMMs swept over M).  Allocates operands of the given shape on the
- * current device, splits them into tf32 planes once, then times `reps` launches
+ * current device, then times `reps` launches
  * of the GEMM kernel (+ the split-K partial sum when splits > 1) with CUDA
  * events after 2 warm-up launches; *ms_out = mean milliseconds per GEMM.
- * bn = 128 or 256 (N tile).  Shape rules as adpsgd_gemm_tf32x3.  Synchronous. */
+ * bn = 64 or 128 (N tile).  Shape rules as adpsgd_gemm_tf32x3.  Synchronous.  */
 adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t bn, int32_t reps,
                                        double* ms_out);
 

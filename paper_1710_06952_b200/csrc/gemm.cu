@@ -6,12 +6,22 @@
 // dW1 = dZ1^T X_b.  Accuracy ~fp32 via the 3xTF32 split:
 //   A = A_hi + A_lo, B = B_hi + B_lo (hi = rna_tf32(x), lo = rna_tf32(x - hi)),
 //   C ~= A_hi B_hi + A_hi B_lo + A_lo B_hi   (three tcgen05.mma into one TMEM accumulator).
+// The operands are read ONCE, as fp32: TMA brings a 128-byte-swizzled fp32 tile
+// into shared memory and the CTA splits it there -- hi overwrites the tile in
+// place (an elementwise split keeps the swizzled layout), lo goes to a second
+// tile -- so no hi/lo planes are ever written to HBM (round 1 pre-split W1, X_b
+// and dZ1^T in separate passes: 3 extra launches and ~19 MB per gradient).
 //
-// CTA = 128 threads, tile 128 x BN, k-block 32 fp32 (= one 128-byte swizzle atom).
-// warp 0 / lane 0: TMA producer (cp.async.bulk.tensor, SWIZZLE_128B, 4 tiles per stage)
-// warp 1 / lane 0: MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8)
-// all 4 warps    : epilogue (tcgen05.ld 32x32b -> registers -> global)
-// Split-K: blockIdx.z takes a K range and writes its own partial plane.
+// CTA = 128 threads, tile 128 x BN (BN = 64 / 128), k-block 32 fp32 (= one
+// 128-byte swizzle atom), STAGES k-blocks in flight.  Per k-block:
+//   thread 0     : TMA producer (refills the stage the previous k-block used once
+//                  its MMAs have drained it: one k-block of slack)
+//   all threads  : split the staged tile into hi / lo, fence.proxy.async, barrier
+//   thread 32    : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8)
+// then all 4 warps run the epilogue (tcgen05.ld 32x32b -> registers -> global).
+// Split-K: blockIdx.z takes a K range and writes its own partial plane.  Grid
+// rows beyond M / 128 run a caller-supplied tail task instead (the MLP's batch
+// reductions ride on the dW1 launch).
 #include <cuda.h>
 #include "internal.h"
 
@@ -57,13 +67,64 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+__device__ __forceinline__ void split_tf32(float v, float& h, float& l) {
+  uint32_t a, b;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(v));
+  const float r = v - __uint_as_float(a);
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(r));
+  h = __uint_as_float(a);
+  l = __uint_as_float(b);
+}
+
+// the MLP's batch reductions (reading R18): db1[u] = sum_b dz1[b][u],
+// dW2[o][u] = sum_b dz2[b][o] h[b][u], db2[o] = sum_b dz2[b][o].  Four lanes per
+// output, each summing every 4th sample (independent loads in flight), combined
+// by shuffles in a fixed order: deterministic.
+__device__ void mlp_reduce_task(const GemmTail& t, int task, int ntask) {
+  const int M = t.M, H = t.H, O = t.O;
+  const long long n = (long long)H + (long long)O * H + O;
+  const int sub = threadIdx.x & 3;
+  const long long per = blockDim.x / 4;
+  for (long long q = (long long)task * per + (threadIdx.x >> 2); q - (threadIdx.x >> 2) < n;
+       q += (long long)ntask * per) {
+    float acc = 0.0f;
+    if (q < n) {
+      if (q < H) {
+#pragma unroll 8
+        for (int b = sub; b < M; b += 4) acc += t.dz1[(long long)b * H + q];
+      } else if (q < H + (long long)O * H) {
+        const long long r = q - H;
+        const int o = (int)(r / H), u = (int)(r % H);
+#pragma unroll 8
+        for (int b = sub; b < M; b += 4) acc = fmaf(t.dz2[(long long)b * O + o], t.h[(long long)b * H + u], acc);
+      } else {
+        const int o = (int)(q - H - (long long)O * H);
+#pragma unroll 8
+        for (int b = sub; b < M; b += 4) acc += t.dz2[(long long)b * O + o];
+      }
+    }
+    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
+    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
+    if (q < n && sub == 0) {
+      if (q < H) t.g[t.off_b1 + q] = acc;
+      else if (q < H + (long long)O * H) t.g[t.off_W2 + (q - H)] = acc;
+      else t.g[t.off_b2 + (q - H - (long long)O * H)] = acc;
+    }
+  }
+}
+
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
-    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmAh, const __grid_constant__ CUtensorMap tmAl,
-                  const __grid_constant__ CUtensorMap tmBh, const __grid_constant__ CUtensorMap tmBl,
-                  float* __restrict__ C, int ldc, int kb_per_split, long long split_stride) {
-  constexpr uint32_t kATile = kBM * 128, kBTile = BN * 128;
-  constexpr uint32_t kStage = 2 * kATile + 2 * kBTile;
+    k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                  float* __restrict__ C, int ldc, int kb_per_split, long long split_stride, int m_tiles,
+                  const __grid_constant__ GemmTail tail) {
+  if ((int)blockIdx.y >= m_tiles) {                          // tail rows of the grid
+    mlp_reduce_task(tail, (int)(blockIdx.y - m_tiles) * gridDim.x + blockIdx.x,
+                    (int)(gridDim.y - m_tiles) * gridDim.x);
+    return;
+  }
+  constexpr uint32_t kATile = kBM * 128, kBTile = BN * 128;  // fp32 tiles (the hi halves after the split)
+  constexpr uint32_t kStage = 2 * kATile + 2 * kBTile;       // [A32|hi][A lo][B32|hi][B lo]
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[STAGES], empty[STAGES], accum;
   __shared__ uint32_t tmem_base_s;
@@ -77,12 +138,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     for (int s = 0; s < STAGES; ++s) { mbar_init(&full[s], 1); mbar_init(&empty[s], 1); }
     mbar_init(&accum, 1);
     mbar_fence_init();
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmAh) : "memory");
-    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmBh) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
   }
+  constexpr uint32_t kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;   // power of 2
   if (warp == 0) {                                           // TMEM: 128 lanes x BN fp32 columns
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
-                     smem_u32(&tmem_base_s)), "r"((uint32_t)BN) : "memory");
+                     smem_u32(&tmem_base_s)), "r"(kTmemCols) : "memory");
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -90,26 +152,43 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = tmem_base_s;
 
-  if (warp == 0 && lane == 0) {
-    // ------------------------------------------------------------ producer
-    for (int kb = 0; kb < kb_per_split; ++kb) {
-      const int s = kb % STAGES;
-      const uint32_t use = (uint32_t)(kb / STAGES);
-      if (kb >= STAGES) mbar_wait(&empty[s], (use - 1u) & 1u);
-      unsigned char* st = sbase + (size_t)s * kStage;
-      mbar_arrive_tx(&full[s], kStage);
-      const int kc = (kb0 + kb) * kBK;
-      tma_load_2d(st, &tmAh, kc, m0, &full[s]);
-      tma_load_2d(st + kATile, &tmAl, kc, m0, &full[s]);
-      tma_load_2d(st + 2 * kATile, &tmBh, kc, n0, &full[s]);
-      tma_load_2d(st + 2 * kATile + kBTile, &tmBl, kc, n0, &full[s]);
+  auto load = [&](int kb) {                                  // thread 0: TMA fp32 A and B tiles of k-block kb
+    const int s = kb % STAGES;
+    unsigned char* st = sbase + (size_t)s * kStage;
+    mbar_arrive_tx(&full[s], kATile + kBTile);
+    const int kc = (kb0 + kb) * kBK;
+    tma_load_2d(st, &tmA, kc, m0, &full[s]);
+    tma_load_2d(st + 2 * kATile, &tmB, kc, n0, &full[s]);
+  };
+  if (threadIdx.x == 0)
+    for (int kb = 0; kb < STAGES && kb < kb_per_split; ++kb) load(kb);
+
+  constexpr uint32_t idesc = tf32_idesc(kBM, BN);
+  for (int kb = 0; kb < kb_per_split; ++kb) {
+    const int s = kb % STAGES;
+    mbar_wait(&full[s], (uint32_t)(kb / STAGES) & 1u);
+    // split the staged fp32 tiles: hi in place, lo into the stage's lo tiles
+    float4* a32 = reinterpret_cast<float4*>(sbase + (size_t)s * kStage);
+    float4* alo = reinterpret_cast<float4*>(sbase + (size_t)s * kStage + kATile);
+    float4* b32 = reinterpret_cast<float4*>(sbase + (size_t)s * kStage + 2 * kATile);
+    float4* blo = reinterpret_cast<float4*>(sbase + (size_t)s * kStage + 2 * kATile + kBTile);
+#pragma unroll
+    for (int q = threadIdx.x; q < (int)(kATile / 16); q += kGemmThreads) {
+      float4 v = a32[q], h, l;
+      split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y); split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
+      a32[q] = h;
+      alo[q] = l;
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------------------------------------------------- MMA issue
-    constexpr uint32_t idesc = tf32_idesc(kBM, BN);
-    for (int kb = 0; kb < kb_per_split; ++kb) {
-      const int s = kb % STAGES;
-      mbar_wait(&full[s], (uint32_t)(kb / STAGES) & 1u);
+#pragma unroll
+    for (int q = threadIdx.x; q < (int)(kBTile / 16); q += kGemmThreads) {
+      float4 v = b32[q], h, l;
+      split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y); split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
+      b32[q] = h;
+      blo[q] = l;
+    }
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
+    __syncthreads();
+    if (threadIdx.x == 32) {
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const uint32_t st = base + (uint32_t)s * kStage;
       const uint64_t ah = sw128_desc(st), al = sw128_desc(st + kATile);
@@ -121,11 +200,16 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
         mma_tf32(tmem, ah + o, bl + o, idesc, 1u);
         mma_tf32(tmem, al + o, bh + o, idesc, 1u);
       }
-      mma_commit(&empty[s]);                                // smem stage free when these complete
+      mma_commit(&empty[s]);                                // stage s free when these complete
+      if (kb == kb_per_split - 1) mma_commit(&accum);       // accumulator ready
     }
-    mma_commit(&accum);                                     // accumulator ready
+    // refill the stage the previous k-block used, once its MMAs drained it
+    if (threadIdx.x == 0 && kb >= 1 && kb - 1 + STAGES < kb_per_split) {
+      const int sp = (kb - 1) % STAGES;
+      mbar_wait(&empty[sp], (uint32_t)((kb - 1) / STAGES) & 1u);
+      load(kb - 1 + STAGES);
+    }
   }
-  __syncwarp();
 
   // ------------------------------------------------------------------ epilogue
   mbar_wait(&accum, 0u);
@@ -155,21 +239,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   __syncthreads();
   if (warp == 0) {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"((uint32_t)BN) : "memory");
-  }
-}
-
-// hi = rna_tf32(x), lo = rna_tf32(x - hi)
-__global__ void k_split_tf32(const float* __restrict__ x, float* __restrict__ hi, float* __restrict__ lo,
-                             long long n) {
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n; i += (long long)gridDim.x * blockDim.x) {
-    const float v = x[i];
-    uint32_t h, l;
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(h) : "f"(v));
-    const float r = v - __uint_as_float(h);
-    asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
-    hi[i] = __uint_as_float(h);
-    lo[i] = __uint_as_float(l);
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(kTmemCols) : "memory");
   }
 }
 
@@ -214,28 +284,30 @@ cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long lon
   return cudaGetLastError();
 }
 
-cudaError_t launch_split_tf32(const float* x, float* hi, float* lo, long long n, cudaStream_t s) {
-  k_split_tf32<<<592, 256, 0, s>>>(x, hi, lo, n);
-  return cudaGetLastError();
-}
-
-// C (+ z * split_stride) = A . B^T over K range of split z; M % 128 == 0, N % BN == 0, K % (32 * splits) == 0
-cudaError_t launch_gemm_tf32x3(const GemmOperands& op, float* C, int M, int N, int K, int splits, int bn,
-                               cudaStream_t s) {
-  if (M % kBM || K % (kBK * splits) || (bn != 128 && bn != 256) || N % bn) return cudaErrorInvalidValue;
+// C (+ z * split_stride) = A . B^T over K range of split z; M % 128 == 0, N % BN == 0, K % (32 * splits) == 0.
+// tail (nullable): tail_rows extra grid rows run the MLP's batch reductions.
+cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float* C, int M, int N, int K, int splits,
+                               int bn, const GemmTail* tail, int tail_rows, cudaStream_t s) {
+  if (M % kBM || K % (kBK * splits) || (bn != 64 && bn != 96 && bn != 128) || N % bn) return cudaErrorInvalidValue;
   const int kbps = K / kBK / splits;
   const long long sstride = (long long)M * N;
-  dim3 grid(N / bn, M / kBM, splits);
+  const GemmTail t = tail ? *tail : GemmTail{};
+  dim3 grid(N / bn, M / kBM + (tail ? tail_rows : 0), splits);
   if (bn == 128) {
     constexpr int S = 3;                                    // 3 x 64 KB stages
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 128 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<128, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gemm_tf32x3<128, S><<<grid, kGemmThreads, smem, s>>>(op.Ah, op.Al, op.Bh, op.Bl, C, N, kbps, sstride);
+    k_gemm_tf32x3<128, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
+  } else if (bn == 96) {
+    constexpr int S = 4;                                    // 4 x 56 KB stages: 128 x 96 tiles, one CTA per SM
+    const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 96 * 128) + 1024;
+    cudaFuncSetAttribute(k_gemm_tf32x3<96, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gemm_tf32x3<96, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
   } else {
-    constexpr int S = 2;                                    // 2 x 96 KB stages
-    const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 256 * 128) + 1024;
-    cudaFuncSetAttribute(k_gemm_tf32x3<256, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gemm_tf32x3<256, S><<<grid, kGemmThreads, smem, s>>>(op.Ah, op.Al, op.Bh, op.Bl, C, N, kbps, sstride);
+    constexpr int S = 4;                                    // 4 x 48 KB stages
+    const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 64 * 128) + 1024;
+    cudaFuncSetAttribute(k_gemm_tf32x3<64, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    k_gemm_tf32x3<64, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
   }
   return cudaGetLastError();
 }

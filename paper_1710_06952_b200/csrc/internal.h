@@ -138,31 +138,37 @@ cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d,
                              cudaStream_t s);
 
 // 3xTF32 tcgen05 GEMM (gemm.cu): C = A . B^T, A [M x K], B [N x K] row-major fp32,
-// operands pre-split into tf32 hi/lo planes and described by SWIZZLE_128B tensor maps
-struct GemmOperands {
-  CUtensorMap Ah, Al, Bh, Bl;
+// described by SWIZZLE_128B fp32 tensor maps (box 32 x 128 for A, 32 x bn for B);
+// the hi / lo split happens in shared memory
+struct GemmTail {                  // the MLP's batch reductions, run by extra grid rows
+  const float *h, *dz1, *dz2;
+  float* g;
+  long long off_b1, off_W2, off_b2;
+  int M, H, O;
 };
 cudaError_t make_tmap_k_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols, int box_rows);
-cudaError_t launch_split_tf32(const float* x, float* hi, float* lo, long long n, cudaStream_t s);
 cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long long n, cudaStream_t s);
-cudaError_t launch_gemm_tf32x3(const GemmOperands& op, float* C, int M, int N, int K, int splits, int bn,
-                               cudaStream_t s);
+cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float* C, int M, int N, int K, int splits,
+                               int bn, const GemmTail* tail, int tail_rows, cudaStream_t s);
 
-// MLP (kind 5): tcgen05-backed gradient (mlp.cu)
+// MLP (kind 5): tcgen05-backed gradient (mlp.cu), 5 launches:
+//   gather (+ batch indices) -> GEMM1 (split-K planes) -> per-sample mid -> GEMM2 || batch reductions
 struct MlpShape { int n_in, n_hid, n_out; };
-struct MlpWork {                   // scratch carve-up + tensor maps, built once per context
+struct MlpWork {                   // scratch carve-up + the fixed tensor maps, built once per context
   MlpShape sh;
   int M, splits;
-  float *xh, *xl, *th, *tl, *w1h, *w1l, *z1p, *hbuf, *dz1, *dz2, *dth, *dtl;
+  float *xb, *xbt, *z1p, *hbuf, *dz1, *dz2, *dzt;
   int* idx;
-  GemmOperands g1, g2;
+  CUtensorMap x_b, dzt_m, xbt_m;   // GEMM1 A, GEMM2 A, GEMM2 B (W1, GEMM1's B, is mapped per call)
+  cudaStream_t side = nullptr;     // the batch reductions run here beside GEMM2
+  cudaEvent_t fork = nullptr, join = nullptr;
 };
 size_t mlp_scratch_floats(const MlpShape& sh, int M);
 bool mlp_supported(const MlpShape& sh, int M);
 cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch);
 cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx,
                             uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s);
-constexpr int kMlpLaunches = 7;
+constexpr int kMlpLaunches = 5;
 
 // one kernel of each translation unit (CUDA module), see preload_modules()
 const void* kernels_module_anchor();

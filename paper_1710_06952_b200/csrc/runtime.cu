@@ -352,7 +352,15 @@ adpsgd_status ensure_gslots(adpsgd_ctx* c, int count) {
   return ADPSGD_OK;
 }
 
-// one MLP scratch (gathered batch, W1 split, partial planes, tensor maps) per stream lane
+void release_mlp_work(MlpWork& w) {
+  if (w.side) cudaStreamDestroy(w.side);
+  if (w.fork) cudaEventDestroy(w.fork);
+  if (w.join) cudaEventDestroy(w.join);
+  w.side = nullptr;
+  w.fork = w.join = nullptr;
+}
+
+// one MLP scratch (gathered batch, partial planes, tensor maps, side stream) per stream lane
 adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c, int lanes = 1) {
   const size_t per = (mlp_scratch_floats(c->mlp, c->M) + 255) / 256 * 256;
   if ((int)c->mlp_work.size() >= lanes) return ADPSGD_OK;
@@ -361,6 +369,7 @@ adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c, int lanes = 1) {
   c->mlp_scratch = nullptr;
   CU(cudaMalloc(&c->mlp_scratch, sizeof(float) * per * lanes));
   c->mlp_scratch_n = per * lanes;
+  for (MlpWork& w : c->mlp_work) release_mlp_work(w);
   c->mlp_work.assign(lanes, MlpWork{});
   for (int l = 0; l < lanes; ++l)                                 // tensor maps over each lane's planes
     CU(mlp_plan(c->mlp_work[l], c->mlp, c->M, c->mlp_scratch + per * l));
@@ -825,6 +834,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
     if (c->peer_models[r]) cudaIpcCloseMemHandle(c->peer_models[r]);
     if (c->peer_ctl[r]) cudaIpcCloseMemHandle(c->peer_ctl[r]);
   }
+  for (MlpWork& w : c->mlp_work) release_mlp_work(w);
   for (auto e : c->last_evt) if (e) cudaEventDestroy(e);
   for (auto e : c->evring) if (e) cudaEventDestroy(e);
   for (auto st : c->pool) if (st) cudaStreamDestroy(st);
@@ -957,8 +967,8 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
                             (long long)c->mlp.n_out * c->mlp.n_hid + c->mlp.n_out;
       if (dim != d || !cfg->data_y) return fail(ADPSGD_E_INVALID, "mlp dims do not match d / labels missing");
       if (!mlp_supported(c->mlp, c->M))
-        return fail(ADPSGD_E_UNSUPPORTED, "MLP tensor-core path needs batch_M, mlp_in, mlp_hid multiples of 128 "
-                                          "and mlp_out <= 32");
+        return fail(ADPSGD_E_UNSUPPORTED, "MLP tensor-core path needs batch_M, mlp_in, mlp_hid multiples of 128, "
+                                          "mlp_hid <= 1024 and mlp_out <= 32");
       c->feat = c->mlp.n_in;
     } else {
       if (!cfg->data_b) return fail(ADPSGD_E_INVALID, "data_b required");
@@ -1926,24 +1936,19 @@ adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32
                                  int32_t splits) {
   GUARD({
     if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(ADPSGD_E_INVALID, "gemm args");
-    if (M % 128 || N % 128 || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
-    const size_t na = (size_t)M * K, nb = (size_t)N * K;
-    float* buf = nullptr;
-    CU(cudaMalloc(&buf, sizeof(float) * (2 * na + 2 * nb + (size_t)splits * M * N)));
-    float *ah = buf, *al = ah + na, *bh = al + na, *bl = bh + nb, *part = bl + nb;
-    GemmOperands op;
+    if (M % 128 || N % 64 || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
+    const int bn = N % 128 == 0 ? 128 : 64;
+    float* part = nullptr;
+    if (splits > 1) CU(cudaMalloc(&part, sizeof(float) * (size_t)splits * M * N));
+    CUtensorMap ta, tb;
     adpsgd_status st = ADPSGD_OK;
-    cudaError_t e = launch_split_tf32(A, ah, al, (long long)na, nullptr);
-    if (e == cudaSuccess) e = launch_split_tf32(B, bh, bl, (long long)nb, nullptr);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Ah, ah, M, K, 128);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Al, al, M, K, 128);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bh, bh, N, K, 128);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bl, bl, N, K, 128);
-    if (e == cudaSuccess) e = launch_gemm_tf32x3(op, splits > 1 ? part : C, M, N, K, splits, 128, nullptr);
+    cudaError_t e = make_tmap_k_major(&ta, A, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&tb, B, N, K, bn);
+    if (e == cudaSuccess) e = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : C, M, N, K, splits, bn, nullptr, 0, nullptr);
     if (e == cudaSuccess && splits > 1) e = launch_sum_planes(part, C, splits, (long long)M * N, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) st = fail(ADPSGD_E_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
-    cudaFree(buf);
+    if (part) cudaFree(part);
     return st;
   })
 }
@@ -1951,27 +1956,23 @@ adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32
 adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t splits, int32_t bn, int32_t reps,
                                        double* ms_out) {
   GUARD({
-    if (!ms_out || M <= 0 || N <= 0 || K <= 0 || splits < 1 || reps < 1 || (bn != 128 && bn != 256))
+    if (!ms_out || M <= 0 || N <= 0 || K <= 0 || splits < 1 || reps < 1 || (bn != 64 && bn != 128))
       return fail(ADPSGD_E_INVALID, "gemm bench args");
     if (M % 128 || N % bn || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
     const size_t na = (size_t)M * K, nb = (size_t)N * K;
     float* buf = nullptr;
-    CU(cudaMalloc(&buf, sizeof(float) * (3 * na + 3 * nb + (size_t)(splits + 1) * M * N)));
-    float *a = buf, *b = a + na, *ah = b + nb, *al = ah + na, *bh = al + na, *bl = bh + nb, *part = bl + nb;
+    CU(cudaMalloc(&buf, sizeof(float) * (na + nb + (size_t)(splits + 1) * M * N)));
+    float *a = buf, *b = a + na, *part = b + nb;
     float* c = part + (size_t)splits * M * N;
-    GemmOperands op;
+    CUtensorMap ta, tb;
     adpsgd_status st = ADPSGD_OK;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     cudaError_t e = launch_fill_hash(a, (long long)na, 1u, nullptr);
     if (e == cudaSuccess) e = launch_fill_hash(b, (long long)nb, 2u, nullptr);
-    if (e == cudaSuccess) e = launch_split_tf32(a, ah, al, (long long)na, nullptr);
-    if (e == cudaSuccess) e = launch_split_tf32(b, bh, bl, (long long)nb, nullptr);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Ah, ah, M, K, 128);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Al, al, M, K, 128);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bh, bh, N, K, bn);
-    if (e == cudaSuccess) e = make_tmap_k_major(&op.Bl, bl, N, K, bn);
+    if (e == cudaSuccess) e = make_tmap_k_major(&ta, a, M, K, 128);
+    if (e == cudaSuccess) e = make_tmap_k_major(&tb, b, N, K, bn);
     auto once = [&]() {
-      cudaError_t r = launch_gemm_tf32x3(op, splits > 1 ? part : c, M, N, K, splits, bn, nullptr);
+      cudaError_t r = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : c, M, N, K, splits, bn, nullptr, 0, nullptr);
       if (r == cudaSuccess && splits > 1) r = launch_sum_planes(part, c, splits, (long long)M * N, nullptr);
       return r;
     };

@@ -22,8 +22,8 @@ def sweep(reps=20):
     for M in (128, 1024, 4096):
         for name, (m, n, k) in (("gemm1 X_b.W1^T", (M, 512, 3072)), ("gemm2 dZ1^T.X_b", (512, 3072, M))):
             best = None
-            for bn in (128, 256):
-                for splits in (1, 2, 4, 8):
+            for bn in (64, 128):
+                for splits in (1, 2, 4, 8, 16):
                     if k % (32 * splits) or n % bn:
                         continue
                     ms = P.gemm_tf32x3_bench(m, n, k, splits, bn, reps)
