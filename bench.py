@@ -677,6 +677,15 @@ def main():
                 "updates_per_s": sumr(u1 - u0) / secw,
                 "gossip_steps_per_s": sumr(s1["local_pair_events"] - s0["local_pair_events"]) / secw,
                 "events_per_s": sumr(s1["local_events"] - s0["local_events"]) / secw}
+            if rank == 0:
+                # staleness of the flushed gradients, tau = k - t_read, from the event log
+                lg = cw.read_log(max(0, cw.ticket() - (1 << 15)))
+                flushed = lg["tau"][(lg["flags"] & 1) == 0]
+                if len(flushed):
+                    hist = np.bincount(flushed)
+                    wf["compensated" if mode == 2 else "plain"]["staleness_histogram"] = {
+                        "tau_counts": hist.tolist()[:64], "mean_tau": float(flushed.mean()),
+                        "max_tau": int(flushed.max()), "events": int(len(flushed))}
             cw.destroy()
             barrier()
         wf["workload"] = "config 4 workload and straggler, adpsgd_run with wait_free = 1 / 2"

@@ -299,12 +299,13 @@ cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float
     cudaFuncSetAttribute(k_gemm_tf32x3<128, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_gemm_tf32x3<128, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
   } else if (bn == 96) {
-    constexpr int S = 4;                                    // 4 x 56 KB stages: 128 x 96 tiles, one CTA per SM
+    constexpr int S = 3;                                    // 3 x 56 KB stages: 128 x 96 tiles
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 96 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<96, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_gemm_tf32x3<96, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
   } else {
-    constexpr int S = 4;                                    // 4 x 48 KB stages
+    constexpr int S = 3;                                    // 3 x 48 KB stages (config-3 replay A/B: 2 / 3 / 4
+                                                            // stages 30.3-31.3k / 31.1k / 29.1k updates/s)
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 64 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<64, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     k_gemm_tf32x3<64, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);

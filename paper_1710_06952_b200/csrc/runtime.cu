@@ -14,6 +14,7 @@
 #include <vector>
 
 #include <nccl.h>
+#include <nvtx3/nvToolsExt.h>
 #include <unistd.h>
 
 #include "../../include/adpsgd.h"
@@ -1082,7 +1083,14 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
     return fail(ADPSGD_E_INVALID, "internal exception");                              \
   }
 
+// NVTX range over a public call (header-only NVTX 3: no cost unless a tool attaches)
+struct NvtxScope {
+  explicit NvtxScope(const char* name) { nvtxRangePushA(name); }
+  ~NvtxScope() { nvtxRangePop(); }
+};
+
 #define CTX_CHECK(c)                                                                  \
+  NvtxScope nvtx_scope_(__func__);                                                    \
   if (!(c)) return fail(ADPSGD_E_INVALID, "null context");                           \
   CU(cudaSetDevice((c)->device));
 

@@ -1,8 +1,9 @@
 """Small, ragged instances of every device path in one process (host and engine
 replay, free-running, wait-free + slow link, step/gossip, consensus, both
 synchronous baselines, lsq/logreg, the tcgen05 MLP) -- a quick all-paths smoke,
-sized so it could also run under `compute-sanitizer --tool memcheck` (which is
-closed on the current GPU pool).
+sized to run under compute-sanitizer (memcheck / racecheck / synccheck) -- which
+this GPU pool refuses ("closed ... runs under it have left GPUs needing a reset",
+profiles/r02_sanitizer_refused.log); the driver-side parity suite is the check.
 
     python tools/sanitize_smoke.py
 """
@@ -39,6 +40,8 @@ def main():
     c.replay(ev, flags=P.REPLAY_HOST)
     ev0, _ = synth.schedule_iid(n, e, K=40, seed=3, local_prob=0.3)
     c.replay(ev0, flags=P.REPLAY_ENGINE)
+    ev1, _ = synth.schedule_iid(n, e, K=40, T=3, seed=7, local_prob=0.3)     # engine stale-read ops
+    c.replay(ev1, flags=P.REPLAY_ENGINE)
     c.run(200)
     c.step(0)
     c.gossip(2, 3)
@@ -85,6 +88,17 @@ def main():
     c.replay(ev)
     c.sync()
     c.destroy()
+    # two in-process ranks on this GPU: cooperative cross-rank events, remote locks, mailboxes
+    tg = P.ThreadGroup(2)
+
+    def rank_body(rk):
+        cc = P.Context(e, n, d, role=r, rank=rk, world_size=2, device=0, placement=1, x0_per_worker=X0,
+                       compute_ns=5_000, group=tg, **q)
+        cc.run(100)
+        cc.sync()
+        tg.barrier()
+        cc.destroy()
+    P.run_ranks(2, rank_body, group=tg)
     torch.cuda.synchronize()
     print("SANITIZE_SMOKE OK")
 
