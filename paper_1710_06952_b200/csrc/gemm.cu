@@ -7,18 +7,19 @@
 //   A = A_hi + A_lo, B = B_hi + B_lo (hi = rna_tf32(x), lo = rna_tf32(x - hi)),
 //   C ~= A_hi B_hi + A_hi B_lo + A_lo B_hi   (three tcgen05.mma into one TMEM accumulator).
 // The operands are read ONCE, as fp32: TMA brings a 128-byte-swizzled fp32 tile
-// into shared memory and the CTA splits it there -- hi overwrites the tile in
-// place (an elementwise split keeps the swizzled layout), lo goes to a second
-// tile -- so no hi/lo planes are ever written to HBM (round 1 pre-split W1, X_b
-// and dZ1^T in separate passes: 3 extra launches and ~19 MB per gradient).
+// into shared memory, which serves as hi as is (the tensor core drops the low 13
+// mantissa bits: hi = trunc_tf32(x)), and the CTA writes lo = rna_tf32(x - hi)
+// into a second tile of the same swizzled layout -- so no hi/lo planes are ever
+// written to HBM (round 1 pre-split W1, X_b and dZ1^T in separate passes: 3 extra
+// launches and ~19 MB per gradient).
 //
-// CTA = 128 threads, tile 128 x BN (BN = 64 / 128), k-block 32 fp32 (= one
+// CTA = 256 threads, tile 128 x BN (BN = 64 / 96 / 128), k-block 32 fp32 (= one
 // 128-byte swizzle atom), STAGES k-blocks in flight.  Per k-block:
 //   thread 0     : TMA producer (refills the stage the previous k-block used once
 //                  its MMAs have drained it: one k-block of slack)
-//   all threads  : split the staged tile into hi / lo, fence.proxy.async, barrier
+//   all threads  : write lo of the staged tiles, fence.proxy.async, barrier
 //   thread 32    : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8)
-// then all 4 warps run the epilogue (tcgen05.ld 32x32b -> registers -> global).
+// then all 8 warps run the epilogue (tcgen05.ld 32x32b -> registers -> global).
 // Split-K: blockIdx.z takes a K range and writes its own partial plane.  Grid
 // rows beyond M / 128 run a caller-supplied tail task instead (the MLP's batch
 // reductions ride on the dW1 launch).
@@ -29,7 +30,7 @@ namespace adp {
 
 namespace {
 
-constexpr int kBM = 128, kBK = 32, kGemmThreads = 128;
+constexpr int kBM = 128, kBK = 32, kGemmThreads = 256;   // 8 warps: all split, warps w and w+4 share TMEM lanes
 
 __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* tm, int c0, int c1, uint64_t* bar) {
   asm volatile(
@@ -67,13 +68,16 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
-__device__ __forceinline__ void split_tf32(float v, float& h, float& l) {
-  uint32_t a, b;
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(a) : "f"(v));
-  const float r = v - __uint_as_float(a);
-  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(b) : "f"(r));
-  h = __uint_as_float(a);
-  l = __uint_as_float(b);
+// The tensor core reads an fp32 word as tf32 by dropping its low 13 mantissa
+// bits, so the staged fp32 tile already IS hi = trunc_tf32(x); only the
+// remainder lo = rna_tf32(x - hi) (x - hi is exact) needs a tile of its own.
+// The dropped lo*lo term is below 2^-20 |a b| (tests/test_gemm_gpu.py: error
+// relative to sum |a||b| < 2e-6, against ~1e-3 for one TF32 product).
+__device__ __forceinline__ float tf32_lo(float v) {
+  const float r = v - __uint_as_float(__float_as_uint(v) & 0xFFFFE000u);
+  uint32_t l;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(l) : "f"(r));
+  return __uint_as_float(l);
 }
 
 // the MLP's batch reductions (reading R18): db1[u] = sum_b dz1[b][u],
@@ -174,17 +178,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     float4* blo = reinterpret_cast<float4*>(sbase + (size_t)s * kStage + 2 * kATile + kBTile);
 #pragma unroll
     for (int q = threadIdx.x; q < (int)(kATile / 16); q += kGemmThreads) {
-      float4 v = a32[q], h, l;
-      split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y); split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
-      a32[q] = h;
-      alo[q] = l;
+      const float4 v = a32[q];
+      alo[q] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
     }
 #pragma unroll
     for (int q = threadIdx.x; q < (int)(kBTile / 16); q += kGemmThreads) {
-      float4 v = b32[q], h, l;
-      split_tf32(v.x, h.x, l.x); split_tf32(v.y, h.y, l.y); split_tf32(v.z, h.z, l.z); split_tf32(v.w, h.w, l.w);
-      b32[q] = h;
-      blo[q] = l;
+      const float4 v = b32[q];
+      blo[q] = make_float4(tf32_lo(v.x), tf32_lo(v.y), tf32_lo(v.z), tf32_lo(v.w));
     }
     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");   // generic writes -> tensor-core reads
     __syncthreads();
@@ -214,11 +214,14 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   // ------------------------------------------------------------------ epilogue
   mbar_wait(&accum, 0u);
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-  float* crow = C + (long long)blockIdx.z * split_stride + (long long)(m0 + warp * 32 + lane) * ldc + n0;
+  // warp w reads TMEM lanes 32 (w % 4) .. + 31 (its quadrant); warps w and w + 4 take alternate
+  // 32-column chunks
+  const int quad = warp & 3;
+  float* crow = C + (long long)blockIdx.z * split_stride + (long long)(m0 + quad * 32 + lane) * ldc + n0;
 #pragma unroll 1
-  for (int c = 0; c < BN / 32; ++c) {
+  for (int c = warp >> 2; c < BN / 32; c += 2) {
     uint32_t v[32];
-    const uint32_t taddr = tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(c * 32);
+    const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32);
     asm volatile(
         "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0, %1, %2, %3, %4, %5, %6, %7, %8, %9, %10, %11, %12, "
         "%13, %14, %15, %16, %17, %18, %19, %20, %21, %22, %23, %24, %25, %26, %27, %28, %29, %30, %31}, [%32];"

@@ -123,15 +123,20 @@ __global__ void __launch_bounds__(kLinThreads) k_linear_grad(int kind, const flo
 // phase 2 splits the M samples into 4 quarters per float4 column group and
 // adds the quarters in a fixed order (deterministic).
 constexpr int kLinThreadsV = 1024;
-__global__ void __launch_bounds__(kLinThreadsV) k_linear_grad_v(int kind, const float* __restrict__ A,
-                                                                const float* __restrict__ b, int S,
-                                                                const int* __restrict__ idx_in, int M,
-                                                                uint2 key, unsigned long long k,
-                                                                const float* __restrict__ xhat,
-                                                                float* __restrict__ g, long long d) {
-  __shared__ float coef[kMaxM];
-  __shared__ int sidx[kMaxM];
-  __shared__ float4 quarter[3][256];
+struct LinSmem {
+  float coef[kMaxM];
+  int sidx[kMaxM];
+  float4 quarter[3][256];
+};
+
+__device__ __forceinline__ void linear_grad_v_body(LinSmem& sm, int kind, const float* __restrict__ A,
+                                                   const float* __restrict__ b, int S,
+                                                   const int* __restrict__ idx_in, int M, uint2 key,
+                                                   unsigned long long k, const float* __restrict__ xhat,
+                                                   float* __restrict__ g, long long d) {
+  float* coef = sm.coef;
+  int* sidx = sm.sidx;
+  float4 (*quarter)[256] = sm.quarter;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
   const long long d4 = d >> 2;
   const float4* x4 = reinterpret_cast<const float4*>(xhat);
@@ -184,6 +189,48 @@ __global__ void __launch_bounds__(kLinThreadsV) k_linear_grad_v(int kind, const 
       reinterpret_cast<float4*>(g)[c] = acc;
     }
     __syncthreads();
+  }
+}
+
+__global__ void __launch_bounds__(kLinThreadsV) k_linear_grad_v(int kind, const float* __restrict__ A,
+                                                                const float* __restrict__ b, int S,
+                                                                const int* __restrict__ idx_in, int M,
+                                                                uint2 key, unsigned long long k,
+                                                                const float* __restrict__ xhat,
+                                                                float* __restrict__ g, long long d) {
+  __shared__ LinSmem sm;
+  linear_grad_v_body(sm, kind, A, b, S, idx_in, M, key, k, xhat, g, d);
+}
+
+// Config 1 in ONE launch per event (latency-bound): the lsq / logreg
+// gradients whose stale read point is X_t (the reads due before event t)
+// read their rows first, then -- after a CTA barrier -- event t itself runs
+// (the pair average and update, Alg. 1 steps 4-6).  The same code as the
+// standalone gradient and event kernels, so the results are identical.
+__global__ void __launch_bounds__(kLinThreadsV) k_lin_step(LinStepParams p) {
+  __shared__ LinSmem sm;
+  for (int r = 0; r < p.nreads; ++r)
+    linear_grad_v_body(sm, p.kind, p.A, p.b, p.S, p.reads[r].idx, p.M, p.key, p.reads[r].k, p.reads[r].x,
+                       p.reads[r].g, p.d);
+  __syncthreads();
+  if (!p.xi) return;
+  float4* xi4 = reinterpret_cast<float4*>(p.xi);
+  float4* xj4 = reinterpret_cast<float4*>(p.xj);
+  const float4* g4 = reinterpret_cast<const float4*>(p.g);
+  const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (long long c = threadIdx.x; c < p.n4; c += blockDim.x) {
+    float4 a = xi4[c], bb = p.xj ? xj4[c] : z;
+    const float4 gg = p.g ? g4[c] : z;
+    const uint32_t c0 = (uint32_t)(c * 4);
+    if (p.xj) {
+      if (!p.g) update4<true, kGradNone>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+      else if (p.ff) update4<true, kGradExternal, true>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+      else update4<true, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+      xj4[c] = bb;
+    } else if (p.g) {
+      update4<false, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+    }
+    xi4[c] = a;
   }
 }
 
@@ -570,6 +617,12 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
     k_linear_grad_v<<<1, kLinThreadsV, 0, s>>>(kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
   else
     k_linear_grad<<<1, kLinThreads, 0, s>>>(kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_lin_step(const LinStepParams& p, cudaStream_t s) {
+  if (p.M > kMaxM || p.d % 4 || p.nreads > kLinStepReads) return cudaErrorInvalidValue;
+  k_lin_step<<<1, kLinThreadsV, 0, s>>>(p);
   return cudaGetLastError();
 }
 

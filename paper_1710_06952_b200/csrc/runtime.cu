@@ -547,7 +547,40 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   if (c->model == ADPSGD_MODEL_MLP && need_slots) ST(ensure_mlp_scratch(c, ns));
   DagState dag(c->n, slots);
   if (ns > 1) ST(dag_fork(c, s, ns));
-  for (int64_t e = 0; e < K; ++e) {
+  // config 1 (lsq / logreg, one lane): the gradients read at X_e and event e share one launch
+  const bool fuse_lin = (c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG) && ns == 1 && !any_comp &&
+                        c->d % 4 == 0 && c->M <= 1024;
+  for (int64_t e = 0; e < K && fuse_lin; ++e) {
+    LinStepParams lp{};
+    lp.kind = (int)c->model; lp.S = c->S; lp.M = c->M; lp.A = c->dA; lp.b = c->db; lp.key = c->seed2();
+    lp.gamma = c->gamma; lp.d = c->d; lp.n4 = c->n4;
+    for (int64_t kp : reads[e]) {
+      if (lp.nreads == kLinStepReads) {                      // more reads at one point than fit: reads only
+        CU(launch_lin_step(lp, s));
+        ++c->launches;
+        lp.nreads = 0;
+      }
+      LinRead& r = lp.reads[lp.nreads++];
+      const int i = ev[kp].i;
+      r.x = c->row(i);
+      r.g = c->gslots + (long long)(kp % slots) * c->d_pad;
+      r.idx = bidx ? c->d_batch + kp * c->M : nullptr;
+      r.k = (ev[kp].flags & ADPSGD_EV_FLUSH_FIRST) ? read_key(k0 + kp - ev[kp].tau, i) : k0 + kp;
+    }
+    const int i = ev[e].i, j = ev[e].j;
+    const bool grad = !(ev[e].flags & ADPSGD_EV_NO_GRAD);
+    if (j >= 0 || grad) {
+      lp.xi = c->row(i);
+      lp.xj = j >= 0 ? c->row(j) : nullptr;
+      lp.g = grad ? c->gslots + (long long)(e % slots) * c->d_pad : nullptr;
+      lp.ff = grad && (ev[e].flags & ADPSGD_EV_FLUSH_FIRST) ? 1 : 0;
+    }
+    if (lp.nreads || lp.xi) {
+      CU(launch_lin_step(lp, s));
+      ++c->launches;
+    }
+  }
+  for (int64_t e = 0; e < K && !fuse_lin; ++e) {
     for (int64_t kp : reads[e]) {     // stale reads that happen before event e
       const int i = ev[kp].i;
       const int lane = ns > 1 ? i % ns : 0;
