@@ -553,43 +553,48 @@ def main():
         n5 = 128 if 128 // world <= 128 and 128 % world == 0 else 16 * world   # BASELINE configs[4]: n = 128
         e5, r5 = synth.ring(n5)
         st5 = synth.stragglers(n5, seed=99, slow_worker=0, slow=10.0, hetero=True)
-        c5 = make_ctx(st5, n5, e5, r5)
-        U5, reps = 8 * n5, 3
-        c5.run(U5, stream)
-        torch.cuda.synchronize()
-        c5.sync()
-        barrier()
-        s50 = c5.stats()
-        ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        ta.record(stream)
-        for _ in range(reps):
+
+        def config5(tc_ns, U5, R5):
+            """AD-PSGD vs AllReduce-SGD updates/s at n5 workers, heterogeneous stragglers"""
+            c5 = make_ctx(st5, n5, e5, r5, compute_ns=tc_ns)
             c5.run(U5, stream)
-        tb.record(stream)
-        torch.cuda.synchronize()
-        c5.sync()
-        barrier()
-        sec5 = maxr(ta.elapsed_time(tb)) / 1e3
-        s51 = c5.stats()
-        c5.allreduce_reset()
-        c5.allreduce_sgd(2, stream)
-        torch.cuda.synchronize()
-        barrier()
-        R5 = 8
-        ta.record(stream)
-        c5.allreduce_sgd(R5, stream)
-        tb.record(stream)
-        torch.cuda.synchronize()
-        sec5ar = maxr(ta.elapsed_time(tb)) / 1e3
-        c5.destroy()
-        barrier()
-        up5 = sumr(s51["local_events"] - s50["local_events"]) / sec5
-        extras["config5"] = {
-            "workload": f"n={n5} ({n5 // world}/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, "
-                        f"t_c={a.compute_us}us",
-            "adpsgd_updates_per_s": up5,
-            "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
-            "allreduce_updates_per_s": R5 * n5 / sec5ar,
-            "adpsgd_vs_allreduce_updates_ratio": up5 / (R5 * n5 / sec5ar)}
+            torch.cuda.synchronize()
+            c5.sync()
+            barrier()
+            s50 = c5.stats()
+            ta, tb = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            ta.record(stream)
+            for _ in range(3):
+                c5.run(U5, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            c5.sync()
+            barrier()
+            sec5 = maxr(ta.elapsed_time(tb)) / 1e3
+            s51 = c5.stats()
+            c5.allreduce_reset()
+            c5.allreduce_sgd(2, stream)
+            torch.cuda.synchronize()
+            barrier()
+            ta.record(stream)
+            c5.allreduce_sgd(R5, stream)
+            tb.record(stream)
+            torch.cuda.synchronize()
+            sec5ar = maxr(ta.elapsed_time(tb)) / 1e3
+            c5.destroy()
+            barrier()
+            up5 = sumr(s51["local_events"] - s50["local_events"]) / sec5
+            return {"adpsgd_updates_per_s": up5,
+                    "adpsgd_gossip_steps_per_s": sumr(s51["local_pair_events"] - s50["local_pair_events"]) / sec5,
+                    "allreduce_updates_per_s": R5 * n5 / sec5ar,
+                    "adpsgd_vs_allreduce_updates_ratio": up5 / (R5 * n5 / sec5ar)}
+
+        extras["config5"] = dict(config5(cns, 8 * n5, 8), workload=(
+            f"n={n5} ({n5 // world}/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, t_c={a.compute_us}us"))
+        # the same at t_c = 1 ms: the workers' compute (not HBM) sets the pace, as in the paper's
+        # GPU clusters -- AllReduce-SGD then waits for the slowest worker every round (P:232-241)
+        extras["config5_tc_1ms"] = dict(config5(1_000_000, 2 * n5, 2), workload=(
+            f"n={n5} ({n5 // world}/GPU) ring, d={d}, s_w = 10^U[0,1] + worker 0 x10, t_c=1ms"))
         def three_way(c4, Rb):
             """updates/s of AD-PSGD (free-running), AllReduce-SGD and D-PSGD on one context"""
             c4.run(U, stream)

@@ -327,25 +327,26 @@ __host__ __device__ __forceinline__ unsigned int claim_nc(unsigned long long w) 
 constexpr unsigned int kClaimSeqMask = 0xFFFFu;
 __host__ __device__ __forceinline__ unsigned int claim_idx(unsigned long long w) { return (unsigned int)w; }
 
-template <int kChunk>
+// chunk = ceil(n / nc) tiles (nc from the claim word, so every claimer agrees)
 struct TileClaim {
   unsigned long long* ctr;
-  unsigned int n, stride, off;
+  unsigned int n, stride, off, chunk;
   unsigned int c, end, ahead;      // current chunk's next / end c; chunk claimed ahead
   bool out;
-  // first = the chunk index the join's claim returned
+  // first = the chunk index the join's claim returned, nc = the word's chunk count
   __device__ __forceinline__ void init(unsigned long long* ctr_, unsigned int n_, unsigned int stride_,
-                                       unsigned int off_, unsigned int first) {
+                                       unsigned int off_, unsigned int first, unsigned int nc) {
     ctr = ctr_; n = n_; stride = stride_; off = off_; out = false;
-    c = first * kChunk;
-    end = c + kChunk < n ? c + kChunk : n;
+    chunk = (n_ + nc - 1) / nc;
+    c = first * chunk;
+    end = c + chunk < n ? c + chunk : n;
     ahead = claim_idx(atomicAdd(ctr, 1ull));
   }
   __device__ __forceinline__ int next() {           // thread 0 only; -1 once exhausted
     if (c >= end) {
-      if (out || ahead * kChunk >= n) { out = true; return -1; }
-      c = ahead * kChunk;
-      end = c + kChunk < n ? c + kChunk : n;
+      if (out || ahead * chunk >= n) { out = true; return -1; }
+      c = ahead * chunk;
+      end = c + chunk < n ? c + chunk : n;
       ahead = claim_idx(atomicAdd(ctr, 1ull));      // used when this chunk is done
     }
     return (int)(c++ * stride + off);
@@ -377,8 +378,8 @@ struct Stager {
   // stage use and issues its copies kStages uses ahead; every thread reads the
   // stage's tile from stile[] (written before a CTA barrier the readers pass).
   // body(tile, a[], b[]) consumes one staged tile.  Returns the tiles done.
-  template <int kClaimChunk, class Body>
-  __device__ __forceinline__ unsigned int drive(TileClaim<kClaimChunk>& cl, const float4* s0, const float4* s1,
+  template <class Body>
+  __device__ __forceinline__ unsigned int drive(TileClaim& cl, const float4* s0, const float4* s1,
                                                 long long hi, Body&& body) {
     if (threadIdx.x == 0) {
       fence_proxy_async();

@@ -48,13 +48,17 @@ constexpr int kPickGuest = 1 << 20;     // a peer's cooperative event posted in 
 constexpr int kTile4 = 1536;            // float4 per stream per stage (24 KB); round-1 A/B: 1536x2 stages
                                         // 0.869-0.871 of the HBM peak vs 1024x3 0.863-0.867, 512x6 0.82
 constexpr int kStages = 2;
-constexpr int kClaimChunk = 8;          // tiles per claimed chunk (A/B at N=1: 4 -> 0.907, 8 -> 0.930, 16 -> 0.928 of peak)
+constexpr int kClaimChunk = 8;          // tiles per claimed chunk, at most (A/B at N=1: 4 -> 0.907, 8 -> 0.930,
+                                        // 16 -> 0.928 of peak); small events use smaller chunks so that up to
+                                        // one chunk per CTA spreads them over the whole grid
 constexpr bool kRotate = true;          // CTA b scans slots from b mod L (else every CTA from slot 0)
-constexpr int kCrossDiv = 4;            // CTAs per GPU on one cross-GPU event: grid / 4 (round-1 A/B at
+constexpr int kCrossDiv = 8;            // CTAs per GPU on one cross-GPU event: grid / 8 (round-2 A/B, claim engine,
+                                        // bench --no-extras: 2 / 4 / 8 -> N=2 0.835 / 0.864 / 0.890, N=4 0.815 /
+                                        // 0.849 / 0.881 of the HBM peak; round-1 static engine at
                                         // N=2: 1 -> 14.17k, 2 -> 14.44k, 4 -> 14.58k, 8 -> 14.05k steps/s)
 constexpr size_t kTmaSmem = (size_t)kStages * 2 * kTile4 * sizeof(float4) + kStages * sizeof(uint64_t);
 using EngineStager = Stager<kTile4, kStages>;
-using Claim = TileClaim<kClaimChunk>;
+using Claim = TileClaim;
 constexpr int kPer = kTile4 / 512;
 
 struct SmemSlot {                  // tid 0 copies the joined event here for the CTA
@@ -73,6 +77,7 @@ struct SmemSlot {                  // tid 0 copies the joined event here for the
   unsigned long long* ctr;
   unsigned int n, stride, off;
   unsigned int first;              // the chunk the join's claim returned
+  unsigned int nc;                 // the claim word's chunk count
   unsigned int* rem;               // the initiator slot's remaining tiles (peer memory for a guest)
   int guest;                       // a peer's cooperative event (our half)
   int slot;                        // local slot (own events) or mailbox index (guest)
@@ -115,6 +120,13 @@ __device__ __forceinline__ bool take_ticket(const EngineParams& p, unsigned long
 
 // Make the slot's event (fields already written) visible as running: fresh
 // claim word (new seq, chunk count), remaining tiles, then the tag.
+// chunks a share of `share` tiles is dealt in: chunk = clamp(T / grid, 1, kClaimChunk)
+__device__ __forceinline__ unsigned int share_chunks(const EngineParams& p, unsigned int share) {
+  const unsigned int per = event_tiles(p) / gridDim.x;
+  const unsigned int chunk = per < 1u ? 1u : (per > (unsigned)kClaimChunk ? (unsigned)kClaimChunk : per);
+  return (share + chunk - 1) / chunk;
+}
+
 __device__ void publish_running(const EngineParams& p, Slot* sl, unsigned int seq) {
   const unsigned int T = event_tiles(p);
   const unsigned int share = sl->coop ? (T + 1u) / 2u : T;
@@ -123,7 +135,7 @@ __device__ void publish_running(const EngineParams& p, Slot* sl, unsigned int se
   sl->commit_ready = 0u;
   sl->rem = T;
   __threadfence();                                   // fields before the claim word (a claim reads them)
-  *(volatile unsigned long long*)&sl->next = claim_word(seq + 1, (share + kClaimChunk - 1) / kClaimChunk);
+  *(volatile unsigned long long*)&sl->next = claim_word(seq + 1, share_chunks(p, share));
   __threadfence_system();                            // ... and before the tag (a guest reads them)
   st_release_gpu(&sl->tag, tag_of(seq + 1, kStateRunning));
 }
@@ -141,7 +153,7 @@ __device__ void post_guest(Slot* sl, const EngineParams& p, int w, int j) {
   *(volatile unsigned int*)&cj->guest_nwork = 0u;
   __threadfence_system();                             // guest_i before the claim word
   *(volatile unsigned long long*)&cj->guest_next =
-      claim_word(sl->gseq, (event_tiles(p) / 2u + kClaimChunk - 1) / kClaimChunk);
+      claim_word(sl->gseq, share_chunks(p, event_tiles(p) / 2u));
   __threadfence_system();
   st_release_sys(&cj->guest_tag, tag_of(sl->gseq, kStateRunning));
 }
@@ -590,6 +602,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         s_ev.stride = coop ? 2u : 1u;
         s_ev.off = 0u;
         s_ev.first = claim_idx(w);
+        s_ev.nc = claim_nc(w);
         s_ev.rem = &sl->rem;
         s_ev.guest = 0;
         s_ev.slot = s;
@@ -632,6 +645,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
           s_ev.stride = 2u;
           s_ev.off = 1u;
           s_ev.first = claim_idx(w);
+          s_ev.nc = claim_nc(w);
           s_ev.rem = &sa->rem;
           s_ev.guest = 1;
           s_ev.slot = l;
@@ -658,7 +672,7 @@ __global__ void __launch_bounds__(kEngineThreads, 2) k_engine(const __grid_const
         else if (now - last_progress > p.watchdog_ns) { latch_error(p, 7u); pick = kExit; }
       } else if (pick != kExit) {
         last_progress = globaltimer();
-        cl.init(s_ev.ctr, s_ev.n, s_ev.stride, s_ev.off, s_ev.first);
+        cl.init(s_ev.ctr, s_ev.n, s_ev.stride, s_ev.off, s_ev.first, s_ev.nc);
       }
       s_pick = pick;
     }
