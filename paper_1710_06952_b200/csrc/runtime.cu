@@ -484,7 +484,6 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
       return fail(ADPSGD_E_UNSUPPORTED, "replay with gradients needs a built-in model");
   unsigned long long k0;
   ST(host_ticket(c, &k0));
-  const int slots = c->T + 1;
   // App. A compensation (reading R20): comp_src[e] = worker i's previous
   // gradient event when it was still buffered at e's read point.  Its gradient
   // is in slot comp_src mod (T+1) at that point: it was computed at its own
@@ -511,6 +510,19 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
       last[i] = e;
     }
   }
+  // Events on disjoint workers commute (every coordinate sees the same op
+  // sequence), so large-d / heavy-gradient replays run as a DAG over a pool of
+  // streams: each op waits (cudaEvent) only for the last writer of the rows it
+  // reads, the readers of the rows it writes, and its gradient slot.  The
+  // result is bitwise the serial one.
+  const int ns =
+      (!any_comp && (c->model == ADPSGD_MODEL_MLP || c->d >= (1 << 16))) ? std::min(kPoolStreams, c->n) : 1;
+  // gradient slots: event e's gradient lives in slot e mod `slots` from its read
+  // to its event; T + 1 suffice in stream order, and in the DAG more slots let
+  // more gradients be in flight (a slot's next read waits for its previous
+  // event): up to 32, within 1 GB
+  const int slots = ns > 1 ? std::max(c->T + 1, (int)std::min<long long>(32, (1LL << 30) / (4 * c->d_pad)))
+                           : c->T + 1;
   bool need_slots = false;
   std::vector<std::vector<int64_t>> reads(K);
   for (int64_t e = 0; e < K; ++e) {
@@ -536,13 +548,6 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
       if (bidx[t] < 0 || bidx[t] >= c->S) return fail(ADPSGD_E_INVALID, "batch index out of range");
     CU(cudaMemcpyAsync(c->d_batch, bidx, sizeof(int) * need, cudaMemcpyHostToDevice, s));
   }
-  // Events on disjoint workers commute (every coordinate sees the same op
-  // sequence), so large-d / heavy-gradient replays run as a DAG over a pool of
-  // streams: each op waits (cudaEvent) only for the last writer of the rows it
-  // reads, the readers of the rows it writes, and its gradient slot.  The
-  // result is bitwise the serial one.
-  const int ns =
-      (!any_comp && (c->model == ADPSGD_MODEL_MLP || c->d >= (1 << 16))) ? std::min(kPoolStreams, c->n) : 1;
   ST(ensure_pool(c, ns));
   if (c->model == ADPSGD_MODEL_MLP && need_slots) ST(ensure_mlp_scratch(c, ns));
   DagState dag(c->n, slots);
