@@ -712,7 +712,7 @@ adpsgd_status engine_launch(adpsgd_ctx* c, int mode, unsigned long long target, 
   }
   p.coop = (c->world > 1 && coop && !(mode == 0 && c->wait_free)) ? 1 : 0;
   // the grid is fixed at init (and checked equal across ranks at import: the
-  // per-GPU cap on a cross event's CTAs is grid / 4 on both sides)
+  // per-GPU cap on a cross event's CTAs is grid / 8 on both sides)
   if (c->engine_grid < 1) return fail(ADPSGD_E_CUDA, "engine kernel cannot be resident");
   CU(cudaMemsetAsync(&c->gctl->abort_flag, 0, sizeof(unsigned int), s));
   // processes: a cooperative launch guarantees co-residency of the grid; in-process
