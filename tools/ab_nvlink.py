@@ -1,4 +1,5 @@
-"""A/B of the cross-GPU event protocol on an all-NVLink schedule (torchrun, N GPUs).
+"""NVLink throughput of the engine on an all-NVLink schedule (torchrun, N GPUs); set
+ADPSGD_LIB to an A/B build from tools/ab_build.py to compare engine constants.
 
   python -m torch.distributed.run --nproc-per-node 2 --master-addr 127.0.0.1 tools/ab_nvlink.py
 Interleave placement on a ring: every edge joins two GPUs.  Pure gossip (W_k
@@ -20,7 +21,8 @@ import paper_1710_06952_b200 as P
 ap = argparse.ArgumentParser()
 ap.add_argument("--d", type=int, default=25_600_000)
 ap.add_argument("--events", type=int, default=128)
-ap.add_argument("--variants", default="0,3,1")
+ap.add_argument("--libs", default="", help="comma-separated ADPSGD_LIB builds to compare (tools/ab_build.py); "
+                                           "empty = the in-tree library")
 ap.add_argument("--model", default="none")
 ap.add_argument("--mode", default="replay", choices=["replay", "run"])
 ap.add_argument("--wpg", type=int, default=8, help="workers per GPU")
@@ -34,12 +36,12 @@ n = a.wpg * world
 e, r = synth.ring(n)
 quad = a.model == "quad"
 ev, _ = synth.schedule_iid(n, e, K=a.events, seed=2, no_grad=not quad)
-for v in [int(x) for x in a.variants.split(",")]:
+for v in [0]:
     xor = a.placement == "xor"
     ctx = P.Context(e, n, a.d, role=r, rank=rank, world_size=world, device=local, placement=2 if xor else 1,
                     worker_rank=synth.placement_xor(n, world) if xor else None, engine_coop=None if a.coop == 0 else a.coop > 0,
                     model=P.MODEL_QUADRATIC if quad else P.MODEL_NONE, gamma=0.01, batch_M=32,
-                    quad_keys=(1, 2), quad_noise_s=0.5, engine_variant=v)
+                    quad_keys=(1, 2), quad_noise_s=0.5)
     s = torch.cuda.Stream()
     go = (lambda: ctx.replay(ev, flags=P.REPLAY_ENGINE, stream=s)) if a.mode == "replay" else \
         (lambda: ctx.run(len(ev), stream=s))

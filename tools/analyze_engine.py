@@ -19,7 +19,7 @@ import paper_1710_06952_b200 as P
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--d", type=int, default=25_600_000)
-ap.add_argument("--configs", default="8:50:0,8:0:0,16:50:0,8:50:1")   # n:compute_us:variant
+ap.add_argument("--configs", default="8:50:0,8:0:0,16:50:0")   # n:compute_us:0[:none]
 ap.add_argument("--updates", type=int, default=512)
 a = ap.parse_args()
 
@@ -31,7 +31,7 @@ for cfgs in a.configs.split(","):
     dk, nk = synth.quad_keys(5)
     ctx = P.Context(e, n, a.d, role=r, model=model, gamma=0.01, batch_M=32, quad_keys=(dk, nk),
                     quad_noise_s=0.5, straggler=synth.stragglers(n), compute_ns=int(cus * 1000),
-                    engine_variant=var, log_capacity=1 << 16)
+                    log_capacity=1 << 16)
     ctx.run(64)
     ctx.sync()
     k0 = ctx.ticket()
