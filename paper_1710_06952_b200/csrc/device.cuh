@@ -9,6 +9,7 @@
 // built without --use_fast_math, so no FTZ/DAZ.
 #pragma once
 #include <cstdint>
+#include <utility>
 #include <cuda_runtime.h>
 
 namespace adp {
@@ -151,6 +152,32 @@ __device__ __forceinline__ float quad_grad(float xhat, uint32_t c, uint32_t data
   const float noise = __fmul_rn(s, v);
   const float det = __fmul_rn(__fmul_rn(Mf, h), __fsub_rn(xhat, xs));
   return __fadd_rn(det, noise);
+}
+
+// ------------------------------------------- programmatic dependent launch ----
+// A kernel launched with programmatic stream serialization (launch_pdl) may start
+// while its predecessor in the stream is still running: it does its independent
+// setup, then waits here for the predecessor to complete and its memory to be
+// visible.  Without that launch attribute the wait is a no-op.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+// let the stream's next (PDL-launched) kernel start its setup now
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+constexpr bool kUsePdl = true;
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = kUsePdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
 // --------------------------------------------------------- memory helpers ----

@@ -123,6 +123,7 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   float* __restrict__ C, int ldc, int kb_per_split, long long split_stride, int m_tiles,
                   const __grid_constant__ GemmTail tail) {
   if ((int)blockIdx.y >= m_tiles) {                          // tail rows of the grid
+    pdl_wait();
     mlp_reduce_task(tail, (int)(blockIdx.y - m_tiles) * gridDim.x + blockIdx.x,
                     (int)(gridDim.y - m_tiles) * gridDim.x);
     return;
@@ -164,6 +165,8 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
     tma_load_2d(st, &tmA, kc, m0, &full[s]);
     tma_load_2d(st + 2 * kATile, &tmB, kc, n0, &full[s]);
   };
+  pdl_wait();                                                // operands written by the predecessor
+  pdl_trigger();
   if (threadIdx.x == 0)
     for (int kb = 0; kb < STAGES && kb < kb_per_split; ++kb) load(kb);
 
@@ -300,18 +303,18 @@ cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float
     constexpr int S = 3;                                    // 3 x 64 KB stages
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 128 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<128, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gemm_tf32x3<128, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<128, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
   } else if (bn == 96) {
     constexpr int S = 3;                                    // 3 x 56 KB stages: 128 x 96 tiles
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 96 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<96, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gemm_tf32x3<96, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<96, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
   } else {
     constexpr int S = 3;                                    // 3 x 48 KB stages (config-3 replay A/B: 2 / 3 / 4
                                                             // stages 30.3-31.3k / 31.1k / 29.1k updates/s)
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 64 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<64, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    k_gemm_tf32x3<64, S><<<grid, kGemmThreads, smem, s>>>(A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<64, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
   }
   return cudaGetLastError();
 }

@@ -24,6 +24,8 @@ __global__ void k_mlp_gather(const float* __restrict__ X, int I, const int* __re
   __shared__ float t[32][33];
   __shared__ int rows[32];
   const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
+  pdl_wait();                                   // the previous gradient's GEMM2 still reads xbt
+  pdl_trigger();
   if (threadIdx.y == 0) {
     const int m = r0 + threadIdx.x;
     int v;
@@ -62,6 +64,8 @@ __global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p,
   const int b = blockIdx.x, u = threadIdx.x;
   const int warp = u >> 5, lane = u & 31, nw = blockDim.x >> 5;
   const float* W2 = w + off_W2;
+  pdl_wait();                                   // GEMM1's split-K planes
+  pdl_trigger();
   float s = 0.0f;
 #pragma unroll 8
   for (int p = 0; p < splits; ++p) s += z1p[((long long)p * M + b) * H + u];
@@ -198,11 +202,15 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   CUtensorMap w1;                                             // W1 [H x I], the first H*I floats of w
   cudaError_t e = make_tmap_k_major(&w1, w, H, I, 64);
   if (e != cudaSuccess) return e;
-  k_mlp_gather<<<dim3(I / 32, M / 32), dim3(32, 8), 0, s>>>(X, I, idx_in, batch_key, k, S, M, wk.idx, wk.xb,
-                                                            wk.xbt);
+  // the chain gather -> GEMM1 -> mid -> GEMM2 uses programmatic dependent launch: each kernel's
+  // setup (GEMM: barriers, TMEM, tensor-map prefetch) overlaps its predecessor's tail
+  if ((e = launch_pdl(k_mlp_gather, dim3(I / 32, M / 32), dim3(32, 8), 0, s, X, I, idx_in, batch_key, k, S, M,
+                      wk.idx, wk.xb, wk.xbt)) != cudaSuccess)
+    return e;
   if ((e = launch_gemm_tf32x3(wk.x_b, w1, wk.z1p, M, H, I, wk.splits, 64, nullptr, 0, s)) != cudaSuccess) return e;
-  k_mlp_mid<<<M, H, 0, s>>>(wk.z1p, wk.splits, M, H, O, w, off_b1, off_W2, off_b2, y, wk.idx, wk.hbuf, wk.dz1,
-                             wk.dz2, wk.dzt);
+  if ((e = launch_pdl(k_mlp_mid, dim3(M), dim3(H), 0, s, (const float*)wk.z1p, wk.splits, M, H, O, w, off_b1,
+                      off_W2, off_b2, y, (const int*)wk.idx, wk.hbuf, wk.dz1, wk.dz2, wk.dzt)) != cudaSuccess)
+    return e;
   // the batch reductions on the side stream, beside GEMM2 (which leaves SMs free)
   if ((e = cudaEventRecord(wk.fork, s)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(wk.side, wk.fork, 0)) != cudaSuccess) return e;

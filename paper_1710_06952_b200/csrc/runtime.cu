@@ -521,7 +521,8 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   // to its event; T + 1 suffice in stream order, and in the DAG more slots let
   // more gradients be in flight (a slot's next read waits for its previous
   // event): up to 32, within 1 GB
-  const int slots = ns > 1 ? std::max(c->T + 1, (int)std::min<long long>(32, (1LL << 30) / (4 * c->d_pad)))
+  constexpr int kDagSlots = 32;
+  const int slots = ns > 1 ? std::max(c->T + 1, (int)std::min<long long>(kDagSlots, (1LL << 30) / (4 * c->d_pad)))
                            : c->T + 1;
   bool need_slots = false;
   std::vector<std::vector<int64_t>> reads(K);
