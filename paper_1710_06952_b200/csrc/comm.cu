@@ -6,6 +6,7 @@
 #include <map>
 #include <memory>
 #include <mutex>
+#include <iterator>
 #include <set>
 
 #include <nccl.h>
@@ -122,6 +123,8 @@ std::map<std::string, std::weak_ptr<LocalGroup>> g_groups;
 
 std::shared_ptr<LocalGroup> lookup_group(const std::string& id, int size) {
   std::lock_guard<std::mutex> lk(g_reg_mu);
+  for (auto e = g_groups.begin(); e != g_groups.end();)        // forget groups whose ranks are gone
+    e = e->second.expired() ? g_groups.erase(e) : std::next(e);
   auto it = g_groups.find(id);
   if (it != g_groups.end())
     if (auto g = it->second.lock()) return g->size == size ? g : nullptr;
