@@ -20,9 +20,7 @@
 //   all threads  : write lo of the staged tiles, fence.proxy.async, barrier
 //   thread 32    : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8)
 // then all 8 warps run the epilogue (tcgen05.ld 32x32b -> registers -> global).
-// Split-K: blockIdx.z takes a K range and writes its own partial plane.  Grid
-// rows beyond M / 128 run a caller-supplied tail task instead (the MLP's batch
-// reductions ride on the dW1 launch).
+// Split-K: blockIdx.z takes a K range and writes its own partial plane.
 #include <cuda.h>
 #include "internal.h"
 
@@ -80,54 +78,10 @@ __device__ __forceinline__ float tf32_lo(float v) {
   return __uint_as_float(l);
 }
 
-// the MLP's batch reductions (reading R18): db1[u] = sum_b dz1[b][u],
-// dW2[o][u] = sum_b dz2[b][o] h[b][u], db2[o] = sum_b dz2[b][o].  Four lanes per
-// output, each summing every 4th sample (independent loads in flight), combined
-// by shuffles in a fixed order: deterministic.
-__device__ void mlp_reduce_task(const GemmTail& t, int task, int ntask) {
-  const int M = t.M, H = t.H, O = t.O;
-  const long long n = (long long)H + (long long)O * H + O;
-  const int sub = threadIdx.x & 3;
-  const long long per = blockDim.x / 4;
-  for (long long q = (long long)task * per + (threadIdx.x >> 2); q - (threadIdx.x >> 2) < n;
-       q += (long long)ntask * per) {
-    float acc = 0.0f;
-    if (q < n) {
-      if (q < H) {
-#pragma unroll 8
-        for (int b = sub; b < M; b += 4) acc += t.dz1[(long long)b * H + q];
-      } else if (q < H + (long long)O * H) {
-        const long long r = q - H;
-        const int o = (int)(r / H), u = (int)(r % H);
-#pragma unroll 8
-        for (int b = sub; b < M; b += 4) acc = fmaf(t.dz2[(long long)b * O + o], t.h[(long long)b * H + u], acc);
-      } else {
-        const int o = (int)(q - H - (long long)O * H);
-#pragma unroll 8
-        for (int b = sub; b < M; b += 4) acc += t.dz2[(long long)b * O + o];
-      }
-    }
-    acc += __shfl_xor_sync(0xffffffffu, acc, 1);
-    acc += __shfl_xor_sync(0xffffffffu, acc, 2);
-    if (q < n && sub == 0) {
-      if (q < H) t.g[t.off_b1 + q] = acc;
-      else if (q < H + (long long)O * H) t.g[t.off_W2 + (q - H)] = acc;
-      else t.g[t.off_b2 + (q - H - (long long)O * H)] = acc;
-    }
-  }
-}
-
 template <int BN, int STAGES>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-                  float* __restrict__ C, int ldc, int kb_per_split, long long split_stride, int m_tiles,
-                  const __grid_constant__ GemmTail tail) {
-  if ((int)blockIdx.y >= m_tiles) {                          // tail rows of the grid
-    pdl_wait();
-    mlp_reduce_task(tail, (int)(blockIdx.y - m_tiles) * gridDim.x + blockIdx.x,
-                    (int)(gridDim.y - m_tiles) * gridDim.x);
-    return;
-  }
+                  float* __restrict__ C, int ldc, int kb_per_split, long long split_stride) {
   constexpr uint32_t kATile = kBM * 128, kBTile = BN * 128;  // fp32 tiles (the hi halves after the split)
   constexpr uint32_t kStage = 2 * kATile + 2 * kBTile;       // [A32|hi][A lo][B32|hi][B lo]
   extern __shared__ unsigned char smem_raw[];
@@ -291,30 +245,28 @@ cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long lon
 }
 
 // C (+ z * split_stride) = A . B^T over K range of split z; M % 128 == 0, N % BN == 0, K % (32 * splits) == 0.
-// tail (nullable): tail_rows extra grid rows run the MLP's batch reductions.
 cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float* C, int M, int N, int K, int splits,
-                               int bn, const GemmTail* tail, int tail_rows, cudaStream_t s) {
+                               int bn, cudaStream_t s) {
   if (M % kBM || K % (kBK * splits) || (bn != 64 && bn != 96 && bn != 128) || N % bn) return cudaErrorInvalidValue;
   const int kbps = K / kBK / splits;
   const long long sstride = (long long)M * N;
-  const GemmTail t = tail ? *tail : GemmTail{};
-  dim3 grid(N / bn, M / kBM + (tail ? tail_rows : 0), splits);
+  dim3 grid(N / bn, M / kBM, splits);
   if (bn == 128) {
     constexpr int S = 3;                                    // 3 x 64 KB stages
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 128 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<128, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(k_gemm_tf32x3<128, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<128, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride);
   } else if (bn == 96) {
     constexpr int S = 3;                                    // 3 x 56 KB stages: 128 x 96 tiles
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 96 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<96, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(k_gemm_tf32x3<96, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<96, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride);
   } else {
     constexpr int S = 3;                                    // 3 x 48 KB stages (config-3 replay A/B: 2 / 3 / 4
                                                             // stages 30.3-31.3k / 31.1k / 29.1k updates/s)
     const size_t smem = (size_t)S * (2 * kBM * 128 + 2 * 64 * 128) + 1024;
     cudaFuncSetAttribute(k_gemm_tf32x3<64, S>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    return launch_pdl(k_gemm_tf32x3<64, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride, M / kBM, t);
+    return launch_pdl(k_gemm_tf32x3<64, S>, grid, dim3(kGemmThreads), smem, s, A, B, C, N, kbps, sstride);
   }
   return cudaGetLastError();
 }

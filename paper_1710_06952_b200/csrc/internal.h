@@ -160,16 +160,10 @@ cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d,
 // 3xTF32 tcgen05 GEMM (gemm.cu): C = A . B^T, A [M x K], B [N x K] row-major fp32,
 // described by SWIZZLE_128B fp32 tensor maps (box 32 x 128 for A, 32 x bn for B);
 // the hi / lo split happens in shared memory
-struct GemmTail {                  // the MLP's batch reductions, run by extra grid rows
-  const float *h, *dz1, *dz2;
-  float* g;
-  long long off_b1, off_W2, off_b2;
-  int M, H, O;
-};
 cudaError_t make_tmap_k_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols, int box_rows);
 cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long long n, cudaStream_t s);
 cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float* C, int M, int N, int K, int splits,
-                               int bn, const GemmTail* tail, int tail_rows, cudaStream_t s);
+                               int bn, cudaStream_t s);
 
 // MLP (kind 5): tcgen05-backed gradient (mlp.cu), 5 launches:
 //   gather (+ batch indices) -> GEMM1 (split-K planes) -> per-sample mid -> GEMM2 || batch reductions

@@ -207,7 +207,7 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   if ((e = launch_pdl(k_mlp_gather, dim3(I / 32, M / 32), dim3(32, 8), 0, s, X, I, idx_in, batch_key, k, S, M,
                       wk.idx, wk.xb, wk.xbt)) != cudaSuccess)
     return e;
-  if ((e = launch_gemm_tf32x3(wk.x_b, w1, wk.z1p, M, H, I, wk.splits, 64, nullptr, 0, s)) != cudaSuccess) return e;
+  if ((e = launch_gemm_tf32x3(wk.x_b, w1, wk.z1p, M, H, I, wk.splits, 64, s)) != cudaSuccess) return e;
   if ((e = launch_pdl(k_mlp_mid, dim3(M), dim3(H), 0, s, (const float*)wk.z1p, wk.splits, M, H, O, w, off_b1,
                       off_W2, off_b2, y, (const int*)wk.idx, wk.hbuf, wk.dz1, wk.dz2, wk.dzt)) != cudaSuccess)
     return e;
@@ -218,7 +218,7 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   k_mlp_reduce<<<(unsigned)((nred * 32 + 255) / 256), 256, 0, wk.side>>>(wk.hbuf, wk.dz1, wk.dz2, M, H, O, g, off_b1,
                                                                           off_W2, off_b2);
   // dW1 in 128 x 96 tiles (I = 3072: 4 x 32 = 128 CTAs, one wave)
-  if ((e = launch_gemm_tf32x3(wk.dzt_m, wk.xbt_m, g, H, I, M, 1, I % 96 == 0 ? 96 : 64, nullptr, 0, s)) != cudaSuccess)
+  if ((e = launch_gemm_tf32x3(wk.dzt_m, wk.xbt_m, g, H, I, M, 1, I % 96 == 0 ? 96 : 64, s)) != cudaSuccess)
     return e;
   if ((e = cudaEventRecord(wk.join, wk.side)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(s, wk.join, 0)) != cudaSuccess) return e;

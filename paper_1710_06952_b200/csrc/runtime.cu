@@ -1991,7 +1991,7 @@ adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32
     adpsgd_status st = ADPSGD_OK;
     cudaError_t e = make_tmap_k_major(&ta, A, M, K, 128);
     if (e == cudaSuccess) e = make_tmap_k_major(&tb, B, N, K, bn);
-    if (e == cudaSuccess) e = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : C, M, N, K, splits, bn, nullptr, 0, nullptr);
+    if (e == cudaSuccess) e = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : C, M, N, K, splits, bn, nullptr);
     if (e == cudaSuccess && splits > 1) e = launch_sum_planes(part, C, splits, (long long)M * N, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) st = fail(ADPSGD_E_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
@@ -2019,7 +2019,7 @@ adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t 
     if (e == cudaSuccess) e = make_tmap_k_major(&ta, a, M, K, 128);
     if (e == cudaSuccess) e = make_tmap_k_major(&tb, b, N, K, bn);
     auto once = [&]() {
-      cudaError_t r = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : c, M, N, K, splits, bn, nullptr, 0, nullptr);
+      cudaError_t r = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : c, M, N, K, splits, bn, nullptr);
       if (r == cudaSuccess && splits > 1) r = launch_sum_planes(part, c, splits, (long long)M * N, nullptr);
       return r;
     };
