@@ -794,10 +794,14 @@ def main():
                             "free-running host-driven loop (super-learners with R=1), device Philox batches",
                 "updates_per_s": world * steps3 / sec3, "samples_per_s": world * steps3 * Mm / sec3}
         if world == 1:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
             extras["config1_lsq"] = config1_leg(P, synth, torch)
             extras["config2_gossip"] = config2_leg(P, synth, torch)
             extras["mlp_config3"] = mlp_leg(P, synth, torch)
-            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            # config 3 free-running: 8 workers as in-process ranks on this GPU, each its own
+            # host-driven AD-PSGD loop (the multi-rank protocol with local pointers)
+            import mlp_free_running_1gpu
+            extras["mlp_config3_free_running_1gpu"] = mlp_free_running_1gpu.run(8)
             import gemm_sweep
             extras["mlp_gemm_sweep"] = gemm_sweep.sweep(reps=10)
 
