@@ -26,6 +26,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# the config-3 free-running leg drives 8 in-process ranks: one hardware queue per stream
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 D_FULL = 25_600_000
 M_BATCH = 32
