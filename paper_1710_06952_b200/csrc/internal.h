@@ -160,20 +160,37 @@ cudaError_t launch_init_rows(float* X, int n_rows, long long d_pad, long long d,
 // 3xTF32 tcgen05 GEMM (gemm.cu): C = A . B^T, A [M x K], B [N x K] row-major fp32,
 // described by SWIZZLE_128B fp32 tensor maps (box 32 x 128 for A, 32 x bn for B);
 // the hi / lo split happens in shared memory
+struct GemmGather {                // gathered-operand / epilogue arguments (MLP GEMMs)
+  const float* x;                  // gathered rows: x + row * ld
+  long long ld;
+  const int* idx;                  // row of each batch sample (GEMM1: NULL -> Philox draw below)
+  int* idx_out;                    // GEMM1 publishes the batch indices here (may be NULL)
+  uint2 key;
+  unsigned long long k;
+  int S;
+  int cluster;                     // CTAs per cluster along z (split-K reduced in DSMEM), 1 = none
+  const float* bias;               // GEMM1 epilogue: h = tanh(z + bias)
+};
 cudaError_t make_tmap_k_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols, int box_rows);
+cudaError_t make_tmap_mn_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols);
 cudaError_t launch_sum_planes(const float* src, float* dst, int planes, long long n, cudaStream_t s);
 cudaError_t launch_gemm_tf32x3(const CUtensorMap& A, const CUtensorMap& B, float* C, int M, int N, int K, int splits,
-                               int bn, cudaStream_t s);
+                               int bn, cudaStream_t s, int cluster = 1);
+cudaError_t launch_mlp_gemm1(const CUtensorMap& B, const GemmGather& gg, float* h, int M, int N, int K, int splits,
+                             int bn, cudaStream_t s);
+cudaError_t launch_mlp_gemm2(const CUtensorMap& A, const GemmGather& gg, float* C, int M, int N, int K, int bn,
+                             cudaStream_t s);
 
-// MLP (kind 5): tcgen05-backed gradient (mlp.cu), 5 launches:
-//   gather (+ batch indices) -> GEMM1 (split-K planes) -> per-sample mid -> GEMM2 || batch reductions
+// MLP (kind 5): tcgen05-backed gradient (mlp.cu), 3 launches on the stream + 1 beside:
+//   GEMM1 (batch draw, X rows gathered, split-K reduced in DSMEM) -> per-sample mid
+//   (tanh, output layer, softmax-CE backward, dz1) -> GEMM2 || batch reductions
 struct MlpShape { int n_in, n_hid, n_out; };
 struct MlpWork {                   // scratch carve-up + the fixed tensor maps, built once per context
   MlpShape sh;
-  int M, splits;
-  float *xb, *xbt, *z1p, *hbuf, *dz1, *dz2, *dzt;
+  int M, splits, planes, bn1, bn2; // planes: GEMM1's cluster-reduced z1 planes (0: GEMM1 writes h)
+  float *z1p, *hbuf, *dz1, *dz2;
   int* idx;
-  CUtensorMap x_b, dzt_m, xbt_m;   // GEMM1 A, GEMM2 A, GEMM2 B (W1, GEMM1's B, is mapped per call)
+  CUtensorMap dz1_m;               // GEMM2 A (MN-major boxes of dz1); W1, GEMM1's B, is mapped per call
   cudaStream_t side = nullptr;     // the batch reductions run here beside GEMM2
   cudaEvent_t fork = nullptr, join = nullptr;
 };
@@ -182,7 +199,7 @@ bool mlp_supported(const MlpShape& sh, int M);
 cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch);
 cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx,
                             uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s);
-constexpr int kMlpLaunches = 5;
+constexpr int kMlpLaunches = 4;
 
 // one kernel of each translation unit (CUDA module), see preload_modules()
 const void* kernels_module_anchor();

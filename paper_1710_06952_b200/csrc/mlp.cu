@@ -1,14 +1,18 @@
 // mlp.cu -- minibatch gradient of the 2-layer MLP (config 3, reading R18):
 //   Z1 = X_b W1^T + b1, H = tanh(Z1), Z2 = H W2^T + b2, loss = sum_b CE(softmax(Z2_b), y_b)
 //   g = sum over the batch of dloss/dw  (a SUM), flat layout [W1 | b1 | W2 | b2].
-// Four launches per gradient:
-//   1. gather: batch indices (explicit or device Philox) and X_b [M x I], X_b^T [I x M] (fp32)
-//   2. GEMM1  Z1 [M x H] = X_b . W1^T on tcgen05 (3xTF32, split-K partial planes; W1 read
-//             straight from the model row through its own tensor map)
-//   3. mid:   one CTA per sample -- sum the K-split planes + b1, tanh, the N = O output layer,
-//             softmax-CE backward, dz1; writes h, dz1, dz2 and dZ1^T (fp32)
-//   4. GEMM2  dW1 [H x I] = dZ1^T . (X_b^T)^T into g, with the batch reductions
-//             (db1, dW2, db2) running beside it on a side stream (fork / join events)
+// Three launches on the stream per gradient, plus one beside it:
+//   1. GEMM1  h [M x H] = tanh(X_b W1^T + b1) on tcgen05 (3xTF32): draws the batch indices
+//             (explicit or device Philox) and publishes them, gathers the X rows itself
+//             (cp.async into the swizzled tiles: X_b is never written), W1 straight from the
+//             model row through its own tensor map, split-K with the partials of each
+//             thread-block cluster reduced in distributed shared memory (4 planes left at
+//             config 3; a single cluster per tile finishes bias + tanh in the epilogue)
+//   2. mid:   one CTA per sample -- h = tanh(sum of the planes + b1), the N = O output layer,
+//             softmax-CE backward, dz1, dz2
+//   3. GEMM2  dW1 [H x I] = dZ1^T X_b into g: dZ1 read MN-major by TMA (no transpose),
+//             X rows gathered again (MN-major), with the batch reductions (db1, dW2, db2)
+//             running beside it on a side stream (fork / join events)
 // The tf32 hi / lo split of every operand happens in shared memory (gemm.cu).
 #include "internal.h"
 
@@ -16,76 +20,61 @@ namespace adp {
 
 namespace {
 
-// batch indices (explicit, or Philox4x32-10(key = seed, ctr = (lo32(k), m, "BATC", hi32(k))), as
-// lsq/logreg) and the gathered batch X_b [M x I] plus its transpose X_b^T [I x M]; 32 x 32 tiles
-__global__ void k_mlp_gather(const float* __restrict__ X, int I, const int* __restrict__ idx_in, uint2 key,
-                             unsigned long long k, int S, int M, int* __restrict__ idx, float* __restrict__ xb,
-                             float* __restrict__ xbt) {
-  __shared__ float t[32][33];
-  __shared__ int rows[32];
-  const int c0 = blockIdx.x * 32, r0 = blockIdx.y * 32;
-  pdl_wait();                                   // the previous gradient's GEMM2 still reads xbt
-  pdl_trigger();
-  if (threadIdx.y == 0) {
-    const int m = r0 + threadIdx.x;
-    int v;
-    if (idx_in) v = idx_in[m];
-    else {
-      const uint4 o = philox4x32_10(make_uint4((uint32_t)k, (uint32_t)m, 0x42415443u, (uint32_t)(k >> 32)), key);
-      v = (int)(((unsigned long long)o.x * (unsigned long long)(uint32_t)S) >> 32);
-    }
-    rows[threadIdx.x] = v;
-    if (blockIdx.x == 0) idx[m] = v;
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const float v = X[(long long)rows[r] * I + c0 + threadIdx.x];
-    t[r][threadIdx.x] = v;
-    xb[(long long)(r0 + r) * I + c0 + threadIdx.x] = v;
-  }
-  __syncthreads();
-  for (int c = threadIdx.y; c < 32; c += blockDim.y) xbt[(long long)(c0 + c) * M + r0 + threadIdx.x] = t[threadIdx.x][c];
-}
+// GEMM1 tile, split-K and cluster sizes at config 3 (I = 3072, H = 512, M = 128): 512 / 64 = 8
+// tiles x 16 splits = 128 CTAs (6 k-blocks each) in 32 clusters of 4 -> 4 partial planes.  (A
+// cluster of 16 would finish tanh(z1 + b1) in the GEMM, but only 7 clusters of 16 -- 15 of 8 --
+// fit on the GPU at once: two waves.)
+constexpr int kG1BN = 64, kG1MaxSplits = 16, kG1Cluster = 4;
 
-// one CTA per sample b, one thread per hidden unit u (blockDim = H): z1 = sum of the
-// split-K partials + b1, tanh, the N = O output layer (W2 column u kept in registers,
-// per-warp shuffle sums then a fixed-order sum over warps), softmax-CE backward across
-// the lanes of warp 0, dz1; writes h, dz1 (row b), dz2 and dZ1^T (column b)
+// one CTA per sample b, one thread per hidden unit u (blockDim = H): h (GEMM1's epilogue, or
+// tanh(sum of GEMM1's partial planes + b1)),
+// the N = O output layer (W2 column u kept in registers, per-warp shuffle sums then a
+// fixed-order sum over warps), softmax-CE backward across the lanes of warp 0, dz1;
+// writes dz1 (row b) and dz2
 constexpr int kMaxOut = 32;
 
-__global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p, int splits, int M, int H, int O,
+__global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p, int planes, int M,
+                                                  float* __restrict__ hbuf, int H, int O,
                                                   const float* __restrict__ w, long long off_b1, long long off_W2,
                                                   long long off_b2, const int* __restrict__ y,
-                                                  const int* __restrict__ idx, float* __restrict__ hbuf,
-                                                  float* __restrict__ dz1buf, float* __restrict__ dz2buf,
-                                                  float* __restrict__ dzt) {
+                                                  const int* __restrict__ idx, float* __restrict__ dz1buf,
+                                                  float* __restrict__ dz2buf) {
   __shared__ float red[32][kMaxOut];
   __shared__ float dz2s[kMaxOut];
+  __shared__ int s_lab;
   const int b = blockIdx.x, u = threadIdx.x;
   const int warp = u >> 5, lane = u & 31, nw = blockDim.x >> 5;
   const float* W2 = w + off_W2;
-  pdl_wait();                                   // GEMM1's split-K planes
-  pdl_trigger();
-  float s = 0.0f;
-#pragma unroll 8
-  for (int p = 0; p < splits; ++p) s += z1p[((long long)p * M + b) * H + u];
-  s += w[off_b1 + u];
-  const float hv = tanhf(s);
-  hbuf[(long long)b * H + u] = hv;
   float w2r[kMaxOut];
 #pragma unroll
+  for (int o = 0; o < kMaxOut; ++o) w2r[o] = o < O ? W2[(long long)o * H + u] : 0.0f;   // the model: before the wait
+  const float b1u = w[off_b1 + u];
+  const float b2l = (warp == 0 && lane < O) ? w[off_b2 + lane] : 0.0f;
+  pdl_wait();                                   // GEMM1's h (or z1 planes) and batch indices
+  pdl_trigger();
+  if (u == 0) s_lab = y[idx[b]];                // the label's two dependent loads overlap the planes'
+
+  float hv;
+  if (planes == 0) hv = hbuf[(long long)b * H + u];             // GEMM1 finished tanh(z1 + b1)
+  else {                                                         // the cluster-reduced planes, in order
+    float s = 0.0f;
+    for (int p = 0; p < planes; ++p) s += z1p[((long long)p * M + b) * H + u];
+    hv = tanhf(s + b1u);
+    hbuf[(long long)b * H + u] = hv;
+  }
+#pragma unroll
   for (int o = 0; o < kMaxOut; ++o) {
-    w2r[o] = o < O ? W2[(long long)o * H + u] : 0.0f;
+    if (o >= O) break;                          // O is uniform: no divergence, no dead shuffles
     float part = w2r[o] * hv;
 #pragma unroll
     for (int q = 16; q; q >>= 1) part += __shfl_xor_sync(0xffffffffu, part, q);
-    if (lane == 0 && o < O) red[warp][o] = part;
+    if (lane == 0) red[warp][o] = part;
   }
   __syncthreads();
   if (warp == 0) {
     float z = -INFINITY;
     if (lane < O) {
-      z = w[off_b2 + lane];
+      z = b2l;
       for (int q = 0; q < nw; ++q) z += red[q][lane];
     }
     float mx = z;
@@ -96,7 +85,7 @@ __global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p,
 #pragma unroll
     for (int q = 16; q; q >>= 1) se += __shfl_xor_sync(0xffffffffu, se, q);
     if (lane < O) {
-      const float d = e / se - (lane == y[idx[b]] ? 1.0f : 0.0f);
+      const float d = e / se - (lane == s_lab ? 1.0f : 0.0f);
       dz2s[lane] = d;
       dz2buf[(long long)b * O + lane] = d;
     }
@@ -108,7 +97,6 @@ __global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p,
     if (o < O) dh = fmaf(w2r[o], dz2s[o], dh);
   const float dz = dh * (1.0f - hv * hv);
   dz1buf[(long long)b * H + u] = dz;
-  dzt[(long long)u * M + b] = dz;
 }
 
 // batch reductions (reading R18): db1[u] = sum_b dz1[b][u], dW2[o][u] = sum_b dz2[b][o] h[b][u],
@@ -145,44 +133,48 @@ __global__ void __launch_bounds__(256) k_mlp_reduce(const float* __restrict__ hb
 
 }  // namespace
 
-// GEMM1 split-K: Z1 is only M x H (4 tiles of 128 x 128 at config 3), so K is split to
-// put ~128 CTAs of 128 x 64 tiles on the GPU (6 k-blocks each at I = 3072)
+// GEMM1 split-K: Z1 is only M x H (8 tiles of 128 x 64 at config 3), so K is split over a
+// cluster of CTAs per tile: the largest power of two <= kG1MaxSplits dividing the k-blocks
+// with <= 160 CTAs in all
 int mlp_splits(const MlpShape& sh, int M) {
-  const int kb = sh.n_in / 32, tiles = (M / 128) * (sh.n_hid / 64);
+  const int kb = sh.n_in / 32, tiles = (M / 128) * (sh.n_hid / kG1BN);
   int best = 1;
-  for (int s = 1; s <= 32; ++s)
+  for (int s = 2; s <= kG1MaxSplits; s *= 2)
     if (kb % s == 0 && tiles * s <= 160) best = s;
   return best;
 }
 
+int mlp_planes(const MlpShape& sh, int M) {
+  const int s = mlp_splits(sh, M);
+  return s <= kG1Cluster ? 0 : s / kG1Cluster;     // 0: the GEMM writes h itself
+}
+
 size_t mlp_scratch_floats(const MlpShape& sh, int M) {
-  const size_t I = sh.n_in, H = sh.n_hid, O = sh.n_out;
-  return 2 * (size_t)M * I                         // X_b, X_b^T
-         + (size_t)mlp_splits(sh, M) * M * H       // Z1 partial planes
+  const size_t H = sh.n_hid, O = sh.n_out;
+  return (size_t)mlp_planes(sh, M) * M * H         // z1 partial planes
          + 2 * (size_t)M * H                       // h, dz1
          + (size_t)M * O                           // dz2
-         + H * (size_t)M                           // dZ1^T
          + (size_t)M + 64;                         // idx
 }
 
 bool mlp_supported(const MlpShape& sh, int M) {
-  return M % 128 == 0 && sh.n_hid % 128 == 0 && sh.n_hid <= 1024 && sh.n_in % 128 == 0 && sh.n_out >= 1 &&
-         sh.n_out <= kMaxOut;
+  return M % 128 == 0 && M <= 1024 && sh.n_hid % 128 == 0 && sh.n_hid <= 1024 && sh.n_in % 128 == 0 &&
+         sh.n_out >= 1 && sh.n_out <= kMaxOut;
 }
 
 cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch) {
   wk.sh = sh;
   wk.M = M;
   wk.splits = mlp_splits(sh, M);
-  const size_t I = sh.n_in, H = sh.n_hid;
+  wk.planes = mlp_planes(sh, M);
+  wk.bn1 = kG1BN;
+  wk.bn2 = sh.n_in % 96 == 0 ? 96 : 64;
+  const size_t H = sh.n_hid;
   float* p = scratch;
-  wk.xb = p; p += (size_t)M * I;
-  wk.xbt = p; p += (size_t)M * I;
-  wk.z1p = p; p += (size_t)wk.splits * M * H;
+  wk.z1p = p; p += (size_t)wk.planes * M * H;
   wk.hbuf = p; p += (size_t)M * H;
   wk.dz1 = p; p += (size_t)M * H;
   wk.dz2 = p; p += (size_t)M * sh.n_out;
-  wk.dzt = p; p += H * M;
   wk.idx = reinterpret_cast<int*>(p);
   cudaError_t e;
   if (!wk.side) {
@@ -190,9 +182,7 @@ cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch) {
     if ((e = cudaEventCreateWithFlags(&wk.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
     if ((e = cudaEventCreateWithFlags(&wk.join, cudaEventDisableTiming)) != cudaSuccess) return e;
   }
-  if ((e = make_tmap_k_major(&wk.x_b, wk.xb, M, I, 128)) != cudaSuccess) return e;      // GEMM1 A
-  if ((e = make_tmap_k_major(&wk.dzt_m, wk.dzt, H, M, 128)) != cudaSuccess) return e;   // GEMM2 A
-  return make_tmap_k_major(&wk.xbt_m, wk.xbt, I, M, I % 96 == 0 ? 96 : 64);             // GEMM2 B
+  return make_tmap_mn_major(&wk.dz1_m, wk.dz1, M, H);          // GEMM2 A: 32 x 32 boxes of dz1 [M x H]
 }
 
 cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx_in,
@@ -200,16 +190,17 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   const int I = wk.sh.n_in, H = wk.sh.n_hid, O = wk.sh.n_out, M = wk.M;
   const long long off_b1 = (long long)H * I, off_W2 = off_b1 + H, off_b2 = off_W2 + (long long)O * H;
   CUtensorMap w1;                                             // W1 [H x I], the first H*I floats of w
-  cudaError_t e = make_tmap_k_major(&w1, w, H, I, 64);
+  cudaError_t e = make_tmap_k_major(&w1, w, H, I, wk.bn1);
   if (e != cudaSuccess) return e;
-  // the chain gather -> GEMM1 -> mid -> GEMM2 uses programmatic dependent launch: each kernel's
+  // the chain GEMM1 -> mid -> GEMM2 uses programmatic dependent launch: each kernel's
   // setup (GEMM: barriers, TMEM, tensor-map prefetch) overlaps its predecessor's tail
-  if ((e = launch_pdl(k_mlp_gather, dim3(I / 32, M / 32), dim3(32, 8), 0, s, X, I, idx_in, batch_key, k, S, M,
-                      wk.idx, wk.xb, wk.xbt)) != cudaSuccess)
+  GemmGather g1 = {};
+  g1.x = X; g1.ld = I; g1.idx = idx_in; g1.idx_out = wk.idx; g1.key = batch_key; g1.k = k; g1.S = S;
+  g1.cluster = wk.planes ? kG1Cluster : wk.splits; g1.bias = w + off_b1;
+  if ((e = launch_mlp_gemm1(w1, g1, wk.planes ? wk.z1p : wk.hbuf, M, H, I, wk.splits, wk.bn1, s)) != cudaSuccess)
     return e;
-  if ((e = launch_gemm_tf32x3(wk.x_b, w1, wk.z1p, M, H, I, wk.splits, 64, s)) != cudaSuccess) return e;
-  if ((e = launch_pdl(k_mlp_mid, dim3(M), dim3(H), 0, s, (const float*)wk.z1p, wk.splits, M, H, O, w, off_b1,
-                      off_W2, off_b2, y, (const int*)wk.idx, wk.hbuf, wk.dz1, wk.dz2, wk.dzt)) != cudaSuccess)
+  if ((e = launch_pdl(k_mlp_mid, dim3(M), dim3(H), 0, s, (const float*)wk.z1p, wk.planes, M, wk.hbuf, H, O, w,
+                      off_b1, off_W2, off_b2, y, (const int*)wk.idx, wk.dz1, wk.dz2)) != cudaSuccess)
     return e;
   // the batch reductions on the side stream, beside GEMM2 (which leaves SMs free)
   if ((e = cudaEventRecord(wk.fork, s)) != cudaSuccess) return e;
@@ -218,13 +209,14 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   k_mlp_reduce<<<(unsigned)((nred * 32 + 255) / 256), 256, 0, wk.side>>>(wk.hbuf, wk.dz1, wk.dz2, M, H, O, g, off_b1,
                                                                           off_W2, off_b2);
   // dW1 in 128 x 96 tiles (I = 3072: 4 x 32 = 128 CTAs, one wave)
-  if ((e = launch_gemm_tf32x3(wk.dzt_m, wk.xbt_m, g, H, I, M, 1, I % 96 == 0 ? 96 : 64, s)) != cudaSuccess)
-    return e;
+  GemmGather g2 = {};
+  g2.x = X; g2.ld = I; g2.idx = wk.idx; g2.cluster = 1;
+  if ((e = launch_mlp_gemm2(wk.dz1_m, g2, g, H, I, M, wk.bn2, s)) != cudaSuccess) return e;
   if ((e = cudaEventRecord(wk.join, wk.side)) != cudaSuccess) return e;
   if ((e = cudaStreamWaitEvent(s, wk.join, 0)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
-const void* mlp_module_anchor() { return (const void*)k_mlp_gather; }
+const void* mlp_module_anchor() { return (const void*)k_mlp_mid; }
 
 }  // namespace adp

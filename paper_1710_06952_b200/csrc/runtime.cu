@@ -1979,20 +1979,27 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
   })
 }
 
+// split-K partials of a tile are reduced in DSMEM across a cluster of CTAs when splits is a
+// power of two <= 16 (one pass, no partial planes); otherwise planes + a fixed-order sum
+static int gemm_cluster(int splits) {
+  return (splits >= 2 && splits <= 16 && (splits & (splits - 1)) == 0) ? splits : 1;
+}
+
 adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
                                  int32_t splits) {
   GUARD({
     if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || splits < 1) return fail(ADPSGD_E_INVALID, "gemm args");
     if (M % 128 || N % 64 || K % (32 * splits)) return fail(ADPSGD_E_INVALID, "gemm shape");
     const int bn = N % 128 == 0 ? 128 : 64;
+    const int cl = gemm_cluster(splits);
     float* part = nullptr;
-    if (splits > 1) CU(cudaMalloc(&part, sizeof(float) * (size_t)splits * M * N));
+    if (cl < splits) CU(cudaMalloc(&part, sizeof(float) * (size_t)splits * M * N));
     CUtensorMap ta, tb;
     adpsgd_status st = ADPSGD_OK;
     cudaError_t e = make_tmap_k_major(&ta, A, M, K, 128);
     if (e == cudaSuccess) e = make_tmap_k_major(&tb, B, N, K, bn);
-    if (e == cudaSuccess) e = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : C, M, N, K, splits, bn, nullptr);
-    if (e == cudaSuccess && splits > 1) e = launch_sum_planes(part, C, splits, (long long)M * N, nullptr);
+    if (e == cudaSuccess) e = launch_gemm_tf32x3(ta, tb, cl < splits ? part : C, M, N, K, splits, bn, nullptr, cl);
+    if (e == cudaSuccess && cl < splits) e = launch_sum_planes(part, C, splits / cl, (long long)M * N, nullptr);
     if (e == cudaSuccess) e = cudaDeviceSynchronize();
     if (e != cudaSuccess) st = fail(ADPSGD_E_CUDA, std::string("gemm: ") + cudaGetErrorString(e));
     if (part) cudaFree(part);
@@ -2018,9 +2025,10 @@ adpsgd_status adpsgd_gemm_tf32x3_bench(int32_t M, int32_t N, int32_t K, int32_t 
     if (e == cudaSuccess) e = launch_fill_hash(b, (long long)nb, 2u, nullptr);
     if (e == cudaSuccess) e = make_tmap_k_major(&ta, a, M, K, 128);
     if (e == cudaSuccess) e = make_tmap_k_major(&tb, b, N, K, bn);
+    const int cl = gemm_cluster(splits);
     auto once = [&]() {
-      cudaError_t r = launch_gemm_tf32x3(ta, tb, splits > 1 ? part : c, M, N, K, splits, bn, nullptr);
-      if (r == cudaSuccess && splits > 1) r = launch_sum_planes(part, c, splits, (long long)M * N, nullptr);
+      cudaError_t r = launch_gemm_tf32x3(ta, tb, cl < splits ? part : c, M, N, K, splits, bn, nullptr, cl);
+      if (r == cudaSuccess && cl < splits) r = launch_sum_planes(part, c, splits / cl, (long long)M * N, nullptr);
       return r;
     };
     for (int w = 0; w < 2 && e == cudaSuccess; ++w) e = once();

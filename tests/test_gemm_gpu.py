@@ -15,8 +15,10 @@ def P():
 
 
 @pytest.mark.parametrize("M,N,K,splits", [(128, 128, 32, 1), (128, 128, 256, 1), (256, 384, 512, 2),
-                                          (128, 512, 3072, 12), (512, 3072, 128, 1)])
+                                          (128, 512, 3072, 12), (128, 512, 3072, 16), (128, 512, 3072, 8),
+                                          (256, 128, 1024, 4), (512, 3072, 128, 1)])
 def test_gemm_tf32x3_matches_fp64(P, M, N, K, splits):
+    """splits a power of two <= 16: split-K reduced in DSMEM over a cluster; 12: partial planes"""
     import torch
     g = torch.Generator(device="cuda").manual_seed(M * 7 + N * 3 + K)
     A = torch.randn(M, K, device="cuda", generator=g)
