@@ -49,7 +49,6 @@ def parse():
     ap.add_argument("--placement", type=int, default=0)
     ap.add_argument("--no-extras", action="store_true", help="skip baseline/no-straggler/cpu legs")
     ap.add_argument("--cpu-events", type=int, default=12)
-    ap.add_argument("--engine-variant", type=int, default=0, help="0 TMA-staged, 1 register slices")
     ap.add_argument("--ctas-per-sm", type=int, default=0)
     ap.add_argument("--topology", default="ring", choices=["ring", "skip"])
     ap.add_argument("--no-fuse", action="store_true", help="never fuse a due passive step into a pair pass")
@@ -292,9 +291,10 @@ def mlp_leg(P, synth, torch, events=64):
 def config1_leg(P, synth, torch, K=2000):
     """Config 1 (BASELINE configs[0]): least squares, n = 4 ring, d = 1024, M = 32,
     T = 4, a seeded 2000-event replay with explicit batches.  Latency-bound
-    (4 KB rows): us/event of the HOST executor (gradient + event kernels) next to
-    the launch floor -- the same schedule as pure averaging (one 4 KB pass per
-    event)."""
+    (4 KB rows): us/event of the HOST executor, which runs the whole lsq schedule
+    in ONE launch (k_lin_replay: per event its stale-read gradients, then the
+    event), next to the same schedule as pure averaging issued one kernel per
+    event (the floor of any one-launch-per-event executor)."""
     n, d, M, T, S = 4, 1024, 32, 4, 8192
     e, r = synth.ring(n)
     A, b = synth.lsq_data(S=S, d=d, seed=1)
@@ -317,7 +317,8 @@ def config1_leg(P, synth, torch, K=2000):
         out[name] = {"us_per_event": 1e6 * sec / K, "events_per_s": K / sec,
                      "kernel_launches_per_event": (ctx.launch_count() - l0) / K}
         ctx.destroy()
-    out["workload"] = f"config1: lsq n={n} ring, d={d}, M={M}, T={T}, {K}-event seeded replay (HOST executor)"
+    out["workload"] = (f"config1: lsq n={n} ring, d={d}, M={M}, T={T}, {K}-event seeded replay (HOST executor: "
+                       f"lsq in one launch; averaging_only one launch per event)")
     return out
 
 
@@ -395,7 +396,7 @@ def main():
                          model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                          quad_noise_s=s, straggler=st, compute_ns=cns if compute_ns is None else compute_ns,
                          seed=1234, log_capacity=1 << 16,
-                         engine_variant=a.engine_variant, engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free,
+                         engine_ctas_per_sm=a.ctas_per_sm, wait_free=wait_free,
                          engine_fuse=not a.no_fuse, engine_coop=None if a.coop == 0 else a.coop > 0)
 
     stream = torch.cuda.Stream()
@@ -680,7 +681,7 @@ def main():
             cl = P.Context(e, n, d, role=r, rank=rank, world_size=world, device=local, placement=a.placement,
                            model=P.MODEL_QUADRATIC, gamma=GAMMA, batch_M=M_BATCH, quad_keys=(dk, nk),
                            quad_noise_s=s, straggler=synth.stragglers(n, slow_worker=None), compute_ns=cns,
-                           seed=1234, log_capacity=1 << 16, engine_variant=a.engine_variant,
+                           seed=1234, log_capacity=1 << 16,
                            engine_ctas_per_sm=a.ctas_per_sm, link_slow=lv, link_ns=link_ns)
             lk[f"link_x{L:g}"] = three_way(cl, 4)
         lk["workload"] = f"config 4, no compute straggler, worker 1 link slowed, link_ns = {link_ns}"
@@ -733,7 +734,7 @@ def main():
             xor = world >= 4 and (world & (world - 1)) == 0
             cn = P.Context(es, ns, d, role=rs, rank=rank, world_size=world, device=local,
                            placement=2 if xor else 1, worker_rank=synth.placement_xor(ns, world) if xor else None,
-                           engine_variant=a.engine_variant, log_capacity=1 << 16)
+                           log_capacity=1 << 16)
             cn.run(2 * ns, stream)
             torch.cuda.synchronize()
             cn.sync()

@@ -119,9 +119,8 @@ typedef struct {
   const float* straggler;     /* n slowdown factors >= 1; NULL = all 1          */
   int64_t compute_ns;         /* emulated per-gradient compute time t_c of a 1x worker        */
   int32_t engine_ctas_per_sm; /* 0 = default                                                  */
-  int32_t engine_variant;     /* 0 = bulk-copy (TMA) staged, CTA barrier per tile (default)   */
-                              /* 1 = register slices; 2 = bulk-copy, per-warp empty barriers; */
-                              /* 3 = variant 0 + two-sided push protocol for cross-GPU pairs  */
+  int32_t engine_variant;     /* reserved (the round-1 A/B variants are gone): must be 0;     */
+                              /* anything else fails with ADPSGD_E_UNSUPPORTED                */
   int64_t log_capacity;       /* event-log ring entries on rank 0; 0 = default (1<<20)        */
   int32_t wait_free;          /* adpsgd_run loop: 0 = Alg. 1 (gradient fused into the event); */
                               /* 1 = App. A wait-free runtime: a worker pulls   */

@@ -101,26 +101,30 @@ cudaError_t launch_quad_grad(const float* xhat, float* g, long long d, long long
 cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, const int* idx,
                                int M, uint2 batch_key, unsigned long long k, const float* xhat,
                                float* g, long long d, cudaStream_t s);
-// config 1's one-launch event: the lsq / logreg gradients read at X_t, then event t
-constexpr int kLinStepReads = 8;
+// config 1's whole replay in ONE launch: per event t, the lsq / logreg gradients read at X_t,
+// then event t (k_lin_replay, one CTA walking the schedule in order)
 struct LinRead {
   const float* x;                  // row read (state X_t)
   float* g;                        // gradient slot written
   const int* idx;                  // explicit batch indices, or null (device Philox)
   unsigned long long k;            // random-draw key
 };
-struct LinStepParams {
-  int kind, S, M, nreads;
-  const float *A, *b;
-  uint2 key;
-  LinRead reads[kLinStepReads];
+struct LinEventOp {
   float *xi, *xj;                  // event t (xi null: reads only)
   const float* g;                  // its gradient slot, null for NO_GRAD
   int ff;                          // App. A flush-first order
+  int r0, r1;                      // its reads: LinRead[r0, r1)
+};
+struct LinReplayParams {
+  int kind, S, M, nops;
+  const float *A, *b;
+  uint2 key;
+  const LinRead* reads;            // device arrays
+  const LinEventOp* ops;
   float gamma;
   long long d, n4;
 };
-cudaError_t launch_lin_step(const LinStepParams& p, cudaStream_t s);
+cudaError_t launch_lin_replay(const LinReplayParams& p, cudaStream_t s);
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s);
 cudaError_t launch_fill_hash(float* x, long long n, uint32_t seed, cudaStream_t s);   // diagnostics
 // App. A local-update compensation of a pulled model: out = fl(x - fl(gamma gp))

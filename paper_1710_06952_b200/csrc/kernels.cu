@@ -146,7 +146,8 @@ __device__ __forceinline__ void linear_grad_v_body(LinSmem& sm, int kind, const 
   for (int m = warp; m < M; m += nw) {
     const float4* a4 = reinterpret_cast<const float4*>(A + (long long)sidx[m] * d);
     float acc = 0.0f;
-    for (long long c = lane; c < d4; c += 32) {
+#pragma unroll 8
+    for (long long c = lane; c < d4; c += 32) {        // unrolled: the loads of a row are in flight together
       const float4 av = __ldg(a4 + c), xv = __ldcg(x4 + c);
       acc = fmaf(av.x, xv.x, acc);
       acc = fmaf(av.y, xv.y, acc);
@@ -171,6 +172,7 @@ __device__ __forceinline__ void linear_grad_v_body(LinSmem& sm, int kind, const 
     const long long c = c0 + t;
     float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
     if (c < d4)
+#pragma unroll 8
       for (int m = q; m < M; m += 4) {
         const float4 av = __ldg(reinterpret_cast<const float4*>(A + (long long)sidx[m] * d) + c);
         const float cm = coef[m];
@@ -202,35 +204,42 @@ __global__ void __launch_bounds__(kLinThreadsV) k_linear_grad_v(int kind, const 
   linear_grad_v_body(sm, kind, A, b, S, idx_in, M, key, k, xhat, g, d);
 }
 
-// Config 1 in ONE launch per event (latency-bound): the lsq / logreg
-// gradients whose stale read point is X_t (the reads due before event t)
-// read their rows first, then -- after a CTA barrier -- event t itself runs
-// (the pair average and update, Alg. 1 steps 4-6).  The same code as the
-// standalone gradient and event kernels, so the results are identical.
-__global__ void __launch_bounds__(kLinThreadsV) k_lin_step(LinStepParams p) {
+// Config 1's replay in ONE launch (latency-bound): one CTA walks the schedule in
+// order; at event t it first computes the lsq / logreg gradients whose stale read point is X_t
+// (the reads due before event t) into their slots, then -- after a CTA barrier -- applies
+// event t (the pair average and update, Alg. 1 steps 4-6); a barrier orders event t's writes
+// before event t + 1's reads.  The same code as the standalone gradient and event kernels, so
+// the results are identical to the per-event launches it replaces.
+__global__ void __launch_bounds__(kLinThreadsV) k_lin_replay(LinReplayParams p) {
   __shared__ LinSmem sm;
-  for (int r = 0; r < p.nreads; ++r)
-    linear_grad_v_body(sm, p.kind, p.A, p.b, p.S, p.reads[r].idx, p.M, p.key, p.reads[r].k, p.reads[r].x,
-                       p.reads[r].g, p.d);
-  __syncthreads();
-  if (!p.xi) return;
-  float4* xi4 = reinterpret_cast<float4*>(p.xi);
-  float4* xj4 = reinterpret_cast<float4*>(p.xj);
-  const float4* g4 = reinterpret_cast<const float4*>(p.g);
   const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
-  for (long long c = threadIdx.x; c < p.n4; c += blockDim.x) {
-    float4 a = xi4[c], bb = p.xj ? xj4[c] : z;
-    const float4 gg = p.g ? g4[c] : z;
-    const uint32_t c0 = (uint32_t)(c * 4);
-    if (p.xj) {
-      if (!p.g) update4<true, kGradNone>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
-      else if (p.ff) update4<true, kGradExternal, true>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
-      else update4<true, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
-      xj4[c] = bb;
-    } else if (p.g) {
-      update4<false, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+  for (int e = 0; e < p.nops; ++e) {
+    const LinEventOp op = p.ops[e];
+    for (int r = op.r0; r < op.r1; ++r) {
+      const LinRead rd = p.reads[r];
+      linear_grad_v_body(sm, p.kind, p.A, p.b, p.S, rd.idx, p.M, p.key, rd.k, rd.x, rd.g, p.d);
     }
-    xi4[c] = a;
+    __syncthreads();
+    if (op.xi) {
+      float4* xi4 = reinterpret_cast<float4*>(op.xi);
+      float4* xj4 = reinterpret_cast<float4*>(op.xj);
+      const float4* g4 = reinterpret_cast<const float4*>(op.g);
+      for (long long c = threadIdx.x; c < p.n4; c += blockDim.x) {
+        float4 a = __ldcg(xi4 + c), bb = op.xj ? __ldcg(xj4 + c) : z;
+        const float4 gg = op.g ? __ldcg(g4 + c) : z;
+        const uint32_t c0 = (uint32_t)(c * 4);
+        if (op.xj) {
+          if (!op.g) update4<true, kGradNone>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+          else if (op.ff) update4<true, kGradExternal, true>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+          else update4<true, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+          __stcg(xj4 + c, bb);
+        } else if (op.g) {
+          update4<false, kGradExternal>(a, bb, gg, z, c0, p.d, p.gamma, QuadParams{}, 0u);
+        }
+        __stcg(xi4 + c, a);
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -620,9 +629,10 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
   return cudaGetLastError();
 }
 
-cudaError_t launch_lin_step(const LinStepParams& p, cudaStream_t s) {
-  if (p.M > kMaxM || p.d % 4 || p.nreads > kLinStepReads) return cudaErrorInvalidValue;
-  k_lin_step<<<1, kLinThreadsV, 0, s>>>(p);
+cudaError_t launch_lin_replay(const LinReplayParams& p, cudaStream_t s) {
+  if (p.M > kMaxM || p.d % 4) return cudaErrorInvalidValue;
+  if (p.nops == 0) return cudaSuccess;
+  k_lin_replay<<<1, kLinThreadsV, 0, s>>>(p);
   return cudaGetLastError();
 }
 

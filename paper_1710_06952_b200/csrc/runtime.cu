@@ -140,6 +140,8 @@ struct adpsgd_ctx {
   float *dA = nullptr, *db = nullptr;
   int* dy = nullptr;
   float* gslots = nullptr;
+  unsigned char* lin_buf = nullptr;   // config-1 replay op list (k_lin_replay)
+  size_t lin_cap = 0;
   int gslot_n = 0;
   float* gstep = nullptr;            // per-local-worker gradient buffers (adpsgd_step)
   float* wf_g = nullptr;             // App. A: [n_local][2][d_pad] gradient rows (wait_free)
@@ -553,38 +555,57 @@ adpsgd_status replay_host(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cons
   if (c->model == ADPSGD_MODEL_MLP && need_slots) ST(ensure_mlp_scratch(c, ns));
   DagState dag(c->n, slots);
   if (ns > 1) ST(dag_fork(c, s, ns));
-  // config 1 (lsq / logreg, one lane): the gradients read at X_e and event e share one launch
+  // config 1 (lsq / logreg, one lane): the whole schedule -- at each event e the gradients read
+  // at X_e, then event e -- in ONE launch of k_lin_replay
   const bool fuse_lin = (c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG) && ns == 1 && !any_comp &&
                         c->d % 4 == 0 && c->M <= 1024;
-  for (int64_t e = 0; e < K && fuse_lin; ++e) {
-    LinStepParams lp{};
-    lp.kind = (int)c->model; lp.S = c->S; lp.M = c->M; lp.A = c->dA; lp.b = c->db; lp.key = c->seed2();
-    lp.gamma = c->gamma; lp.d = c->d; lp.n4 = c->n4;
-    for (int64_t kp : reads[e]) {
-      if (lp.nreads == kLinStepReads) {                      // more reads at one point than fit: reads only
-        CU(launch_lin_step(lp, s));
-        ++c->launches;
-        lp.nreads = 0;
+  if (fuse_lin && K > 0) {
+    std::vector<LinRead> lr;
+    std::vector<LinEventOp> lo((size_t)K);
+    for (int64_t e = 0; e < K; ++e) {
+      LinEventOp& op = lo[(size_t)e];
+      op.r0 = (int)lr.size();
+      for (int64_t kp : reads[e]) {
+        LinRead r{};
+        const int i = ev[kp].i;
+        r.x = c->row(i);
+        r.g = c->gslots + (long long)(kp % slots) * c->d_pad;
+        r.idx = bidx ? c->d_batch + kp * c->M : nullptr;
+        r.k = (ev[kp].flags & ADPSGD_EV_FLUSH_FIRST) ? read_key(k0 + kp - ev[kp].tau, i) : k0 + kp;
+        lr.push_back(r);
       }
-      LinRead& r = lp.reads[lp.nreads++];
-      const int i = ev[kp].i;
-      r.x = c->row(i);
-      r.g = c->gslots + (long long)(kp % slots) * c->d_pad;
-      r.idx = bidx ? c->d_batch + kp * c->M : nullptr;
-      r.k = (ev[kp].flags & ADPSGD_EV_FLUSH_FIRST) ? read_key(k0 + kp - ev[kp].tau, i) : k0 + kp;
+      op.r1 = (int)lr.size();
+      const int i = ev[e].i, j = ev[e].j;
+      const bool grad = !(ev[e].flags & ADPSGD_EV_NO_GRAD);
+      if (j >= 0 || grad) {
+        op.xi = c->row(i);
+        op.xj = j >= 0 ? c->row(j) : nullptr;
+        op.g = grad ? c->gslots + (long long)(e % slots) * c->d_pad : nullptr;
+        op.ff = grad && (ev[e].flags & ADPSGD_EV_FLUSH_FIRST) ? 1 : 0;
+      }
     }
-    const int i = ev[e].i, j = ev[e].j;
-    const bool grad = !(ev[e].flags & ADPSGD_EV_NO_GRAD);
-    if (j >= 0 || grad) {
-      lp.xi = c->row(i);
-      lp.xj = j >= 0 ? c->row(j) : nullptr;
-      lp.g = grad ? c->gslots + (long long)(e % slots) * c->d_pad : nullptr;
-      lp.ff = grad && (ev[e].flags & ADPSGD_EV_FLUSH_FIRST) ? 1 : 0;
+    const size_t bytes = lo.size() * sizeof(LinEventOp) + lr.size() * sizeof(LinRead);
+    if (c->lin_cap < bytes) {
+      if (c->lin_buf) cudaFree(c->lin_buf);
+      c->lin_buf = nullptr;
+      CU(cudaMalloc(&c->lin_buf, bytes));
+      c->lin_cap = bytes;
     }
-    if (lp.nreads || lp.xi) {
-      CU(launch_lin_step(lp, s));
-      ++c->launches;
-    }
+    // lin_buf may still feed the previous replay, and the host vectors die with this call:
+    // stage them in stream order and wait (a few tens of KB)
+    CU(cudaStreamSynchronize(s));
+    CU(cudaMemcpyAsync(c->lin_buf, lo.data(), lo.size() * sizeof(LinEventOp), cudaMemcpyHostToDevice, s));
+    if (!lr.empty())
+      CU(cudaMemcpyAsync(c->lin_buf + lo.size() * sizeof(LinEventOp), lr.data(), lr.size() * sizeof(LinRead),
+                         cudaMemcpyHostToDevice, s));
+    CU(cudaStreamSynchronize(s));
+    LinReplayParams lp{};
+    lp.kind = (int)c->model; lp.S = c->S; lp.M = c->M; lp.A = c->dA; lp.b = c->db; lp.key = c->seed2();
+    lp.gamma = c->gamma; lp.d = c->d; lp.n4 = c->n4; lp.nops = (int)K;
+    lp.ops = reinterpret_cast<const LinEventOp*>(c->lin_buf);
+    lp.reads = reinterpret_cast<const LinRead*>(c->lin_buf + lo.size() * sizeof(LinEventOp));
+    CU(launch_lin_replay(lp, s));
+    ++c->launches;
   }
   for (int64_t e = 0; e < K && !fuse_lin; ++e) {
     for (int64_t kp : reads[e]) {     // stale reads that happen before event e
@@ -879,7 +900,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
   for (auto e : c->evring) if (e) cudaEventDestroy(e);
   for (auto st : c->pool) if (st) cudaStreamDestroy(st);
   void* bufs[] = {c->models, c->ctl_arena, c->d_workers, c->d_nbrs, c->d_local_ids,
-                  c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch,
+                  c->d_rev, c->dx0, c->dA, c->db, c->dy, c->gslots, c->gstep, c->mlp_scratch, c->lin_buf,
                   c->d_batch, c->sum64, c->mk_acc, c->xr, c->gsum, c->rrows,
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
                   c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar, c->agree64};

@@ -13,3 +13,6 @@ timeout 600 ncu -k regex:k_engine -s 1 -c 1 --set full --import-source on --cloc
   -o gpurun_out/${T}_k_engine_full python tools/prof_engine.py --updates 256 --runs 2 > gpurun_out/${T}_prof_engine.log 2>&1
 timeout 600 ncu -k regex:k_gemm -s 2 -c 2 --set full --import-source on --clock-control none \
   -o gpurun_out/${T}_gemm_full python tools/prof_mlp.py > /dev/null 2>&1
+# per-CTA phase trace of the GEMM kernels (tools/gemm_probe_build.sh builds build_probe/base/probe)
+timeout 120 ./build_probe/base/probe > gpurun_out/${T}_gemm_phase_trace.txt 2>&1
+timeout 300 python tools/mlp_host_bound.py > gpurun_out/${T}_mlp_host_bound.txt 2>&1

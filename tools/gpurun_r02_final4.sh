@@ -12,8 +12,3 @@ for N in 2 4; do
   timeout 1500 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 \
     --master-port $((29511 + N)) bench.py --gpus $N > gpurun_out/${T}_bench_N${N}.json 2> gpurun_out/${T}_bench_N${N}.err
 done
-for v in d16 main d16; do
-  if [ $v = main ]; then L=paper_1710_06952_b200/libadpsgd.so; else L=build_ab/$v/libadpsgd.so; fi
-  ADPSGD_LIB=$L timeout 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29650 bench.py --gpus 4 --no-extras --steps 20 > gpurun_out/${T}_ab_${v}.json 2>/dev/null
-  python -c "import json; d=json.loads(open('gpurun_out/${T}_ab_${v}.json').read().strip().splitlines()[-1]); print('N=4', '$v', round(d['value']), round(d['updates_per_s']), round(d['roofline']['frac'],4))" >> gpurun_out/${T}_ab_summary.txt
-done
