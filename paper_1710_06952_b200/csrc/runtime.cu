@@ -177,6 +177,7 @@ struct adpsgd_ctx {
   int super_R = 0;
   float* super_g = nullptr;                        // learner gradient, then the group's sum
   unsigned long long* super_k = nullptr;           // ticket broadcast by the group leader
+  unsigned long long* k_host = nullptr;            // pinned: step_multi reads its ticket here
   int* super_bar = nullptr;                        // group barrier word
   long long super_c = 0;                           // gradient events of this rank's super-learner
   std::vector<std::vector<int>> super_nb;          // super-learner ring neighbours
@@ -855,6 +856,19 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
     c->rrows_n = c->T + 1;
     ST(upload_workers(c));
   }
+  // the op list (<= one op per endpoint of each event + one read per event), sized before the
+  // collective below: after it a peer's engine may already run, and with ranks sharing a GPU
+  // (comm_local) a cudaMalloc / cudaFree that synchronises the device would wait for it
+  {
+    const size_t cap = (size_t)3 * (size_t)K + (size_t)c->n_local + 1;
+    if (c->rev_cap < cap) {
+      CU(cudaDeviceSynchronize());
+      if (c->d_rev) cudaFree(c->d_rev);
+      c->d_rev = nullptr;
+      CU(cudaMalloc(&c->d_rev, sizeof(ReplayEv) * cap));
+      c->rev_cap = cap;
+    }
+  }
   // k and the epochs are tracked identically on every rank (they only change
   // through collective calls whose effect is known: a replay advances k by K
   // and the epochs by the schedule, a run ends at exactly its target), so no
@@ -870,12 +884,7 @@ adpsgd_status replay_engine(adpsgd_ctx* c, const adpsgd_event* ev, int64_t K, cu
     c->h_rev.insert(c->h_rev.end(), per[l].begin(), per[l].end());
     c->h_slots[l].ev_end = (long long)c->h_rev.size();
   }
-  if (c->rev_cap < c->h_rev.size() + 1) {
-    if (c->d_rev) cudaFree(c->d_rev);
-    c->d_rev = nullptr;
-    CU(cudaMalloc(&c->d_rev, sizeof(ReplayEv) * (c->h_rev.size() + 1)));
-    c->rev_cap = c->h_rev.size() + 1;
-  }
+  if (c->rev_cap < c->h_rev.size() + 1) return fail(ADPSGD_E_STATE, "replay op list exceeds its bound");
   if (!c->h_rev.empty())
     CU(cudaMemcpyAsync(c->d_rev, c->h_rev.data(), sizeof(ReplayEv) * c->h_rev.size(), cudaMemcpyHostToDevice, s));
   CU(cudaMemcpyAsync(c->d_slots, c->h_slots.data(), sizeof(Slot) * c->n_local, cudaMemcpyHostToDevice, s));
@@ -905,6 +914,7 @@ adpsgd_status destroy_impl(adpsgd_ctx* c) {
                   c->dp_x[0], c->dp_x[1], c->dp_halo, c->d_dp_nbr[0], c->d_dp_nbr[1], c->d_dp_deg,
                   c->d_dp_wself, c->wf_g, c->comp_row, c->super_g, c->super_k, c->super_bar, c->agree64};
   for (void* b : bufs) if (b) cudaFree(b);
+  if (c->k_host) cudaFreeHost(c->k_host);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
   return ADPSGD_OK;
@@ -1040,6 +1050,11 @@ adpsgd_status init_impl(const adpsgd_graph* g, int32_t n_workers, int64_t d,
   CU(cudaSetDevice(c->device));
   ST(preload_modules(c->device));
   CU(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  // the ticket slot host-driven steps and super-learners read back, allocated here and never
+  // lazily: a cudaMalloc while another rank's lock kernel spins can stall until that rank's
+  // commit -- which may be waiting to be launched by the thread inside cudaMalloc
+  CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
+  CU(cudaMallocHost(&c->k_host, sizeof(unsigned long long)));
   // models
   CU(cudaMalloc(&c->models, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
   CU(cudaMemset(c->models, 0, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
@@ -1275,6 +1290,11 @@ adpsgd_status adpsgd_connect(adpsgd_ctx* c, const void* nccl_id) {
       if (!nccl_id) return fail(ADPSGD_E_INVALID, "nccl_id required when world_size > 1");
       if (c->comm_local) CO(make_local_comm(nccl_id, c->world, c->rank, c->device, &c->comm, m_));
       else CO(make_nccl_comm(nccl_id, c->world, c->rank, &c->comm, m_));
+      // adpsgd_step's built-in gradient buffers, now rather than under another rank's lock wait
+      if (c->model == ADPSGD_MODEL_LSQ || c->model == ADPSGD_MODEL_LOGREG || c->model == ADPSGD_MODEL_MLP) {
+        if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
+        if (c->model == ADPSGD_MODEL_MLP) ST(ensure_mlp_scratch(c, 1));
+      }
     }
     c->connected = true;
     return ADPSGD_OK;
@@ -1339,16 +1359,10 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
   auto row_of = [&](int v) {
     return c->peer_models[c->worker_rank[v]] + (long long)c->worker_local[v] * c->d_pad;
   };
-  if (!c->super_k) {
-    CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));
-    CU(cudaDeviceSynchronize());
-  }
-  // allocate before taking the lock: nothing that may synchronise the device
-  // (which would wait for a peer's lock kernel spinning on our lock) runs under it
-  if (!gossip && !grad && c->model != ADPSGD_MODEL_QUADRATIC) {
-    if (!c->gstep) CU(cudaMalloc(&c->gstep, sizeof(float) * c->d_pad * std::max(1, c->n_local)));
-    if (c->model == ADPSGD_MODEL_MLP) ST(ensure_mlp_scratch(c, 1));
-  }
+  // every buffer was allocated at connect: nothing here may synchronise the device (which
+  // would wait for a peer's lock kernel spinning on a lock whose release this thread launches)
+  if (!gossip && !grad && c->model != ADPSGD_MODEL_QUADRATIC && !c->gstep)
+    return fail(ADPSGD_E_STATE, "adpsgd_step: gradient buffers missing (allocated by adpsgd_connect)");
   cudaStream_t st = c->use(s);
   // rows of local workers stay ordered with this context's other streams (as
   // the single-GPU adpsgd_step / adpsgd_gossip order them)
@@ -1360,9 +1374,9 @@ static adpsgd_status step_multi(adpsgd_ctx* c, int w, const float* grad, adpsgd_
   // call naming the passive first)
   unsigned int* lock = &ctl_of((j >= 0 && c->role[w] == 0) ? j : w)->lock;
   CU(launch_super_lock(lock, &c->gctl0->ticket, c->super_k, &c->gctl->error, 20ull * 1000000000ull, st));
-  unsigned long long k = 0;
-  CU(cudaMemcpyAsync(&k, c->super_k, sizeof k, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(c->k_host, c->super_k, sizeof(unsigned long long), cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
+  const unsigned long long k = *c->k_host;
   if (k == ~0ull) return fail(ADPSGD_E_TIMEOUT, "adpsgd_step: lock wait exceeded the watchdog");
   int mode = gossip ? kGradNone : kGradExternal;
   const float* g = grad;
@@ -1717,7 +1731,6 @@ static adpsgd_status super_setup(adpsgd_ctx* c) {
   if (R > 1 && !c->super_comm) CO(c->comm->split(c->rank / R, c->rank % R, &c->super_comm, m_));
   if (!c->super_g) {
     CU(cudaMalloc(&c->super_g, sizeof(float) * c->d_pad));
-    if (!c->super_k) CU(cudaMalloc(&c->super_k, sizeof(unsigned long long)));   // step_multi may own it
     // MLP scratch now: its first allocation synchronises the device, which must
     // not happen under a lock (in-process ranks share the device with the
     // lock kernels spinning on it)
