@@ -37,6 +37,16 @@ def test_virtual_ranks_parity(world):
     assert not fails, fails
 
 
+@pytest.mark.skipif(os.environ.get("ADPSGD_TEST_WORLD8") != "1",
+                    reason="opt-in (ADPSGD_TEST_WORLD8=1, ~85 s): 8 in-process ranks, the N = 8 protocol on one GPU")
+def test_virtual_ranks_parity_world8():
+    """mp_worker's checks with 8 in-process ranks on cuda:0: the cross-rank protocol at the
+    world size the 8-GPU scaling run uses (this pool's boxes have at most 4 GPUs)."""
+    import mp_worker
+    fails = _virtual(8, lambda r, G: mp_worker.body(r, 8, 0, G))
+    assert not fails, fails
+
+
 @pytest.mark.parametrize("world", [2, 4])
 def test_virtual_super_learner(world):
     """Every factorisation world = S*R, R learners co-located on one GPU: replicas
