@@ -524,14 +524,15 @@ def main():
     for k in range(a.steps):
         b_ = k % 2
         ctx.run(U, stream)
-        if k >= 2:
+        if k >= 2 and rank == 0:
             stream.wait_event(copied[b_])       # buffer b_'s copy from step k - 2 is done
         ctx.consensus_mean(outs[b_].data_ptr(), with_mk=False, stream=stream)
-        ready.record(stream)
-        copy_stream.wait_event(ready)
-        with torch.cuda.stream(copy_stream):
-            hosts[b_].copy_(outs[b_], non_blocking=True)
-        copied[b_].record(copy_stream)
+        if rank == 0:                           # x_bar is the same on every rank: rank 0 returns it
+            ready.record(stream)
+            copy_stream.wait_event(ready)
+            with torch.cuda.stream(copy_stream):
+                hosts[b_].copy_(outs[b_], non_blocking=True)
+            copied[b_].record(copy_stream)
     torch.cuda.synchronize()
     te = maxr(time.perf_counter() - te0)
     pairs_e = sumr(ctx.stats()["local_pair_events"] - st_e["local_pair_events"])
@@ -873,10 +874,11 @@ def main():
                      "peak_source": "MEASURED_PEAKS.json hbm_gbs (burst copy)"},
         "clocks": clocks,
         "e2e": {"value": pairs_e / te, "unit": "gossip-steps/s",
-                "h2d_bytes_per_step": 136 * n_local * world, "d2h_bytes_per_step": 4 * d * world,
-                "note": "public API (Context.run + consensus_mean), x_bar of every step copied to pinned host "
-                        "memory on a copy stream while the next step runs (double-buffered; every copy inside "
-                        "the timed region), host wall clock, max over ranks",
+                "h2d_bytes_per_step": 136 * n_local * world, "d2h_bytes_per_step": 4 * d,
+                "note": "public API (Context.run + consensus_mean on every rank), x_bar of every step copied "
+                        "by rank 0 to pinned host memory on a copy stream while the next step runs (double-"
+                        "buffered; every copy inside the timed region; x_bar is identical on all ranks), host "
+                        "wall clock, max over ranks",
                 "synchronous": {"value": pairs_sync / te_sync, "d2h_bytes_per_step": (16 + 4 * d) * world,
                                 "note": "M_k read back and x_bar copied before the next step starts"}},
         "gpu_launches": launches,
