@@ -35,6 +35,7 @@
 // (deterministic) -- one plane per cluster (and, for GEMM1 with one cluster per tile,
 // h = tanh(z1 + b1) itself) is written, no partial planes travel through HBM.
 #include <cuda.h>
+#include <atomic>
 #include "internal.h"
 
 namespace adp {
@@ -518,9 +519,18 @@ cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, float* C, int
                        long long sstride, const GemmGather& gg, cudaStream_t s) {
   auto kern = k_gemm_tf32x3<BN, AM, BM, EPI>;
   const size_t smem = gemm_smem(BN, EPI != kEpiStore);
-  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e == cudaSuccess && gg.cluster > 8) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // function attributes once per instantiation and device (a process may drive several GPUs)
+  static std::atomic<unsigned long long> configured{0};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
   if (e != cudaSuccess) return e;
+  const unsigned long long bit = 1ull << (dev & 63);
+  if (!(configured.load(std::memory_order_acquire) & bit)) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e == cudaSuccess) e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+    configured.fetch_or(bit, std::memory_order_acq_rel);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = dim3(kGemmThreads);

@@ -194,7 +194,9 @@ struct MlpWork {                   // scratch carve-up + the fixed tensor maps, 
   int M, splits, planes, bn1, bn2; // planes: GEMM1's cluster-reduced z1 planes (0: GEMM1 writes h)
   float *z1p, *hbuf, *dz1, *dz2;
   int* idx;
-  CUtensorMap dz1_m;               // GEMM2 A (MN-major boxes of dz1); W1, GEMM1's B, is mapped per call
+  CUtensorMap dz1_m;               // GEMM2 A (MN-major boxes of dz1)
+  mutable CUtensorMap w1_m;        // GEMM1 B: W1 of the model row last used (rows never move)
+  mutable const float* w1_src = nullptr;
   cudaStream_t side = nullptr;     // the batch reductions run here beside GEMM2
   cudaEvent_t fork = nullptr, join = nullptr;
 };

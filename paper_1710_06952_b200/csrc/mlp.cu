@@ -189,9 +189,12 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
                             uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s) {
   const int I = wk.sh.n_in, H = wk.sh.n_hid, O = wk.sh.n_out, M = wk.M;
   const long long off_b1 = (long long)H * I, off_W2 = off_b1 + H, off_b2 = off_W2 + (long long)O * H;
-  CUtensorMap w1;                                             // W1 [H x I], the first H*I floats of w
-  cudaError_t e = make_tmap_k_major(&w1, w, H, I, wk.bn1);
-  if (e != cudaSuccess) return e;
+  cudaError_t e;
+  if (wk.w1_src != w) {                                       // W1 [H x I], the first H*I floats of w
+    if ((e = make_tmap_k_major(&wk.w1_m, w, H, I, wk.bn1)) != cudaSuccess) return e;
+    wk.w1_src = w;
+  }
+  const CUtensorMap& w1 = wk.w1_m;
   // the chain GEMM1 -> mid -> GEMM2 uses programmatic dependent launch: each kernel's
   // setup (GEMM: barriers, TMEM, tensor-map prefetch) overlaps its predecessor's tail
   GemmGather g1 = {};
