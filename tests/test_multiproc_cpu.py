@@ -149,3 +149,20 @@ def test_replay_plan_stale_reads_are_placed_at_their_read_points():
         assert len(cand) == 1
         g = cand[0]
         assert grow == row_of[g] and k == 50 + g   # Alg. 1 events: the key is the event's k
+
+
+def test_replay_plan_fits_the_preallocated_op_list():
+    """The engine replay sizes its device op list before the collective that lets a peer's
+    engine start (runtime.cu replay_engine: 3 K + n_local + 1 entries), so the plan of any rank
+    must fit that bound -- events, stale reads and pure averages alike, at world 1, 2 and 4."""
+    import paper_1710_06952_b200 as P
+    n, T, K = 16, 4, 600
+    e, _ = synth.ring(n)
+    ev, _ = synth.schedule_iid(n, e, K=K, T=T, seed=23, local_prob=0.3)
+    ev[::5, 3] = 1
+    for world in (1, 2, 4):
+        wr = np.array([w % world for w in range(n)], np.int32)
+        for r in range(world):
+            rows, _ = P.plan_replay(wr, r, ev, k0=7, T=T, stale_reads=True)
+            n_local = int((wr == r).sum())
+            assert len(rows) <= 3 * K + n_local + 1, (world, r, len(rows))
