@@ -373,6 +373,29 @@ def test_mlp_replay_within_1e4(P, dims, K, T):
     ctx.destroy()
 
 
+def test_mlp_batch_256_multi_tile_within_1e4(P):
+    """MLP gradients at batch M = 256: two M tiles in GEMM1 (each drawing and publishing its own
+    batch rows), GEMM1's split-K left as two cluster-reduced planes that the per-sample kernel
+    sums, and GEMM2's K = 256 contraction refilling its gathered stages -- replayed with stale
+    reads against the fp64 oracle under reading R11."""
+    I, H, Ocl = 256, 128, 10
+    n, M, T, K = 4, 256, 2, 40
+    e, r = synth.ring(n)
+    X, y = synth.mlp_data(S=2048, n_in=I, n_out=Ocl, s=0.3, seed=5)
+    x0 = synth.mlp_init(I, H, Ocl, seed=6)
+    ev, bi = synth.schedule_iid(n, e, K=K, T=T, M=M, S=X.shape[0], seed=33)
+    ctx = P.Context(e, n, x0.size, role=r, T=T, model=P.MODEL_MLP, gamma=0.005, batch_M=M, data_A=X, data_y=y,
+                    mlp_dims=(I, H, Ocl), x0=x0)
+    ctx.replay(ev, batch_idx=bi)
+    ctx.sync()
+    Xg = read_all(ctx)
+    prob = O.OracleProblem(O.MODEL_MLP, M=M, gamma=0.005, A=X, y=y, dims=(I, H, Ocl))
+    Xo, _ = O.replay(prob, np.tile(x0, (n, 1)), e, r, ev, bi, T=T)
+    ok = c11_ok(Xg, Xo)
+    assert ok.all(), (np.abs(Xg - Xo).max(), (~ok).sum())
+    ctx.destroy()
+
+
 # ------------------------------------------------- spectral-gap contraction --
 def test_pure_gossip_contracts_at_the_spectral_rate(P):
     """Config 2 property (north star): on the n = 16 bipartite ring, the seed-mean
