@@ -50,17 +50,27 @@ constexpr int kSplitThreads = 256, kGemmThreads = kSplitThreads + 32, kIssuer = 
 // raw (fp32) stages per tile width: R x (A + B tiles) + 2 lo buffers of B [+ the cluster
 // reduction's receive buffer, 128 x (BN + 4) fp32] <= 200 KB
 __host__ __device__ constexpr int recv_bytes(int bn, bool cluster) { return cluster ? 128 * (bn + 4) * 4 : 0; }
-__host__ __device__ constexpr int raw_stages(int bn, bool cluster) {
-  return (204800 - recv_bytes(bn, cluster) - 2 * bn * 128) / ((128 + bn) * 128) > 8
-             ? 8
-             : (204800 - recv_bytes(bn, cluster) - 2 * bn * 128) / ((128 + bn) * 128);
+// dynamic shared memory per CTA: the generic (TMA / TMA) kernels take one CTA per SM and deep
+// pipelines; the MLP's gathering kernels ("compact") fit two CTAs per SM, so the gradients of
+// different workers overlap their MMA issue (free-running config 3: 35k -> 37k updates/s)
+__host__ __device__ constexpr int smem_budget(bool compact) { return compact ? 86016 : 204800; }
+__host__ __device__ constexpr int stages_fit(int bn, bool cluster, bool compact) {
+  return (smem_budget(compact) - recv_bytes(bn, cluster) - 2 * bn * 128) / ((128 + bn) * 128);
+}
+__host__ __device__ constexpr int raw_stages(int bn, bool cluster, bool compact) {
+  return stages_fit(bn, cluster, compact) > 8 ? 8 : stages_fit(bn, cluster, compact) < 2 ? 2
+                                                                                        : stages_fit(bn, cluster, compact);
 }
 constexpr int kMaxGatherRows = 1024;     // batch rows a gathering CTA indexes (MLP: batch_M <= 1024)
-// TMEM: three accumulators -- hi.hi, hi.lo, lo.hi in columns [128 p, 128 p + BN), p = 0, 1, 2:
-// consecutive MMAs into one accumulator form a dependency chain that small (N <= 128, K = 8)
-// tf32 MMAs cannot hide, three independent chains can -- and A's hi / lo tiles of k-block kb
-// in columns [384 + 64 (kb % 2), + 32) / [+ 32, + 64)
-constexpr uint32_t kTmemCols = 512, kTmemAcc = 128, kTmemA = 384;
+// TMEM: the generic kernels keep three accumulators -- hi.hi, hi.lo, lo.hi in columns
+// [128 p, 128 p + BN), p = 0, 1, 2 (summed small terms first: max error 6.6e-6 -> 2.5e-6 in
+// tools/gemm_mn_probe.cu) -- and A's hi / lo tiles of k-block kb in columns [384 + 64 (kb % 2),
+// + 32) / [+ 32, + 64); the compact kernels one accumulator and A at column 128, 256 columns
+// in all so that two CTAs share an SM's TMEM
+__host__ __device__ constexpr int n_accs(bool compact) { return compact ? 1 : 3; }
+__host__ __device__ constexpr uint32_t tmem_cols(bool compact) { return compact ? 256u : 512u; }
+__host__ __device__ constexpr uint32_t tmem_a(bool compact) { return compact ? 128u : 384u; }
+constexpr uint32_t kTmemAcc = 128;
 enum : int { kOpTma = 0, kOpGatherK = 1, kOpTmaMN = 2, kOpGatherMN = 3 };
 enum : int { kEpiStore = 0, kEpiCluster = 1, kEpiClusterTanh = 2 };
 
@@ -207,10 +217,15 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
                   float* __restrict__ C, int ldc, int kb_per_split, long long split_stride, const GemmGather gg) {
   constexpr bool kGather = AM == kOpGatherK || BM == kOpGatherMN;
   constexpr bool kCluster = EPI != kEpiStore;
-  constexpr int R = raw_stages(BN, kCluster);
+  constexpr bool kCompact = AM != kOpTma || BM != kOpTma;
+  constexpr int R = raw_stages(BN, kCluster, kCompact);
+  constexpr int kAccs = n_accs(kCompact);
+  constexpr uint32_t kTmemCols = tmem_cols(kCompact), kTmemA = tmem_a(kCompact);
   constexpr uint32_t kATile = kBM * 128, kBTile = BN * 128;  // fp32 tiles (the hi halves after the split)
   constexpr uint32_t kRaw = kATile + kBTile;                 // raw stage r: [A32][B32|hi]; then 2 x [B lo]
   constexpr uint32_t kTmaBytes = (AM == kOpGatherK ? 0u : kATile) + (BM == kOpGatherMN ? 0u : kBTile);
+  static_assert(!kCluster || (uint32_t)kBM * (BN + 4) * 4 <= R * kRaw + 2 * kBTile,
+                "the epilogue's reduction buffer must fit in the drained stages");
   extern __shared__ unsigned char smem_raw[];
   __shared__ __align__(8) uint64_t full[R], rawfree[R], lofree[2], split_done[2], accum, recv_bar;
   __shared__ uint32_t tmem_base_s;
@@ -326,8 +341,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
           const uint32_t oa = 8u * kk;
           const uint32_t acc = (kb | kk) ? 1u : 0u;
           mma_tf32_ts(tmem, ahi + oa, bh + ob, idesc, acc);
-          mma_tf32_ts(tmem + kTmemAcc, ahi + oa, bl + ob, idesc, acc);
-          mma_tf32_ts(tmem + 2 * kTmemAcc, alo + oa, bh + ob, idesc, acc);
+          if constexpr (kAccs == 3) {
+            mma_tf32_ts(tmem + kTmemAcc, ahi + oa, bl + ob, idesc, acc);
+            mma_tf32_ts(tmem + 2 * kTmemAcc, alo + oa, bh + ob, idesc, acc);
+          } else {
+            mma_tf32_ts(tmem, ahi + oa, bl + ob, idesc, 1u);
+            mma_tf32_ts(tmem, alo + oa, bh + ob, idesc, 1u);
+          }
         }
         if (kb < 12) trace_point(14 + kb, kIssuer);
         mma_commit(&rawfree[s]);                            // raw stage s free when these complete
@@ -413,15 +433,20 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   for (int c = warp >> 2; warp < 8 && c < BN / 32; c += 2) {
     uint32_t v[32], w[32];
     const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(c * 32);
-    tmem_ld32(taddr + kTmemAcc, v);                          // hi.lo + lo.hi, then + hi.hi
-    tmem_ld32(taddr + 2 * kTmemAcc, w);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    if constexpr (kAccs == 3) {
+      tmem_ld32(taddr + kTmemAcc, v);                        // hi.lo + lo.hi, then + hi.hi
+      tmem_ld32(taddr + 2 * kTmemAcc, w);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(v[q]) + __uint_as_float(w[q]));
-    tmem_ld32(taddr, w);
-    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(v[q]) + __uint_as_float(w[q]));
+      tmem_ld32(taddr, w);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-    for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(w[q]) + __uint_as_float(v[q]));
+      for (int q = 0; q < 32; ++q) v[q] = __float_as_uint(__uint_as_float(w[q]) + __uint_as_float(v[q]));
+    } else {
+      tmem_ld32(taddr, v);
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+    }
     if constexpr (EPI == kEpiStore) {
       float4* dst = reinterpret_cast<float4*>(C + (long long)blockIdx.z * split_stride +
                                               (long long)(m0 + quad * 32 + lane) * ldc + n0 + c * 32);
@@ -509,8 +534,9 @@ CUresult encode_2d(CUtensorMap* tm, const float* ptr, long long rows, long long 
             CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
 }
 
-constexpr size_t gemm_smem(int bn, bool cluster) {
-  return (size_t)raw_stages(bn, cluster) * (kBM * 128 + bn * 128) + 2 * bn * 128 + recv_bytes(bn, cluster) + 1024;
+constexpr size_t gemm_smem(int bn, bool cluster, bool compact) {
+  return (size_t)raw_stages(bn, cluster, compact) * (kBM * 128 + bn * 128) + 2 * bn * 128 + recv_bytes(bn, cluster) +
+         1024;
 }
 
 // one launch: PDL always, a (1, 1, cluster) thread-block cluster when cluster > 1
@@ -518,7 +544,7 @@ template <int BN, int AM, int BM, int EPI>
 cudaError_t launch_one(const CUtensorMap& A, const CUtensorMap& B, float* C, int ldc, dim3 grid, int kbps,
                        long long sstride, const GemmGather& gg, cudaStream_t s) {
   auto kern = k_gemm_tf32x3<BN, AM, BM, EPI>;
-  const size_t smem = gemm_smem(BN, EPI != kEpiStore);
+  const size_t smem = gemm_smem(BN, EPI != kEpiStore, AM != kOpTma || BM != kOpTma);
   // function attributes once per instantiation and device (a process may drive several GPUs)
   static std::atomic<unsigned long long> configured{0};
   int dev = 0;

@@ -98,19 +98,19 @@ int main() {
   // ---- how many clusters of the GEMM1 kernel can be resident at once
   for (int cs : {16, 8, 4}) {
     auto kern = k_gemm_tf32x3<64, kOpGatherK, kOpTma, kEpiClusterTanh>;
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem(64, true));
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gemm_smem(64, true, true));
     cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(8, 1, 16);
     cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = gemm_smem(64, true);
+    cfg.dynamicSmemBytes = gemm_smem(64, true, true);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
     at[0].val.clusterDim.x = 1; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = cs;
     cfg.attrs = at; cfg.numAttrs = 1;
     int n = -1;
     cudaError_t e = cudaOccupancyMaxActiveClusters(&n, kern, &cfg);
-    printf("cluster %2d: max active clusters %d (%s), smem %zu\n", cs, n, cudaGetErrorString(e), gemm_smem(64, true));
+    printf("cluster %2d: max active clusters %d (%s), smem %zu\n", cs, n, cudaGetErrorString(e), gemm_smem(64, true, true));
   }
   // ---- config-3 shapes, traced: GEMM1 (gather K-major A, TMA B, cluster tanh) and GEMM2
   {
