@@ -211,6 +211,58 @@ __device__ __forceinline__ float tf32_lo(float v) {
   return __uint_as_float((__float_as_uint(r) + 0x1000u) & 0xFFFFE000u);
 }
 
+// GEMM2's extra CTAs: the MLP's batch reductions (reading R18) db1[u] = sum_b dz1[b][u],
+// dW2[o][u] = sum_b dz2[b][o] h[b][u], db2[o] = sum_b dz2[b][o].  Unit c owns hidden units
+// [32 c, 32 c + 32); thread (u, q) sums samples b = q, q + 8, .. (coalesced over u), and the 8
+// partial sums of each output are added in order q = 0..7 (deterministic); CTA 0's last warp
+// does db2.  Runs beside the dW1 tiles, so the gradient needs no side stream.
+constexpr int kRedMaxOut = 32;
+__device__ void mlp_batch_reduce(const GemmGather& gg, int c, unsigned char* sbase) {
+  const int tid = threadIdx.x, H = gg.r_H, O = gg.r_O, M = gg.r_M;
+  float* part = reinterpret_cast<float*>(sbase);            // [8][O + 1][32]
+  pdl_wait();                                               // h, dz1, dz2 of the per-sample kernel
+  pdl_trigger();
+  if (tid < 256) {
+    const int ul = tid & 31, q = tid >> 5, u = c * 32 + ul;
+    float a1 = 0.0f, aw[kRedMaxOut];
+#pragma unroll
+    for (int o = 0; o < kRedMaxOut; ++o) aw[o] = 0.0f;
+    if (u < H) {
+#pragma unroll 4
+      for (int b = q; b < M; b += 8) {
+        const float hv = gg.r_h[(long long)b * H + u];
+        a1 += gg.r_dz1[(long long)b * H + u];
+#pragma unroll
+        for (int o = 0; o < kRedMaxOut; ++o) {
+          if (o >= O) break;
+          aw[o] = fmaf(gg.r_dz2[(long long)b * O + o], hv, aw[o]);
+        }
+      }
+    }
+    part[(q * (O + 1)) * 32 + ul] = a1;
+#pragma unroll
+    for (int o = 0; o < kRedMaxOut; ++o) {
+      if (o >= O) break;
+      part[(q * (O + 1) + 1 + o) * 32 + ul] = aw[o];
+    }
+  }
+  __syncthreads();
+  for (int t = tid; t < (O + 1) * 32; t += blockDim.x) {   // output row r (0: db1, 1 + o: dW2[o]), unit ul
+    const int r = t >> 5, ul = t & 31, u = c * 32 + ul;
+    if (u >= H) continue;
+    float acc = 0.0f;
+    for (int q = 0; q < 8; ++q) acc += part[(q * (O + 1) + r) * 32 + ul];
+    if (r == 0) gg.r_g[gg.r_off_b1 + u] = acc;
+    else gg.r_g[gg.r_off_W2 + (long long)(r - 1) * H + u] = acc;
+  }
+  if (c == 0 && tid >= 256 && tid - 256 < O) {              // db2: one lane per output
+    const int o = tid - 256;
+    float acc = 0.0f;
+    for (int b = 0; b < M; ++b) acc += gg.r_dz2[(long long)b * O + o];
+    gg.r_g[gg.r_off_b2 + o] = acc;
+  }
+}
+
 template <int BN, int AM, int BM, int EPI>
 __global__ void __launch_bounds__(kGemmThreads, 1)
     k_gemm_tf32x3(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
@@ -234,6 +286,13 @@ __global__ void __launch_bounds__(kGemmThreads, 1)
   const uint32_t base = (smem_u32(smem_raw) + 1023u) & ~1023u;    // SW128 needs 1024-B alignment
   unsigned char* sbase = smem_raw + (base - smem_u32(smem_raw));
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  if constexpr (BM == kOpGatherMN) {                          // GEMM2's batch-reduction CTAs
+    if (gg.red_ctas && (int)blockIdx.x >= (int)gridDim.x - gg.red_ctas) {   // unit c owns 32 hidden units
+      mlp_batch_reduce(gg, ((int)blockIdx.x - ((int)gridDim.x - gg.red_ctas)) * (int)gridDim.y + (int)blockIdx.y,
+                       sbase);
+      return;
+    }
+  }
   const int n0 = blockIdx.x * BN, m0 = blockIdx.y * kBM;
   const int kb0 = blockIdx.z * kb_per_split;
   trace_point(0);
@@ -658,7 +717,9 @@ cudaError_t launch_mlp_gemm2(const CUtensorMap& A, const GemmGather& gg, float* 
                              cudaStream_t s) {
   if (M % kBM || K % kBK || K > kMaxGatherRows || (bn != 64 && bn != 96) || N % bn || gg.cluster != 1)
     return cudaErrorInvalidValue;
-  const dim3 grid(N / bn, M / kBM, 1);
+  // red_ctas extra columns of CTAs x the M / 128 rows give the batch reduction's 32-unit slices
+  if (gg.red_ctas && (gg.r_O > kRedMaxOut || gg.red_ctas * (M / kBM) * 32 < gg.r_H)) return cudaErrorInvalidValue;
+  const dim3 grid(N / bn + gg.red_ctas, M / kBM, 1);
   if (bn == 96) return launch_one<96, kOpTmaMN, kOpGatherMN, kEpiStore>(A, A, C, N, grid, K / kBK, 0, gg, s);
   return launch_one<64, kOpTmaMN, kOpGatherMN, kEpiStore>(A, A, C, N, grid, K / kBK, 0, gg, s);
 }

@@ -174,6 +174,12 @@ struct GemmGather {                // gathered-operand / epilogue arguments (MLP
   int S;
   int cluster;                     // CTAs per cluster along z (split-K reduced in DSMEM), 1 = none
   const float* bias;               // GEMM1 epilogue: h = tanh(z + bias)
+  // GEMM2's extra CTAs (the last red_ctas of grid.x): the MLP's batch reductions db1, dW2, db2
+  // over h, dz1 [M x H] and dz2 [M x O] into g (offsets of b1 / W2 / b2)
+  int red_ctas, r_M, r_H, r_O;
+  const float *r_h, *r_dz1, *r_dz2;
+  float* r_g;
+  long long r_off_b1, r_off_W2, r_off_b2;
 };
 cudaError_t make_tmap_k_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols, int box_rows);
 cudaError_t make_tmap_mn_major(CUtensorMap* tm, const float* ptr, long long rows, long long cols);
@@ -185,9 +191,9 @@ cudaError_t launch_mlp_gemm1(const CUtensorMap& B, const GemmGather& gg, float* 
 cudaError_t launch_mlp_gemm2(const CUtensorMap& A, const GemmGather& gg, float* C, int M, int N, int K, int bn,
                              cudaStream_t s);
 
-// MLP (kind 5): tcgen05-backed gradient (mlp.cu), 3 launches on the stream + 1 beside:
+// MLP (kind 5): tcgen05-backed gradient (mlp.cu), 3 launches:
 //   GEMM1 (batch draw, X rows gathered, split-K reduced in DSMEM) -> per-sample mid
-//   (tanh, output layer, softmax-CE backward, dz1) -> GEMM2 || batch reductions
+//   (tanh, output layer, softmax-CE backward, dz1) -> GEMM2 (+ the batch reductions in extra CTAs)
 struct MlpShape { int n_in, n_hid, n_out; };
 struct MlpWork {                   // scratch carve-up + the fixed tensor maps, built once per context
   MlpShape sh;
@@ -197,15 +203,13 @@ struct MlpWork {                   // scratch carve-up + the fixed tensor maps, 
   CUtensorMap dz1_m;               // GEMM2 A (MN-major boxes of dz1)
   mutable CUtensorMap w1_m;        // GEMM1 B: W1 of the model row last used (rows never move)
   mutable const float* w1_src = nullptr;
-  cudaStream_t side = nullptr;     // the batch reductions run here beside GEMM2
-  cudaEvent_t fork = nullptr, join = nullptr;
 };
 size_t mlp_scratch_floats(const MlpShape& sh, int M);
 bool mlp_supported(const MlpShape& sh, int M);
 cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch);
 cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int S, const int* idx,
                             uint2 batch_key, unsigned long long k, const float* w, float* g, cudaStream_t s);
-constexpr int kMlpLaunches = 4;
+constexpr int kMlpLaunches = 3;
 
 // one kernel of each translation unit (CUDA module), see preload_modules()
 const void* kernels_module_anchor();

@@ -41,6 +41,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_event(float* xi, float* xj, con
                                                     const float* xhat, long long d, long long n4,
                                                     float gamma, QuadParams q, uint32_t kk,
                                                     const unsigned long long* guard) {
+  pdl_wait();                               // launched with PDL: the predecessor's rows / gradient
+  pdl_trigger();
   if (guard && *guard == ~0ull) return;     // the event's lock wait timed out (error latched): skip
   const long long per = (n4 + gridDim.x - 1) / gridDim.x;
   const long long lo = (long long)blockIdx.x * per;
@@ -568,15 +570,17 @@ __global__ void k_super_commit(LogEntry* log, long long log_cap, const unsigned 
 template <bool P, int G>
 cudaError_t ev(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
                float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s, const unsigned long long* guard) {
-  k_event<P, G><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk, guard);
-  return cudaGetLastError();
+  // programmatic dependent launch: the event's launch and prologue overlap its predecessor (in
+  // the MLP chain, GEMM2) and it waits for that grid at griddepcontrol.wait
+  return launch_pdl(k_event<P, G>, dim3(stream_grid(n4)), dim3(kThreads), 0, s, xi, xj, g, xh, d, n4, gamma, q, kk,
+                    guard);
 }
 
 template <int G>
 cudaError_t ev_ff(float* xi, float* xj, const float* g, const float* xh, long long d, long long n4,
                   float gamma, const QuadParams& q, uint32_t kk, cudaStream_t s, const unsigned long long* guard) {
-  k_event<true, G, true><<<stream_grid(n4), kThreads, 0, s>>>(xi, xj, g, xh, d, n4, gamma, q, kk, guard);
-  return cudaGetLastError();
+  return launch_pdl(k_event<true, G, true>, dim3(stream_grid(n4)), dim3(kThreads), 0, s, xi, xj, g, xh, d, n4, gamma,
+                    q, kk, guard);
 }
 
 }  // namespace

@@ -1,7 +1,7 @@
 // mlp.cu -- minibatch gradient of the 2-layer MLP (config 3, reading R18):
 //   Z1 = X_b W1^T + b1, H = tanh(Z1), Z2 = H W2^T + b2, loss = sum_b CE(softmax(Z2_b), y_b)
 //   g = sum over the batch of dloss/dw  (a SUM), flat layout [W1 | b1 | W2 | b2].
-// Three launches on the stream per gradient, plus one beside it:
+// Three launches per gradient:
 //   1. GEMM1  h [M x H] = tanh(X_b W1^T + b1) on tcgen05 (3xTF32): draws the batch indices
 //             (explicit or device Philox) and publishes them, gathers the X rows itself
 //             (cp.async into the swizzled tiles: X_b is never written), W1 straight from the
@@ -11,8 +11,8 @@
 //   2. mid:   one CTA per sample -- h = tanh(sum of the planes + b1), the N = O output layer,
 //             softmax-CE backward, dz1, dz2
 //   3. GEMM2  dW1 [H x I] = dZ1^T X_b into g: dZ1 read MN-major by TMA (no transpose),
-//             X rows gathered again (MN-major), with the batch reductions (db1, dW2, db2)
-//             running beside it on a side stream (fork / join events)
+//             X rows gathered again (MN-major); extra CTAs of the same launch compute the
+//             batch reductions (db1, dW2, db2)
 // The tf32 hi / lo split of every operand happens in shared memory (gemm.cu).
 #include "internal.h"
 
@@ -99,38 +99,6 @@ __global__ void __launch_bounds__(1024) k_mlp_mid(const float* __restrict__ z1p,
   dz1buf[(long long)b * H + u] = dz;
 }
 
-// batch reductions (reading R18): db1[u] = sum_b dz1[b][u], dW2[o][u] = sum_b dz2[b][o] h[b][u],
-// db2[o] = sum_b dz2[b][o] -- one warp per output, lane l sums samples l, l + 32, ..., then a
-// shuffle tree in a fixed order (deterministic).  Runs on the side stream beside GEMM2.
-__global__ void __launch_bounds__(256) k_mlp_reduce(const float* __restrict__ hbuf, const float* __restrict__ dz1,
-                                                    const float* __restrict__ dz2, int M, int H, int O,
-                                                    float* __restrict__ g, long long off_b1, long long off_W2,
-                                                    long long off_b2) {
-  const long long n = (long long)H + (long long)O * H + O;
-  const int lane = threadIdx.x & 31;
-  for (long long q = ((long long)blockIdx.x * blockDim.x + threadIdx.x) >> 5; q < n;
-       q += ((long long)gridDim.x * blockDim.x) >> 5) {
-    float acc = 0.0f;
-    if (q < H) {
-      for (int b = lane; b < M; b += 32) acc += dz1[(long long)b * H + q];
-    } else if (q < H + (long long)O * H) {
-      const long long r = q - H;
-      const int o = (int)(r / H), u = (int)(r % H);
-      for (int b = lane; b < M; b += 32) acc = fmaf(dz2[(long long)b * O + o], hbuf[(long long)b * H + u], acc);
-    } else {
-      const int o = (int)(q - H - (long long)O * H);
-      for (int b = lane; b < M; b += 32) acc += dz2[(long long)b * O + o];
-    }
-#pragma unroll
-    for (int w = 16; w; w >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, w);
-    if (lane == 0) {
-      if (q < H) g[off_b1 + q] = acc;
-      else if (q < H + (long long)O * H) g[off_W2 + (q - H)] = acc;
-      else g[off_b2 + (q - H - (long long)O * H)] = acc;
-    }
-  }
-}
-
 }  // namespace
 
 // GEMM1 split-K: Z1 is only M x H (8 tiles of 128 x 64 at config 3), so K is split over a
@@ -176,12 +144,6 @@ cudaError_t mlp_plan(MlpWork& wk, const MlpShape& sh, int M, float* scratch) {
   wk.dz1 = p; p += (size_t)M * H;
   wk.dz2 = p; p += (size_t)M * sh.n_out;
   wk.idx = reinterpret_cast<int*>(p);
-  cudaError_t e;
-  if (!wk.side) {
-    if ((e = cudaStreamCreateWithFlags(&wk.side, cudaStreamNonBlocking)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&wk.fork, cudaEventDisableTiming)) != cudaSuccess) return e;
-    if ((e = cudaEventCreateWithFlags(&wk.join, cudaEventDisableTiming)) != cudaSuccess) return e;
-  }
   return make_tmap_mn_major(&wk.dz1_m, wk.dz1, M, H);          // GEMM2 A: 32 x 32 boxes of dz1 [M x H]
 }
 
@@ -205,18 +167,15 @@ cudaError_t launch_mlp_grad(const MlpWork& wk, const float* X, const int* y, int
   if ((e = launch_pdl(k_mlp_mid, dim3(M), dim3(H), 0, s, (const float*)wk.z1p, wk.planes, M, wk.hbuf, H, O, w,
                       off_b1, off_W2, off_b2, y, (const int*)wk.idx, wk.dz1, wk.dz2)) != cudaSuccess)
     return e;
-  // the batch reductions on the side stream, beside GEMM2 (which leaves SMs free)
-  if ((e = cudaEventRecord(wk.fork, s)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(wk.side, wk.fork, 0)) != cudaSuccess) return e;
-  const long long nred = (long long)H + (long long)O * H + O;
-  k_mlp_reduce<<<(unsigned)((nred * 32 + 255) / 256), 256, 0, wk.side>>>(wk.hbuf, wk.dz1, wk.dz2, M, H, O, g, off_b1,
-                                                                          off_W2, off_b2);
-  // dW1 in 128 x 96 tiles (I = 3072: 4 x 32 = 128 CTAs, one wave)
+  // dW1 in 128 x 96 tiles (I = 3072: 4 x 32 = 128 CTAs) and, in extra CTAs of the same launch,
+  // the batch reductions db1, dW2, db2
   GemmGather g2 = {};
   g2.x = X; g2.ld = I; g2.idx = wk.idx; g2.cluster = 1;
+  const int units = (H + 31) / 32, rows = H / 128;
+  g2.red_ctas = (units + rows - 1) / rows;
+  g2.r_M = M; g2.r_H = H; g2.r_O = O; g2.r_h = wk.hbuf; g2.r_dz1 = wk.dz1; g2.r_dz2 = wk.dz2; g2.r_g = g;
+  g2.r_off_b1 = off_b1; g2.r_off_W2 = off_W2; g2.r_off_b2 = off_b2;
   if ((e = launch_mlp_gemm2(wk.dz1_m, g2, g, H, I, M, wk.bn2, s)) != cudaSuccess) return e;
-  if ((e = cudaEventRecord(wk.join, wk.side)) != cudaSuccess) return e;
-  if ((e = cudaStreamWaitEvent(s, wk.join, 0)) != cudaSuccess) return e;
   return cudaGetLastError();
 }
 

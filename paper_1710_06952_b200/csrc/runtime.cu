@@ -356,13 +356,7 @@ adpsgd_status ensure_gslots(adpsgd_ctx* c, int count) {
   return ADPSGD_OK;
 }
 
-void release_mlp_work(MlpWork& w) {
-  if (w.side) cudaStreamDestroy(w.side);
-  if (w.fork) cudaEventDestroy(w.fork);
-  if (w.join) cudaEventDestroy(w.join);
-  w.side = nullptr;
-  w.fork = w.join = nullptr;
-}
+void release_mlp_work(MlpWork& w) { w = MlpWork{}; }
 
 // one MLP scratch (gathered batch, partial planes, tensor maps, side stream) per stream lane
 adpsgd_status ensure_mlp_scratch(adpsgd_ctx* c, int lanes = 1) {
