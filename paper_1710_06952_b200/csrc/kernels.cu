@@ -56,6 +56,8 @@ __global__ void __launch_bounds__(kThreads, 2) k_event(float* xi, float* xj, con
 __global__ void __launch_bounds__(kThreads) k_quad_grad(const float* __restrict__ xhat,
                                                         float* __restrict__ g, long long d,
                                                         long long n4, QuadParams q, uint32_t kk) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const float4 x = ld_cg4(reinterpret_cast<const float4*>(xhat) + i);
@@ -89,6 +91,8 @@ __global__ void __launch_bounds__(kLinThreads) k_linear_grad(int kind, const flo
                                                              uint2 key, unsigned long long k,
                                                              const float* __restrict__ xhat,
                                                              float* __restrict__ g, long long d) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   __shared__ float coef[kMaxM];
   __shared__ int sidx[kMaxM];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
@@ -202,6 +206,8 @@ __global__ void __launch_bounds__(kLinThreadsV) k_linear_grad_v(int kind, const 
                                                                 uint2 key, unsigned long long k,
                                                                 const float* __restrict__ xhat,
                                                                 float* __restrict__ g, long long d) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   __shared__ LinSmem sm;
   linear_grad_v_body(sm, kind, A, b, S, idx_in, M, key, k, xhat, g, d);
 }
@@ -246,6 +252,8 @@ __global__ void __launch_bounds__(kLinThreadsV) k_lin_replay(LinReplayParams p) 
 }
 
 __global__ void k_copy(float4* __restrict__ dst, const float4* __restrict__ src, long long n4) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x)
     st_cg4(dst + i, ld_cg4(src + i));
@@ -427,6 +435,8 @@ __global__ void __launch_bounds__(kThreads) k_ar_grad_sum(const float* __restric
                                                           long long n4, QuadParams q,
                                                           unsigned long long k_base, int n_local,
                                                           const int* __restrict__ local_ids) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
     const float4 xv4 = ld_cg4(reinterpret_cast<const float4*>(x) + i);
@@ -448,6 +458,8 @@ __global__ void __launch_bounds__(kThreads) k_ar_grad_sum(const float* __restric
 __global__ void __launch_bounds__(kThreads) k_ar_update(float* __restrict__ x,
                                                         const float* __restrict__ gsum, float gamma,
                                                         int n, long long d, long long n4) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   const float nf = (float)n;
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4;
        i += (long long)gridDim.x * blockDim.x) {
@@ -473,6 +485,8 @@ __global__ void __launch_bounds__(kThreads) k_dpsgd(const float* const* __restri
                                                     long long d_pad, long long d, QuadParams q, int model,
                                                     float gamma, unsigned long long k_base,
                                                     const int* __restrict__ local_ids) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   __shared__ const float4* snb[kDpMaxDeg];
   const int l = blockIdx.y;
   const float4* xi = reinterpret_cast<const float4*>(xin + (long long)l * d_pad);
@@ -523,6 +537,8 @@ __global__ void k_init_rows(float* X, int n_rows, long long d_pad, long long d, 
 
 __global__ void k_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
                               long long k, int i, int j, unsigned int flags, int grad) {
+  pdl_wait();                               // PDL launch: wait for the predecessor grid
+  pdl_trigger();
   atomicMax(&gctl0->ticket, (unsigned long long)(k + 1));
   atomicMax(&gctl0->committed, (unsigned long long)(k + 1));
   if (grad) atomicAdd(&ctl_i->updates, 1ull);
@@ -618,8 +634,8 @@ cudaError_t launch_event(float* xi, float* xj, const float* g, const float* xhat
 
 cudaError_t launch_quad_grad(const float* xhat, float* g, long long d, long long n4,
                              const QuadParams& q, unsigned long long k, cudaStream_t s) {
-  k_quad_grad<<<stream_grid(n4), kThreads, 0, s>>>(xhat, g, d, n4, q, quad_event_key_h(q.noise_key, k));
-  return cudaGetLastError();
+  return launch_pdl(k_quad_grad, dim3(stream_grid(n4)), dim3(kThreads), 0, s, xhat, g, d, n4, q,
+                    quad_event_key_h(q.noise_key, k));
 }
 
 cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, const int* idx,
@@ -627,10 +643,9 @@ cudaError_t launch_linear_grad(int kind, const float* A, const float* b, int S, 
                                float* g, long long d, cudaStream_t s) {
   if (M > kMaxM) return cudaErrorInvalidValue;
   if (d % 4 == 0)
-    k_linear_grad_v<<<1, kLinThreadsV, 0, s>>>(kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
-  else
-    k_linear_grad<<<1, kLinThreads, 0, s>>>(kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
-  return cudaGetLastError();
+    return launch_pdl(k_linear_grad_v, dim3(1), dim3(kLinThreadsV), 0, s, kind, A, b, S, idx, M, batch_key, k, xhat, g,
+                      d);
+  return launch_pdl(k_linear_grad, dim3(1), dim3(kLinThreads), 0, s, kind, A, b, S, idx, M, batch_key, k, xhat, g, d);
 }
 
 cudaError_t launch_lin_replay(const LinReplayParams& p, cudaStream_t s) {
@@ -641,9 +656,8 @@ cudaError_t launch_lin_replay(const LinReplayParams& p, cudaStream_t s) {
 }
 
 cudaError_t launch_copy(float* dst, const float* src, long long n4, cudaStream_t s) {
-  k_copy<<<stream_grid(n4), kThreads, 0, s>>>(reinterpret_cast<float4*>(dst),
-                                              reinterpret_cast<const float4*>(src), n4);
-  return cudaGetLastError();
+  return launch_pdl(k_copy, dim3(stream_grid(n4)), dim3(kThreads), 0, s, reinterpret_cast<float4*>(dst),
+                    reinterpret_cast<const float4*>(src), n4);
 }
 
 cudaError_t launch_fill_hash(float* x, long long n, uint32_t seed, cudaStream_t s) {
@@ -707,21 +721,19 @@ cudaError_t launch_consensus_mk(const float* X, int n_rows, long long d_pad, lon
 cudaError_t launch_ar_grad_sum(const float* x, float* gsum, long long d, long long n4,
                                const QuadParams& q, unsigned long long k_base, int n_local,
                                const int* local_ids, cudaStream_t s) {
-  k_ar_grad_sum<<<stream_grid(n4), kThreads, 0, s>>>(x, gsum, d, n4, q, k_base, n_local, local_ids);
-  return cudaGetLastError();
+  return launch_pdl(k_ar_grad_sum, dim3(stream_grid(n4)), dim3(kThreads), 0, s, x, gsum, d, n4, q, k_base, n_local,
+                    local_ids);
 }
 
 cudaError_t launch_ar_update(float* x, const float* gsum, float gamma, int n, long long d,
                              long long n4, cudaStream_t s) {
-  k_ar_update<<<stream_grid(n4), kThreads, 0, s>>>(x, gsum, gamma, n, d, n4);
-  return cudaGetLastError();
+  return launch_pdl(k_ar_update, dim3(stream_grid(n4)), dim3(kThreads), 0, s, x, gsum, gamma, n, d, n4);
 }
 
 cudaError_t launch_step_commit(GlobalCtl* gctl0, WorkerCtl* ctl_i, LogEntry* log, long long log_cap,
                                long long k, int i, int j, unsigned int flags, int grad,
                                cudaStream_t s) {
-  k_step_commit<<<1, 1, 0, s>>>(gctl0, ctl_i, log, log_cap, k, i, j, flags, grad);
-  return cudaGetLastError();
+  return launch_pdl(k_step_commit, dim3(1), dim3(1), 0, s, gctl0, ctl_i, log, log_cap, k, i, j, flags, grad);
 }
 
 cudaError_t launch_super_lock(unsigned int* lock, unsigned long long* ticket, unsigned long long* kout,
@@ -748,9 +760,8 @@ cudaError_t launch_dpsgd(const float* const* nbr, const int* deg, const float* w
   // all rows of the round in one launch: ~2 waves of 512-thread CTAs over the GPU
   const int bx = (int)std::min<long long>((d_pad / 4 + kThreads - 1) / kThreads,
                                           std::max(1LL, 4LL * sm_count() / n_local));
-  k_dpsgd<<<dim3(bx, n_local), kThreads, 0, s>>>(nbr, deg, w_self, w_nb, xin, xout, d_pad, d, q, model, gamma, k_base,
-                                                 local_ids);
-  return cudaGetLastError();
+  return launch_pdl(k_dpsgd, dim3(bx, n_local), dim3(kThreads), 0, s, nbr, deg, w_self, w_nb, xin, xout, d_pad, d, q,
+                    model, gamma, k_base, local_ids);
 }
 
 cudaError_t launch_delay(unsigned long long ns, cudaStream_t s) {
