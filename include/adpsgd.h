@@ -377,8 +377,10 @@ adpsgd_status adpsgd_plan_replay(int32_t n, const int32_t* worker_rank, int32_t 
  * C[M x N] = A[M x K] . B[N x K]^T, fp32 row-major DEVICE pointers on the current
  * device, computed as 3xTF32 (hi*hi + hi*lo + lo*hi, the split done in shared
  * memory) with tcgen05.mma into TMEM, split-K over `splits` CTAs per tile
- * (partials summed in a fixed order).  Requires M % 128 == 0, N % 64 == 0,
- * K % (32 * splits) == 0.  Synchronous.                                        */
+ * (partials summed in a fixed order: in distributed shared memory across a
+ * thread-block cluster when splits is a power of two <= 16, else through
+ * partial planes).  Requires M % 128 == 0, N % 64 == 0, K % (32 * splits) == 0.
+ * Synchronous.                                                                  */
 adpsgd_status adpsgd_gemm_tf32x3(const float* A, const float* B, float* C, int32_t M, int32_t N, int32_t K,
                                  int32_t splits);
 
