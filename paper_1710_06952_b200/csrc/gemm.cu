@@ -5,16 +5,15 @@
 // Used by the MLP minibatch gradient (config 3): Z1 = X_b W1^T and
 // dW1 = dZ1^T X_b.  Accuracy ~fp32 via the 3xTF32 split:
 //   A = A_hi + A_lo, B = B_hi + B_lo (hi = trunc_tf32(x), lo = rna_tf32(x - hi)),
-//   C ~= A_hi B_hi + A_hi B_lo + A_lo B_hi   (three tcgen05.mma into one TMEM accumulator).
-// The operands are read ONCE, as fp32: a 128-byte-swizzled fp32 tile lands in shared
-// memory and serves as hi as is (the tensor core drops the low 13 mantissa bits), and
-// the CTA writes lo = rna_tf32(x - hi) into a second tile of the same swizzled layout --
-// no hi/lo planes are ever written to HBM.
+//   C ~= A_hi B_hi + A_hi B_lo + A_lo B_hi   (three tcgen05.mma per K step).
+// The operands are read ONCE, as fp32: a staged fp32 word serves as hi as is (the tensor core
+// drops the low 13 mantissa bits) and lo = rna_tf32(x - hi) is derived on chip -- no hi/lo
+// planes are ever written to HBM.
 //
-// CTA = 256 threads, tile 128 x BN (BN = 32 / 64 / 96 / 128), k-block 32 fp32.  The raw fp32
-// tiles of R(BN) = 8 / 6 / 5 / 4 k-blocks (fewer with a cluster reduction buffer) are in flight
-// at once; the lo tiles live in two buffers of their own.  Each operand arrives in one of three ways
-// (template AM / BM):
+// CTA = 9 warps, tile 128 x BN (BN = 32 / 64 / 96 / 128), k-block 32 fp32.  Raw fp32 tiles of
+// several k-blocks are in flight (generic kernels: up to 8 / 7 / 6 / 5 with one CTA per SM;
+// the MLP's gathering kernels are "compact", two CTAs per SM).  Each operand arrives in one of
+// three ways (template AM / BM):
 //   kOpTma      K-major tile by a TMA tensor load (cp.async.bulk.tensor, SWIZZLE_128B)
 //   kOpTmaMN    MN-major tile by TMA (the contraction runs over the rows of a row-major
 //               matrix: dW1 = dZ1^T X_b reads dZ1 [batch x H] without a transpose)
@@ -23,9 +22,11 @@
 //               the minibatch is never materialised in HBM
 // and completes on the stage's mbarrier (TMA: complete_tx; cp.async: one
 // cp.async.mbarrier.arrive.noinc per thread).  Per k-block:
-//   all threads  : write lo of the staged tiles, fence.proxy.async, barrier
-//   thread 32    : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, M=128, N=BN, K=8)
-//   producers    : refill the stage the previous k-block used once its MMAs drained it
+//   warps 0-3 : A's row (thread = row) -> TMEM as hi and lo (tcgen05.st)
+//   warps 4-7 : B's lo tile into a shared-memory buffer (hi stays in the staged tile)
+//   warp 8    : MMA issuer (tcgen05.mma.cta_group::1.kind::tf32, A from TMEM, B from shared
+//               memory, M = 128, N = BN, K = 8) and the TMA loads / refills
+// split and MMA hand over through mbarriers, so the split of k-block kb + 1 overlaps kb's MMAs.
 // Epilogue (template EPI): kEpiStore writes the CTA's split-K plane; kEpiCluster /
 // kEpiClusterTanh reduce the split-K partials of a thread-block cluster (consecutive
 // blockIdx.z of one output tile) in distributed shared memory: CTA p owns rows
@@ -122,14 +123,6 @@ __device__ __forceinline__ uint32_t mn_off(int r, int j) {
 __host__ __device__ constexpr uint32_t tf32_idesc(int M, int N, bool a_mn, bool b_mn) {
   return (1u << 4) | (2u << 7) | (2u << 10) | (a_mn ? 1u << 15 : 0u) | (b_mn ? 1u << 16 : 0u) |
          ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
-}
-
-__device__ __forceinline__ void mma_tf32(uint32_t tmem_d, uint64_t ad, uint64_t bd, uint32_t idesc, uint32_t acc) {
-  asm volatile(
-      "{ .reg .pred p; setp.ne.b32 p, %4, 0; "
-      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p; }"
-      ::"r"(tmem_d), "l"(ad), "l"(bd), "r"(idesc), "r"(acc)
-      : "memory");
 }
 
 // A from TMEM (K-major: lane = row, one 32-bit column per k), B from shared memory
