@@ -386,6 +386,9 @@ struct TileClaim {
 // identically in every thread and sets each stage's mbarrier parity.
 template <int kTile4, int kStages>
 struct Stager {
+  // each of the engine's 512 threads applies kTile4 / 512 float4 of a staged tile: a tile size
+  // that is not a multiple of 512 would silently leave part of every tile unwritten
+  static_assert(kTile4 % 512 == 0, "kTile4 must be a multiple of the engine's 512 threads");
   float4* buf;      // [kStages][2][kTile4]
   uint64_t* bar;    // [kStages] full barriers
   int* stile;       // [kStages] tile held by each stage, -1 = none (shared memory)

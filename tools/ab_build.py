@@ -3,6 +3,11 @@ constants replaced in a copy of the sources (the product keeps no A/B macros);
 select one at run time with ADPSGD_LIB=build_ab/<name>/libadpsgd.so.
 
     python tools/ab_build.py chunk4 kClaimChunk=4  div2 kCrossDiv=2
+
+A variant is only as safe as the constant's own checks: run the parity tests with
+ADPSGD_LIB pointing at it before trusting its numbers (a kTile4 that is not a multiple
+of 512 once looked 24 % faster because it skipped a third of every tile's writes; the
+Stager now rejects it at compile time).
 """
 import os
 import re
